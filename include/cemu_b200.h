@@ -1,0 +1,200 @@
+/* cemu_b200.h -- C-ABI of the B200-native collective-emulation path.
+ *
+ * Drop-in boundary.  The reference (arxiv 2405.02969 "NeuronaBox", C++
+ * re-creation `cemu`) interposes on collective calls at
+ *   cemu::WorkerSession             proj/include/cemu/collective.hpp:50-131
+ *     allreduce_async / allgather_async / wait / close
+ * and the paper interposes on NCCL itself.  This header
+ * exports the NCCL shapes (nccl.h 2.27.3: ncclAllReduce :392-393,
+ * ncclAllGather :425-426, ncclReduceScatter :408-410, ncclBroadcast :379,
+ * ncclCommInitRank, ncclCommDestroy, ncclCommCount, ncclCommUserRank,
+ * ncclGetErrorString, ncclGroupStart/End) under a `cemu` prefix; the
+ * communicator's world is JobConfig.world_size (proj/include/cemu/
+ * config.hpp:43-62) and its rank must be one of JobConfig.real_ranks.  The
+ * job config comes from $CEMU_CONFIG (cemuCommInitRank) or explicit text
+ * (cemuCommInitRankConfig), in the reference's key=value format
+ * (proj/src/config.cpp:153-262).
+ *
+ * All collectives are stream-ordered and asynchronous: nothing blocks the
+ * host; completion is observed through the stream (this replaces
+ * WorkerSession::wait, collective.cpp:223-228).  Buffers are device memory
+ * owned by the caller.  Plain pointers and sizes only.
+ */
+#ifndef CEMU_B200_H_
+#define CEMU_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CEMU_B200_VERSION 10000
+
+struct CUstream_st;
+typedef struct CUstream_st* cemuStream_t; /* == cudaStream_t */
+
+/* Result codes: same values as ncclResult_t (nccl.h). */
+typedef enum {
+  cemuSuccess = 0,
+  cemuUnhandledCudaError = 1,
+  cemuSystemError = 2,
+  cemuInternalError = 3,
+  cemuInvalidArgument = 4,
+  cemuInvalidUsage = 5,
+  cemuRemoteError = 6,
+  cemuInProgress = 7
+} cemuResult_t;
+
+/* Datatypes: same values as ncclDataType_t. */
+typedef enum {
+  cemuInt8 = 0, cemuUint8 = 1, cemuInt32 = 2, cemuUint32 = 3,
+  cemuInt64 = 4, cemuUint64 = 5, cemuFloat16 = 6, cemuFloat32 = 7,
+  cemuFloat64 = 8, cemuBfloat16 = 9
+} cemuDataType_t;
+
+/* Reduction ops: same values as ncclRedOp_t.  The reference only sums
+ * (proj/src/reduce.cpp:7-19); anything but cemuSum is cemuInvalidArgument. */
+typedef enum { cemuSum = 0, cemuProd = 1, cemuMax = 2, cemuMin = 3, cemuAvg = 4 } cemuRedOp_t;
+
+#define CEMU_UNIQUE_ID_BYTES 128
+typedef struct { char internal[CEMU_UNIQUE_ID_BYTES]; } cemuUniqueId; /* == ncclUniqueId */
+
+typedef struct cemuComm* cemuComm_t;
+
+/* ------------------------------------------------------------------ */
+/* Communicator management (ncclGetUniqueId / ncclCommInitRank / ...)  */
+/* ------------------------------------------------------------------ */
+cemuResult_t cemuGetVersion(int* version);
+/* Wraps ncclGetUniqueId when the job places several real ranks on this box;
+ * any 128 bytes otherwise. */
+cemuResult_t cemuGetUniqueId(cemuUniqueId* uniqueId);
+/* ncclCommInitRank shape.  nranks must equal world_size of the config named
+ * by $CEMU_CONFIG; rank must be a real rank.  Device = the caller's current
+ * CUDA device. */
+cemuResult_t cemuCommInitRank(cemuComm_t* comm, int nranks, cemuUniqueId commId, int rank);
+/* Same with the config given as text (reference key=value format). */
+cemuResult_t cemuCommInitRankConfig(cemuComm_t* comm, const char* configText,
+                                    cemuUniqueId commId, int rank, int cudaDevice);
+cemuResult_t cemuCommDestroy(cemuComm_t comm);
+cemuResult_t cemuCommCount(const cemuComm_t comm, int* count);      /* world size */
+cemuResult_t cemuCommUserRank(const cemuComm_t comm, int* rank);    /* world rank */
+cemuResult_t cemuCommCuDevice(const cemuComm_t comm, int* device);
+const char* cemuGetErrorString(cemuResult_t result);
+/* Last error text of this thread (names the offending field/argument). */
+const char* cemuGetLastError(cemuComm_t comm);
+
+/* ------------------------------------------------------------------ */
+/* Collectives (NCCL signatures)                                        */
+/* ------------------------------------------------------------------ */
+/* replaces WorkerSession::allreduce_async (collective.cpp:213-216) */
+cemuResult_t cemuAllReduce(const void* sendbuff, void* recvbuff, size_t count,
+                           cemuDataType_t datatype, cemuRedOp_t op, cemuComm_t comm,
+                           cemuStream_t stream);
+/* replaces WorkerSession::allgather_async (collective.cpp:218-221) */
+cemuResult_t cemuAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
+                           cemuDataType_t datatype, cemuComm_t comm, cemuStream_t stream);
+/* NEW (absent from the reference, nccl.h:408-410 shape) */
+cemuResult_t cemuReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount,
+                               cemuDataType_t datatype, cemuRedOp_t op, cemuComm_t comm,
+                               cemuStream_t stream);
+/* NEW (absent from the reference, nccl.h:379 shape) */
+cemuResult_t cemuBroadcast(const void* sendbuff, void* recvbuff, size_t count,
+                           cemuDataType_t datatype, int root, cemuComm_t comm,
+                           cemuStream_t stream);
+cemuResult_t cemuGroupStart(void);
+cemuResult_t cemuGroupEnd(void);
+
+/* ------------------------------------------------------------------ */
+/* Emulation observability: the per-call schedule record                */
+/* ------------------------------------------------------------------ */
+/* Every collective call gets a sequential id (the reference's op_id,
+ * collective.cpp:200).  When the delay model is active the device writes
+ * the per-step release floors it evaluated (engine.cpp:36-42 semantics,
+ * integer us relative to the call start) and the %globaltimer instant each
+ * to-real step was released; read them after the stream is synchronized. */
+typedef struct {
+  uint64_t call_id;
+  int32_t coll;          /* 0 allreduce, 1 allgather, 2 reduce-scatter, 3 broadcast */
+  int32_t delay_active;  /* 0: no spin kernel was enqueued */
+  uint32_t steps;        /* K = to-real messages of the boundary */
+  uint32_t world;
+  uint64_t model_bytes;  /* m of the delay model */
+  int64_t model_latency_us;  /* max_j floor_j (host closed form, A14) */
+  int64_t t_start_ns;    /* device %globaltimer at the call's first kernel */
+  int64_t t_end_ns;      /* device %globaltimer when the last step released */
+  int64_t device_latency_us; /* max_j floor_j as evaluated on the device */
+} cemuCallRecord;
+
+cemuResult_t cemuCommLastCallId(cemuComm_t comm, uint64_t* callId);
+/* Copies the record (and up to `cap` floors / release times / offsets) of a
+ * call still held in the comm's record ring. Synchronous device read. */
+cemuResult_t cemuCommCallRecord(cemuComm_t comm, uint64_t callId, cemuCallRecord* rec,
+                                int64_t* floorsUs, int64_t* releaseNs, double* offsetsUs,
+                                size_t cap);
+
+/* ------------------------------------------------------------------ */
+/* Job config (proj/src/config.cpp) -- bit-compatible render + digest    */
+/* ------------------------------------------------------------------ */
+typedef struct cemuJobConfig* cemuJobConfig_t;
+/* parse_job_config (config.cpp:153-262) + validate (85-149).  On error
+ * returns cemuInvalidArgument and writes the ConfigError text (which names
+ * the offending field) into err. */
+cemuResult_t cemuConfigParse(const char* text, cemuJobConfig_t* cfg, char* err, size_t errcap);
+cemuResult_t cemuConfigLoad(const char* path, cemuJobConfig_t* cfg, char* err, size_t errcap);
+void cemuConfigFree(cemuJobConfig_t cfg);
+/* render_job_config (config.cpp:264-302): returns length, or -(needed). */
+int cemuConfigRender(cemuJobConfig_t cfg, char* out, size_t cap);
+/* config_digest (config.cpp:304-312): FNV-1a 64 of the render. */
+uint64_t cemuConfigDigest(cemuJobConfig_t cfg);
+uint32_t cemuConfigWorldSize(cemuJobConfig_t cfg);
+/* Writes up to cap real ranks (ascending); returns how many there are. */
+uint32_t cemuConfigRealRanks(cemuJobConfig_t cfg, uint32_t* out, size_t cap);
+
+/* ------------------------------------------------------------------ */
+/* Schedule + delay model (pure host functions, for parity checks)      */
+/* ------------------------------------------------------------------ */
+/* Delay model parameters: LinkParams + DelayModelParams (config.hpp:18-24,
+ * delay.hpp:16-29) plus the new cost-model algorithm selector. */
+typedef struct {
+  int32_t kind;   /* 0 none, 1 alpha_beta, 2 fixed   (config.hpp:27) */
+  int32_t algo;   /* 0 ring (reference), 1 tree, 2 hierarchical (new) */
+  double alpha_us, beta_us_per_byte, gamma_us_per_byte;
+  double fixed_us, inject_us;
+  uint32_t gpus_per_node;          /* hierarchical: ranks per node */
+  double intra_alpha_us, intra_beta_us_per_byte;  /* hierarchical intra links */
+} cemuDelayModel;
+
+/* dag.cpp:32-46 */
+uint64_t cemuChunkBytes(uint32_t n, uint64_t totalBytes, uint32_t elemSize, uint32_t chunk);
+uint64_t cemuChunkOffsetBytes(uint32_t n, uint64_t totalBytes, uint32_t elemSize, uint32_t chunk);
+/* dag.cpp:73-82; coll 0 allreduce, 1 allgather */
+uint32_t cemuPositions(int coll, uint32_t n);
+uint32_t cemuSendChunkAt(int coll, uint32_t n, uint32_t rank, uint32_t position);
+/* Closed-form project_boundary (dag.cpp:232-338) for one real rank, in the
+ * dump_boundary text format (dag.cpp:378-393).  Returns length or -needed. */
+int cemuBoundaryDump(int coll, uint32_t n, uint64_t bytes, uint32_t elemSize, uint32_t realRank,
+                     char* out, size_t cap);
+/* BoundaryDag::count(kToReal) for an arbitrary real set. */
+uint32_t cemuToRealCount(int coll, uint32_t n, const uint32_t* real, uint32_t nreal);
+/* delay.cpp:5-21 (ring) and the new tree / hierarchical forms. */
+double cemuModelTotalUs(const cemuDelayModel* m, int coll, uint32_t n, uint64_t bytes);
+/* delay.cpp:23-47 */
+int cemuReleaseOffsets(const cemuDelayModel* m, int coll, uint32_t n, uint64_t bytes,
+                       uint32_t k, double* out);
+/* engine.cpp:36-42 */
+int cemuReleaseFloors(const cemuDelayModel* m, int coll, uint32_t n, uint64_t bytes, uint32_t k,
+                      int64_t nowUs, int64_t* out);
+/* A14 closed form: completion - registration for an instantaneous real node */
+int64_t cemuCallLatencyUs(const cemuDelayModel* m, int coll, uint32_t n, uint64_t bytes,
+                          uint32_t k);
+
+/* Payload generator (see paper_2405_02969_b200/csrc/payload.cuh). */
+uint32_t cemuPayloadKey(uint64_t seed, uint32_t rank);
+uint32_t cemuPayloadWord(uint32_t key, uint64_t wordIndex);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CEMU_B200_H_ */

@@ -1,0 +1,687 @@
+/* oracle/cemu_oracle.c -- TEST INFRASTRUCTURE ONLY.  See cemu_oracle.h.
+ *
+ * Written as a plain sequential restatement: clarity over speed, one element
+ * at a time, no SIMD, no sharing with the product code under
+ * paper_2405_02969_b200/.  Built with -ffp-contract=off so every double
+ * expression rounds exactly in source order, as the reference's x86-64 build
+ * does (no FMA in the baseline ISA; proj/CMakeLists.txt sets no -march).
+ */
+#include "cemu_oracle.h"
+
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ======================================================================= */
+/* schedule                                                                */
+/* ======================================================================= */
+
+/* dag.cpp:32-39: element-granular floor split, last chunk takes remainder */
+uint64_t or_chunk_bytes(uint32_t n, uint64_t total, uint32_t elem, uint32_t c) {
+  uint64_t elems = total / elem;
+  uint64_t base = elems / n;
+  uint64_t rem = elems % n;
+  uint64_t mine = base;
+  if (c == n - 1) mine += rem;
+  return mine * elem;
+}
+
+/* dag.cpp:41-46 */
+uint64_t or_chunk_offset_bytes(uint32_t n, uint64_t total, uint32_t elem,
+                               uint32_t c) {
+  uint64_t elems = total / elem;
+  uint64_t base = elems / n;
+  return (uint64_t)c * base * elem;
+}
+
+/* dag.cpp:98: 2(n-1) positions for allreduce, n-1 for allgather.  The new
+ * reduce-scatter is the allreduce's first n-1 positions; broadcast is a
+ * pipelined ring of n-1 hops. */
+uint32_t or_positions(int coll, uint32_t n) {
+  if (coll == OR_ALLREDUCE) return 2 * (n - 1);
+  return n - 1;
+}
+
+static uint32_t mod_n(int64_t x, uint32_t n) {
+  int64_t r = x % (int64_t)n;
+  if (r < 0) r += n;
+  return (uint32_t)r;
+}
+
+/* dag.cpp:73-82 */
+uint32_t or_send_chunk_at(int coll, uint32_t n, uint32_t rank, uint32_t p) {
+  if (coll == OR_ALLGATHER) return mod_n((int64_t)rank - p, n);
+  if (p <= n - 2) return mod_n((int64_t)rank - p, n);
+  uint32_t t = p - (n - 1);
+  return mod_n((int64_t)rank + 1 - t, n);
+}
+
+/* Closed form of project_boundary (dag.cpp:232-338) for a single real rank
+ * R.  Crossing messages per position p: from-real R -> R+1 and to-real
+ * R-1 -> R.  Canonical order sorts by (src, dst) within a step
+ * (dag.cpp:291-294).  Edges of the transitive reduction:
+ *   to-real@p  -> from-real@p+1        (the real node forwards what it got)
+ *   from-real@p -> to-real@p+n-1       (allreduce: the chunk returns after
+ *                                        n-1 hops through the emulated ring)
+ * Verified against the reference's O(n^3) projection in the tests. */
+int or_dump_boundary_single_real(int coll, uint32_t n, uint64_t bytes,
+                                 uint32_t elem, uint32_t R, char* out,
+                                 size_t cap) {
+  uint32_t P = or_positions(coll, n);
+  uint32_t pred = (R + n - 1) % n, succ = (R + 1) % n;
+  /* from-real first iff its src (R) sorts before the to-real src (R-1) */
+  int fr_first = R < pred;
+  size_t len = 0;
+  char line[256];
+  char* buf = (char*)malloc((size_t)P * 2 * 96 + (size_t)P * 2 * 32 + 256);
+  if (!buf) return -1;
+  len += (size_t)sprintf(buf + len, "# boundary %s n=%u side=emulated\n",
+                         coll == OR_ALLREDUCE ? "allreduce" : "allgather", n);
+  for (uint32_t p = 0; p < P; ++p) {
+    for (int half = 0; half < 2; ++half) {
+      int is_fr = (half == 0) == fr_first;
+      uint32_t src = is_fr ? R : pred;
+      uint32_t dst = is_fr ? succ : R;
+      uint32_t chunk = or_send_chunk_at(coll, n, src, p);
+      uint64_t size = coll == OR_ALLREDUCE
+                          ? or_chunk_bytes(n, bytes, elem, chunk)
+                          : bytes;
+      int w = sprintf(line, "0 %s %u %u %u %u %llu\n",
+                      is_fr ? "from_real:recv" : "to_real:send", p, src, dst,
+                      chunk, (unsigned long long)size);
+      memcpy(buf + len, line, (size_t)w);
+      len += (size_t)w;
+    }
+  }
+  len += (size_t)sprintf(buf + len, "edges\n");
+  /* vertex index of (dir, p) */
+#define FR(p) (2 * (p) + (fr_first ? 0 : 1))
+#define TR(p) (2 * (p) + (fr_first ? 1 : 0))
+  /* collect and sort edges (u, v) lexicographically */
+  uint32_t ne = 0;
+  uint32_t* eu = (uint32_t*)malloc(sizeof(uint32_t) * 2 * P + 8);
+  uint32_t* ev = (uint32_t*)malloc(sizeof(uint32_t) * 2 * P + 8);
+  for (uint32_t p = 0; p + 1 < P; ++p) {
+    eu[ne] = TR(p);
+    ev[ne] = FR(p + 1);
+    ++ne;
+  }
+  if (coll == OR_ALLREDUCE) {
+    for (uint32_t p = 0; p + n - 1 < P; ++p) {
+      eu[ne] = FR(p);
+      ev[ne] = TR(p + n - 1);
+      ++ne;
+    }
+  }
+#undef FR
+#undef TR
+  for (uint32_t i = 1; i < ne; ++i) { /* insertion sort, small */
+    uint32_t u = eu[i], v = ev[i];
+    uint32_t j = i;
+    while (j > 0 && (eu[j - 1] > u || (eu[j - 1] == u && ev[j - 1] > v))) {
+      eu[j] = eu[j - 1];
+      ev[j] = ev[j - 1];
+      --j;
+    }
+    eu[j] = u;
+    ev[j] = v;
+  }
+  for (uint32_t i = 0; i < ne; ++i) {
+    len += (size_t)sprintf(buf + len, "%u %u\n", eu[i], ev[i]);
+  }
+  free(eu);
+  free(ev);
+  int ret;
+  if (len + 1 > cap) {
+    ret = -(int)(len + 1);
+  } else {
+    memcpy(out, buf, len + 1);
+    ret = (int)len;
+  }
+  free(buf);
+  return ret;
+}
+
+/* Crossing to-real messages: one per position for every ring edge v -> r
+ * with v emulated and r real (build_ring_dag edges r -> r+1). */
+uint32_t or_to_real_count(int coll, uint32_t n, const uint32_t* real,
+                          uint32_t nreal) {
+  uint32_t edges = 0;
+  for (uint32_t v = 0; v < n; ++v) {
+    uint32_t r = (v + 1) % n;
+    int v_real = 0, r_real = 0;
+    for (uint32_t i = 0; i < nreal; ++i) {
+      if (real[i] == v) v_real = 1;
+      if (real[i] == r) r_real = 1;
+    }
+    if (!v_real && r_real) ++edges;
+  }
+  return edges * or_positions(coll, n);
+}
+
+/* ======================================================================= */
+/* delay model                                                             */
+/* ======================================================================= */
+
+/* delay.cpp:5-13, same expression and operation order */
+double or_ring_allreduce_delay_us(uint32_t n, uint64_t bytes, double a,
+                                  double b, double g) {
+  const double steps = 2.0 * (n - 1);
+  const double frac = (double)(n - 1) / n;
+  const double m = (double)bytes;
+  return steps * a + 2.0 * frac * m * b + frac * m * g;
+}
+
+/* delay.cpp:15-21 */
+double or_ring_allgather_delay_us(uint32_t n, uint64_t bytes, double a,
+                                  double b) {
+  const double steps = (double)(n - 1);
+  const double m = (double)bytes;
+  return steps * a + steps * m * b;
+}
+
+/* NEW (parity unpinned): ring reduce-scatter = the first n-1 allreduce steps
+ * over total bytes m = n * recv bytes. */
+static double ring_reducescatter_us(uint32_t n, uint64_t bytes, double a,
+                                    double b, double g) {
+  const double steps = (double)(n - 1);
+  const double frac = (double)(n - 1) / n;
+  const double m = (double)bytes;
+  return steps * a + frac * m * b + frac * m * g;
+}
+
+/* NEW: pipelined ring broadcast, n-1 hops of latency, one pass of bytes. */
+static double ring_broadcast_us(uint32_t n, uint64_t bytes, double a,
+                                double b) {
+  const double steps = (double)(n - 1);
+  const double m = (double)bytes;
+  return steps * a + m * b;
+}
+
+static uint32_t ceil_log2(uint32_t n) {
+  uint32_t d = 0;
+  while ((1u << d) < n) ++d;
+  return d;
+}
+
+/* NEW: pipelined (double) binary tree, depth d = ceil(log2 n). */
+static double tree_allreduce_us(uint32_t n, uint64_t bytes, double a, double b,
+                                double g) {
+  const double steps = 2.0 * ceil_log2(n);
+  const double m = (double)bytes;
+  return steps * a + 2.0 * m * b + m * g;
+}
+
+static double tree_broadcast_us(uint32_t n, uint64_t bytes, double a,
+                                double b) {
+  const double steps = (double)ceil_log2(n);
+  const double m = (double)bytes;
+  return steps * a + m * b;
+}
+
+/* NEW: hierarchical ring over N = n/G nodes of G ranks.  Allreduce = intra
+ * reduce-scatter, inter ring allreduce of m/G, intra allgather. */
+static double hier_us(const or_delay_model* M, int coll, uint32_t n,
+                      uint64_t bytes) {
+  const uint32_t G = M->gpus_per_node ? M->gpus_per_node : 1;
+  const uint32_t N = n / G;
+  const double ai = M->intra_alpha_us, bi = M->intra_beta_us_per_byte;
+  const double ae = M->alpha_us, be = M->beta_us_per_byte;
+  const double g = M->gamma_us_per_byte;
+  const double m = (double)bytes;
+  const double gm1 = (double)(G - 1);
+  const double fi = (double)(G - 1) / G;
+  const double nm1 = (double)(N - 1);
+  const double fe = (double)(N - 1) / N;
+  const double shard = m / G;
+  switch (coll) {
+    case OR_ALLREDUCE: {
+      double intra_rs = gm1 * ai + fi * m * bi + fi * m * g;
+      double inter_ar = 2.0 * nm1 * ae + 2.0 * fe * shard * be + fe * shard * g;
+      double intra_ag = gm1 * ai + fi * m * bi;
+      return intra_rs + inter_ar + intra_ag;
+    }
+    case OR_ALLGATHER: { /* bytes = per-rank block */
+      double intra_ag = gm1 * ai + gm1 * m * bi;
+      double inter_ag = nm1 * ae + nm1 * (G * m) * be;
+      return intra_ag + inter_ag;
+    }
+    case OR_REDUCESCATTER: {
+      double intra_rs = gm1 * ai + fi * m * bi + fi * m * g;
+      double inter_rs = nm1 * ae + fe * shard * be + fe * shard * g;
+      return intra_rs + inter_rs;
+    }
+    default: { /* broadcast */
+      double inter = nm1 * ae + m * be;
+      double intra = gm1 * ai + m * bi;
+      return inter + intra;
+    }
+  }
+}
+
+double or_model_total_us(const or_delay_model* M, int coll, uint32_t n,
+                         uint64_t bytes) {
+  if (M->algo == OR_ALGO_HIER) return hier_us(M, coll, n, bytes);
+  if (M->algo == OR_ALGO_TREE) {
+    if (coll == OR_ALLREDUCE)
+      return tree_allreduce_us(n, bytes, M->alpha_us, M->beta_us_per_byte,
+                               M->gamma_us_per_byte);
+    if (coll == OR_BROADCAST)
+      return tree_broadcast_us(n, bytes, M->alpha_us, M->beta_us_per_byte);
+    /* allgather / reduce-scatter have no tree form: ring, as NCCL does */
+  }
+  switch (coll) {
+    case OR_ALLREDUCE:
+      return or_ring_allreduce_delay_us(n, bytes, M->alpha_us,
+                                        M->beta_us_per_byte,
+                                        M->gamma_us_per_byte);
+    case OR_ALLGATHER:
+      return or_ring_allgather_delay_us(n, bytes, M->alpha_us,
+                                        M->beta_us_per_byte);
+    case OR_REDUCESCATTER:
+      return ring_reducescatter_us(n, bytes, M->alpha_us, M->beta_us_per_byte,
+                                   M->gamma_us_per_byte);
+    default:
+      return ring_broadcast_us(n, bytes, M->alpha_us, M->beta_us_per_byte);
+  }
+}
+
+/* delay.cpp:23-47: none -> 0, fixed -> fixed_us, alpha_beta -> total*(j+1)/K,
+ * then offsets[0] += inject_us. */
+int or_release_offsets(const or_delay_model* M, int coll, uint32_t n,
+                       uint64_t bytes, uint32_t k, double* out) {
+  if (k == 0) return 0;
+  if (M->kind == OR_DELAY_ALPHA_BETA) {
+    const double total = or_model_total_us(M, coll, n, bytes);
+    for (uint32_t j = 0; j < k; ++j) {
+      out[j] = total * (double)(j + 1) / (double)k;
+    }
+  } else {
+    for (uint32_t j = 0; j < k; ++j) {
+      out[j] = M->kind == OR_DELAY_FIXED ? M->fixed_us : 0.0;
+    }
+  }
+  out[0] += M->inject_us;
+  return (int)k;
+}
+
+/* engine.cpp:36-42: now + llround(offset) */
+int or_release_floors(const or_delay_model* M, int coll, uint32_t n,
+                      uint64_t bytes, uint32_t k, int64_t now_us,
+                      int64_t* out) {
+  double* off = (double*)malloc(sizeof(double) * (k ? k : 1));
+  or_release_offsets(M, coll, n, bytes, k, off);
+  for (uint32_t j = 0; j < k; ++j) out[j] = now_us + (int64_t)llround(off[j]);
+  free(off);
+  return (int)k;
+}
+
+/* A14: with an instantaneous real node, head-of-line release makes the call
+ * complete at the largest floor (engine.cpp:58-70). */
+int64_t or_call_latency_us(const or_delay_model* M, int coll, uint32_t n,
+                           uint64_t bytes, uint32_t k) {
+  int64_t* fl = (int64_t*)malloc(sizeof(int64_t) * (k ? k : 1));
+  or_release_floors(M, coll, n, bytes, k, 0, fl);
+  int64_t best = 0;
+  for (uint32_t j = 0; j < k; ++j) {
+    if (fl[j] > best) best = fl[j];
+  }
+  free(fl);
+  return best;
+}
+
+/* ======================================================================= */
+/* payload generator                                                       */
+/* ======================================================================= */
+
+/* Per-rank key: the splitmix64 finalizer `mix` of tools/cemu_coll.cpp:22-31
+ * (the reference's own seeded per-rank input precedent) with trial 0, folded
+ * to 32 bits. */
+uint32_t or_payload_key(uint64_t seed, uint32_t rank) {
+  uint64_t h = seed ^ (0ull * 0x9e3779b97f4a7c15ull) ^
+               ((uint64_t)rank * 0xbf58476d1ce4e5b9ull);
+  h ^= h >> 30;
+  h *= 0xbf58476d1ce4e5b9ull;
+  h ^= h >> 27;
+  h *= 0x94d049bb133111ebull;
+  h ^= h >> 31;
+  return (uint32_t)(h ^ (h >> 32));
+}
+
+/* Counter-based 32-bit word j of a rank's payload stream: a Weyl counter
+ * XOR the key, then two multiply/xorshift rounds. */
+uint32_t or_payload_word(uint32_t key, uint64_t j) {
+  uint32_t ctr = (uint32_t)j * 0x9E3779B9u;
+  ctr ^= (uint32_t)(j >> 32) * 0x85EBCA77u;
+  uint32_t x = key ^ ctr;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  x *= 0x846CA68Bu;
+  x ^= x >> 16;
+  return x;
+}
+
+static uint32_t pbyte(uint32_t key, uint64_t e) {
+  return (or_payload_word(key, e >> 2) >> (8 * (e & 3))) & 0xFFu;
+}
+
+/* float payload element: (byte - 128) * 2^-7, exact in every float type */
+static int pdyadic(uint32_t key, uint64_t e) { return (int)pbyte(key, e) - 128; }
+
+/* ---- half / bfloat16 helpers ---- */
+uint16_t or_f32_to_bf16(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu)) return 0x7FFF;
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+float or_bf16_to_f32(uint16_t h) {
+  uint32_t u = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+uint16_t or_f32_to_f16(float f) {
+  _Float16 h = (_Float16)f;
+  uint16_t u;
+  memcpy(&u, &h, 2);
+  return u;
+}
+float or_f16_to_f32(uint16_t u) {
+  _Float16 h;
+  memcpy(&h, &u, 2);
+  return (float)h;
+}
+
+static size_t dsize(int dtype) {
+  switch (dtype) {
+    case OR_INT8: case OR_UINT8: return 1;
+    case OR_FLOAT16: case OR_BFLOAT16: return 2;
+    case OR_INT32: case OR_UINT32: case OR_FLOAT32: return 4;
+    default: return 8;
+  }
+}
+
+void or_payload(int dtype, uint32_t key, uint64_t first, uint64_t count,
+                void* out) {
+  for (uint64_t i = 0; i < count; ++i) {
+    uint64_t e = first + i;
+    switch (dtype) {
+      case OR_INT8: case OR_UINT8:
+        ((uint8_t*)out)[i] = (uint8_t)pbyte(key, e);
+        break;
+      case OR_INT32: case OR_UINT32:
+        ((uint32_t*)out)[i] = or_payload_word(key, e);
+        break;
+      case OR_INT64: case OR_UINT64:
+        ((uint64_t*)out)[i] = (uint64_t)or_payload_word(key, 2 * e) |
+                              ((uint64_t)or_payload_word(key, 2 * e + 1) << 32);
+        break;
+      case OR_FLOAT32:
+        ((float*)out)[i] = (float)pdyadic(key, e) * 0.0078125f;
+        break;
+      case OR_FLOAT64:
+        ((double*)out)[i] = (double)pdyadic(key, e) * 0.0078125;
+        break;
+      case OR_FLOAT16:
+        ((uint16_t*)out)[i] = or_f32_to_f16((float)pdyadic(key, e) * 0.0078125f);
+        break;
+      case OR_BFLOAT16:
+        ((uint16_t*)out)[i] = or_f32_to_bf16((float)pdyadic(key, e) * 0.0078125f);
+        break;
+    }
+  }
+}
+
+/* ======================================================================= */
+/* collectives                                                             */
+/* ======================================================================= */
+
+static int is_real(const uint32_t* real, uint32_t nreal, uint32_t r) {
+  for (uint32_t i = 0; i < nreal; ++i) {
+    if (real[i] == r) return 1;
+  }
+  return 0;
+}
+
+static int real_index(const uint32_t* real, uint32_t nreal, uint32_t r) {
+  for (uint32_t i = 0; i < nreal; ++i) {
+    if (real[i] == r) return (int)i;
+  }
+  return -1;
+}
+
+/* x + y in the dtype's own arithmetic (the real part's fold) */
+static void add_elem(int dtype, void* acc, const void* src, uint64_t i) {
+  switch (dtype) {
+    case OR_INT8: case OR_UINT8:
+      ((uint8_t*)acc)[i] = (uint8_t)(((uint8_t*)acc)[i] + ((const uint8_t*)src)[i]);
+      break;
+    case OR_INT32: case OR_UINT32:
+      ((uint32_t*)acc)[i] += ((const uint32_t*)src)[i];
+      break;
+    case OR_INT64: case OR_UINT64:
+      ((uint64_t*)acc)[i] += ((const uint64_t*)src)[i];
+      break;
+    case OR_FLOAT32:
+      ((float*)acc)[i] = ((float*)acc)[i] + ((const float*)src)[i];
+      break;
+    case OR_FLOAT64:
+      ((double*)acc)[i] = ((double*)acc)[i] + ((const double*)src)[i];
+      break;
+    case OR_FLOAT16:
+      ((uint16_t*)acc)[i] = or_f32_to_f16(or_f16_to_f32(((uint16_t*)acc)[i]) +
+                                          or_f16_to_f32(((const uint16_t*)src)[i]));
+      break;
+    case OR_BFLOAT16:
+      ((uint16_t*)acc)[i] = or_f32_to_bf16(or_bf16_to_f32(((uint16_t*)acc)[i]) +
+                                           or_bf16_to_f32(((const uint16_t*)src)[i]));
+      break;
+  }
+}
+
+/* out[i] = x[i] (+) Sum over emulated ranks v (ascending) of payload_v(first+i).
+ * Float types: S = exact integer sum of (byte-128); result rounds once:
+ * T(fp32(x) + S * 2^-7).  Integers wrap. */
+static void add_virtual(int dtype, uint32_t W, const uint32_t* real,
+                        uint32_t nreal, uint64_t seed, const void* x,
+                        void* out, uint64_t first, uint64_t count) {
+  uint32_t nv = 0;
+  uint32_t* keys = (uint32_t*)malloc(sizeof(uint32_t) * W);
+  for (uint32_t r = 0; r < W; ++r) {
+    if (!is_real(real, nreal, r)) keys[nv++] = or_payload_key(seed, r);
+  }
+  for (uint64_t i = 0; i < count; ++i) {
+    uint64_t e = first + i;
+    switch (dtype) {
+      case OR_INT8: case OR_UINT8: {
+        uint8_t acc = ((const uint8_t*)x)[i];
+        for (uint32_t v = 0; v < nv; ++v) acc = (uint8_t)(acc + pbyte(keys[v], e));
+        ((uint8_t*)out)[i] = acc;
+        break;
+      }
+      case OR_INT32: case OR_UINT32: {
+        uint32_t acc = ((const uint32_t*)x)[i];
+        for (uint32_t v = 0; v < nv; ++v) acc += or_payload_word(keys[v], e);
+        ((uint32_t*)out)[i] = acc;
+        break;
+      }
+      case OR_INT64: case OR_UINT64: {
+        uint64_t acc = ((const uint64_t*)x)[i];
+        for (uint32_t v = 0; v < nv; ++v) {
+          acc += (uint64_t)or_payload_word(keys[v], 2 * e) |
+                 ((uint64_t)or_payload_word(keys[v], 2 * e + 1) << 32);
+        }
+        ((uint64_t*)out)[i] = acc;
+        break;
+      }
+      default: {
+        int64_t S = 0;
+        for (uint32_t v = 0; v < nv; ++v) S += pdyadic(keys[v], e);
+        if (dtype == OR_FLOAT64) {
+          ((double*)out)[i] = ((const double*)x)[i] + (double)S * 0.0078125;
+        } else {
+          const float sv = (float)S * 0.0078125f;
+          if (dtype == OR_FLOAT32) {
+            ((float*)out)[i] = ((const float*)x)[i] + sv;
+          } else if (dtype == OR_FLOAT16) {
+            ((uint16_t*)out)[i] =
+                or_f32_to_f16(or_f16_to_f32(((const uint16_t*)x)[i]) + sv);
+          } else {
+            ((uint16_t*)out)[i] =
+                or_f32_to_bf16(or_bf16_to_f32(((const uint16_t*)x)[i]) + sv);
+          }
+        }
+        break;
+      }
+    }
+  }
+  free(keys);
+}
+
+/* Sum of the real ranks' buffers over elements [first, first+count). */
+static void real_sum(int dtype, uint32_t nreal, const void* const* sends,
+                     uint64_t first, uint64_t count, void* out) {
+  size_t es = dsize(dtype);
+  memcpy(out, (const uint8_t*)sends[0] + first * es, count * es);
+  for (uint32_t i = 1; i < nreal; ++i) {
+    const uint8_t* s = (const uint8_t*)sends[i] + first * es;
+    for (uint64_t k = 0; k < count; ++k) add_elem(dtype, out, s, k);
+  }
+}
+
+int or_allreduce(int dtype, int mode, uint32_t W, const uint32_t* real,
+                 uint32_t nreal, uint32_t me, uint64_t seed,
+                 const void* const* sends, void* recv, uint64_t count) {
+  size_t es = dsize(dtype);
+  int mi = real_index(real, nreal, me);
+  if (mi < 0) return -1;
+  if (mode == OR_PAYLOAD_ZERO) {
+    /* A10: every emulated reply is zeros; with the reduce-scatter running
+     * first the real rank keeps chunk (me+1) mod W, every gathered chunk is
+     * overwritten with zeros (test_transport.cpp:129-167). */
+    if (nreal != 1) return -2;
+    uint64_t total = count * es;
+    memset(recv, 0, total);
+    uint32_t keep = (me + 1) % W;
+    uint64_t off = or_chunk_offset_bytes(W, total, (uint32_t)es, keep);
+    uint64_t len = or_chunk_bytes(W, total, (uint32_t)es, keep);
+    memcpy((uint8_t*)recv + off, (const uint8_t*)sends[0] + off, len);
+    return 0;
+  }
+  void* x = malloc(count * es + 1);
+  real_sum(dtype, nreal, sends, 0, count, x);
+  add_virtual(dtype, W, real, nreal, seed, x, recv, 0, count);
+  free(x);
+  return 0;
+}
+
+int or_allgather(int dtype, int mode, uint32_t W, const uint32_t* real,
+                 uint32_t nreal, uint32_t me, uint64_t seed,
+                 const void* const* sends, void* recv, uint64_t sendcount) {
+  size_t es = dsize(dtype);
+  if (real_index(real, nreal, me) < 0) return -1;
+  if (mode == OR_PAYLOAD_ZERO && nreal != 1) return -2;
+  for (uint32_t b = 0; b < W; ++b) {
+    uint8_t* dst = (uint8_t*)recv + (uint64_t)b * sendcount * es;
+    int ri = real_index(real, nreal, b);
+    if (ri >= 0) {
+      memcpy(dst, sends[ri], sendcount * es);
+    } else if (mode == OR_PAYLOAD_ZERO) {
+      memset(dst, 0, sendcount * es);  /* test_transport.cpp:169-182 */
+    } else {
+      or_payload(dtype, or_payload_key(seed, b), 0, sendcount, dst);
+    }
+  }
+  return 0;
+}
+
+int or_reducescatter(int dtype, int mode, uint32_t W, const uint32_t* real,
+                     uint32_t nreal, uint32_t me, uint64_t seed,
+                     const void* const* sends, void* recv, uint64_t recvcount) {
+  size_t es = dsize(dtype);
+  int mi = real_index(real, nreal, me);
+  if (mi < 0) return -1;
+  uint64_t first = (uint64_t)me * recvcount;
+  if (mode == OR_PAYLOAD_ZERO) {
+    if (nreal != 1) return -2;
+    memcpy(recv, (const uint8_t*)sends[0] + first * es, recvcount * es);
+    return 0;
+  }
+  void* x = malloc(recvcount * es + 1);
+  real_sum(dtype, nreal, sends, first, recvcount, x);
+  add_virtual(dtype, W, real, nreal, seed, x, recv, first, recvcount);
+  free(x);
+  return 0;
+}
+
+int or_broadcast(int dtype, int mode, uint32_t W, const uint32_t* real,
+                 uint32_t nreal, uint32_t me, uint32_t root, uint64_t seed,
+                 const void* root_send, void* recv, uint64_t count) {
+  size_t es = dsize(dtype);
+  (void)W;
+  if (real_index(real, nreal, me) < 0) return -1;
+  if (is_real(real, nreal, root)) {
+    memcpy(recv, root_send, count * es);
+  } else if (mode == OR_PAYLOAD_ZERO) {
+    if (nreal != 1) return -2;
+    memset(recv, 0, count * es);
+  } else {
+    or_payload(dtype, or_payload_key(seed, root), 0, count, recv);
+  }
+  return 0;
+}
+
+/* proj/tests/oracles.hpp:43-101 restated for allreduce: lockstep positions,
+ * every rank snapshots the chunk it sends, then every rank folds
+ * (dst = dst + incoming) or stores the chunk it receives. */
+int or_ring_execute_allreduce(int dtype, uint32_t n, const void* const* inputs,
+                              uint64_t count, uint32_t me, void* out) {
+  if (dtype != OR_INT32 && dtype != OR_FLOAT32 && dtype != OR_UINT32) return -1;
+  const uint32_t es = 4;
+  const uint64_t total = count * es;
+  uint8_t** bufs = (uint8_t**)malloc(sizeof(uint8_t*) * n);
+  uint8_t** wire = (uint8_t**)malloc(sizeof(uint8_t*) * n);
+  for (uint32_t r = 0; r < n; ++r) {
+    bufs[r] = (uint8_t*)malloc(total + 1);
+    memcpy(bufs[r], inputs[r], total);
+    wire[r] = (uint8_t*)malloc(total + 1);
+  }
+  const uint32_t P = 2 * (n - 1);
+  for (uint32_t p = 0; p < P; ++p) {
+    for (uint32_t r = 0; r < n; ++r) {
+      uint32_t c = or_send_chunk_at(OR_ALLREDUCE, n, r, p);
+      memcpy(wire[r], bufs[r] + or_chunk_offset_bytes(n, total, es, c),
+             or_chunk_bytes(n, total, es, c));
+    }
+    for (uint32_t r = 0; r < n; ++r) {
+      uint32_t src = (r + n - 1) % n;
+      uint32_t c = or_send_chunk_at(OR_ALLREDUCE, n, src, p);
+      uint64_t off = or_chunk_offset_bytes(n, total, es, c);
+      uint64_t len = or_chunk_bytes(n, total, es, c) / es;
+      if (p <= n - 2) {
+        for (uint64_t i = 0; i < len; ++i) {
+          if (dtype == OR_FLOAT32) {
+            float* d = (float*)(bufs[r] + off);
+            d[i] = d[i] + ((float*)wire[src])[i];
+          } else {
+            uint32_t* d = (uint32_t*)(bufs[r] + off);
+            d[i] = d[i] + ((uint32_t*)wire[src])[i];
+          }
+        }
+      } else {
+        memcpy(bufs[r] + off, wire[src], len * es);
+      }
+    }
+  }
+  memcpy(out, bufs[me], total);
+  for (uint32_t r = 0; r < n; ++r) {
+    free(bufs[r]);
+    free(wire[r]);
+  }
+  free(bufs);
+  free(wire);
+  return 0;
+}

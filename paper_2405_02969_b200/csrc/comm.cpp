@@ -1,0 +1,686 @@
+// comm.cpp -- the NCCL-shaped communicator of the emulated world.
+//
+// One cemuComm per real rank (one process per GPU).  Its world is the job's
+// world_size; the real ranks of the job are the GPUs on this box and share
+// an inner NCCL communicator (only created when there are several).  Every
+// collective splits into
+//   real part      NCCL over NVLink among the local real GPUs (k > 1 only)
+//   emulated part  sm_100a kernels synthesising the W-k emulated peers'
+//                  payloads and folding them in (kernels.cu)
+//   network delay  the device-evaluated alpha-beta model released on
+//                  %globaltimer by a spin kernel on the same stream
+// replacing WorkerSession::run_op's TCP ring (proj/src/collective.cpp:
+// 268-355) and the emulator process (proj/src/emulator.cpp:59-272).
+//
+// Stream-ordered, asynchronous; the host never blocks.  Argument and usage
+// errors map to cemuInvalidArgument / cemuInvalidUsage with a message that
+// names the offending argument (cemuGetLastError), as the reference's
+// TransportError/ConfigError texts do (collective.cpp:190-205).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "cemu_b200.h"
+#include "config.hpp"
+#include "delay_math.cuh"
+#include "kernels.hpp"
+#include "payload.cuh"
+#include "schedule.hpp"
+
+using namespace cemu_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+cemuResult_t fail(cemuResult_t code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+// ---- NCCL, loaded on demand (only jobs with several real GPUs need it) ----
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int,
+                         ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+std::mutex g_nccl_mu;
+Nccl g_nccl;
+bool g_nccl_tried = false;
+
+const Nccl* nccl() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (!g_nccl_tried) {
+    g_nccl_tried = true;
+    const char* env = std::getenv("CEMU_NCCL_LIB");
+    // an already-loaded libnccl.so.2 (e.g. torch's) is reused by soname
+    void* h = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("/usr/lib/x86_64-linux-gnu/libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      Nccl n;
+      n.h = h;
+#define CEMU_SYM(field, name) n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name))
+      CEMU_SYM(GetUniqueId, "ncclGetUniqueId");
+      CEMU_SYM(CommInitRank, "ncclCommInitRank");
+      CEMU_SYM(CommDestroy, "ncclCommDestroy");
+      CEMU_SYM(AllReduce, "ncclAllReduce");
+      CEMU_SYM(AllGather, "ncclAllGather");
+      CEMU_SYM(ReduceScatter, "ncclReduceScatter");
+      CEMU_SYM(Broadcast, "ncclBroadcast");
+      CEMU_SYM(Reduce, "ncclReduce");
+      CEMU_SYM(GroupStart, "ncclGroupStart");
+      CEMU_SYM(GroupEnd, "ncclGroupEnd");
+      CEMU_SYM(GetErrorString, "ncclGetErrorString");
+#undef CEMU_SYM
+      if (n.GetUniqueId && n.CommInitRank && n.AllReduce && n.AllGather && n.ReduceScatter &&
+          n.Broadcast && n.Reduce && n.GroupStart && n.GroupEnd && n.CommDestroy) {
+        g_nccl = n;
+      }
+    }
+  }
+  return g_nccl.h ? &g_nccl : nullptr;
+}
+
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case cemuInt8: case cemuUint8: return 1;
+    case cemuFloat16: case cemuBfloat16: return 2;
+    case cemuInt32: case cemuUint32: case cemuFloat32: return 4;
+    case cemuInt64: case cemuUint64: case cemuFloat64: return 8;
+    default: return 0;
+  }
+}
+
+// Deferred calls between cemuGroupStart/End (NCCL group semantics: nothing
+// needs to start before ncclGroupEnd).  The composite ops chain NCCL calls
+// with our kernels, so they are replayed in order at GroupEnd.
+thread_local int g_group_depth = 0;
+thread_local std::vector<std::function<cemuResult_t()>> g_group_ops;
+
+}  // namespace
+
+struct cemuComm {
+  JobConfig cfg;
+  uint32_t W = 0, rank = 0;
+  int device = 0;
+  std::vector<uint32_t> real;  // ascending world ranks of the real GPUs
+  uint32_t k = 1, li = 0;      // number of real ranks, my index among them
+  bool contiguous = true;      // real ranks form one block [real[0], real[0]+k)
+  cemuDelayModel delay{};
+  bool delay_active = false;
+  uint64_t seed = 1;
+  PayloadMode mode = PayloadMode::kHash;
+  std::vector<uint32_t> virt;  // emulated ranks, ascending
+  uint32_t* d_virt_keys = nullptr;
+  uint32_t* d_virt_ranks = nullptr;
+  // per-call record ring
+  static constexpr uint32_t kSlots = 64;
+  uint32_t kmax = 1;
+  int64_t* d_slots = nullptr;
+  struct Meta {
+    uint64_t call_id = ~0ull;
+    int32_t coll = 0;
+    bool delay = false;
+    uint32_t k = 0;
+    uint64_t bytes = 0;
+    int64_t latency = 0;
+  } meta[kSlots];
+  uint64_t calls = 0;
+  ncclComm_t inner = nullptr;
+  uint64_t launches = 0;
+};
+
+namespace {
+
+struct Call {
+  cemuComm* c;
+  int64_t* slot = nullptr;
+  bool stamped = false;
+  int launches = 0;
+  cudaStream_t s;
+
+  Call(cemuComm* comm, int coll, uint64_t model_bytes, cudaStream_t stream) : c(comm), s(stream) {
+    const uint64_t id = c->calls++;
+    const uint32_t i = static_cast<uint32_t>(id % cemuComm::kSlots);
+    auto& m = c->meta[i];
+    m.call_id = id;
+    m.coll = coll;
+    m.delay = c->delay_active;
+    m.k = to_real_count(coll, c->W, c->real);
+    m.bytes = model_bytes;
+    m.latency = c->delay_active ? call_latency_us(c->delay, coll, c->W, model_bytes, m.k) : 0;
+    if (c->delay_active) slot = c->d_slots + i * slot_words(c->kmax);
+  }
+  // pointer the first kernel of the call writes t_start into (or null)
+  int64_t* take_stamp() {
+    if (!slot || stamped) return nullptr;
+    stamped = true;
+    return slot;
+  }
+  cudaError_t stamp_now() {
+    if (!slot || stamped) return cudaSuccess;
+    stamped = true;
+    return launch_stamp(slot, s, &launches);
+  }
+  cudaError_t finish(int coll) {
+    c->launches += launches;
+    if (!slot) return cudaSuccess;
+    const auto& m = c->meta[static_cast<uint32_t>((c->calls - 1) % cemuComm::kSlots)];
+    DelayLaunch d;
+    d.model = c->delay;
+    d.coll = coll;
+    d.n = c->W;
+    d.bytes = m.bytes;
+    d.k = m.k;
+    d.kmax = c->kmax;
+    d.self_stamp = stamped ? 0 : 1;
+    int l = 0;
+    const cudaError_t e = launch_delay_spin(d, slot, s, &l);
+    c->launches += l;
+    return e;
+  }
+};
+
+#define CUDA_OK(expr)                                                                   \
+  do {                                                                                  \
+    const cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(cemuUnhandledCudaError, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NCCL_OK(expr)                                                                       \
+  do {                                                                                      \
+    const ncclResult_t r_ = (expr);                                                         \
+    if (r_ != ncclSuccess)                                                                  \
+      return fail(static_cast<cemuResult_t>(r_),                                            \
+                  std::string(#expr) + ": " +                                               \
+                      (nccl()->GetErrorString ? nccl()->GetErrorString(r_) : "nccl error")); \
+  } while (0)
+
+cemuResult_t check_common(cemuComm* c, int dt, const char* what) {
+  if (!c) return fail(cemuInvalidArgument, std::string(what) + ": comm is null");
+  if (dtype_size(dt) == 0) {
+    return fail(cemuInvalidArgument, std::string(what) + ": unsupported datatype " + std::to_string(dt));
+  }
+  if (cudaSetDevice(c->device) != cudaSuccess) {
+    return fail(cemuUnhandledCudaError, std::string(what) + ": cannot select device");
+  }
+  return cemuSuccess;
+}
+
+cemuResult_t check_op(int op, const char* what) {
+  if (op != cemuSum) {
+    return fail(cemuInvalidArgument,
+                std::string(what) + ": only cemuSum is supported (the reference only sums)");
+  }
+  return cemuSuccess;
+}
+
+cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, int rank, int device) {
+  if (!out) return fail(cemuInvalidArgument, "cemuCommInitRank: comm pointer is null");
+  if (rank < 0 || static_cast<uint32_t>(rank) >= cfg.world_size) {
+    return fail(cemuInvalidArgument, "rank " + std::to_string(rank) + " out of range [0," +
+                                         std::to_string(cfg.world_size - 1) + "]");
+  }
+  if (!cfg.is_real(static_cast<uint32_t>(rank))) {
+    return fail(cemuInvalidArgument,
+                "rank " + std::to_string(rank) + " is not a real rank in this job");
+  }
+  auto c = std::make_unique<cemuComm>();
+  c->W = cfg.world_size;
+  c->rank = static_cast<uint32_t>(rank);
+  c->device = device;
+  c->real.assign(cfg.real_ranks.begin(), cfg.real_ranks.end());
+  c->k = static_cast<uint32_t>(c->real.size());
+  c->li = static_cast<uint32_t>(std::find(c->real.begin(), c->real.end(), c->rank) - c->real.begin());
+  c->contiguous = c->real.back() - c->real.front() + 1 == c->k;
+  c->seed = cfg.payload_seed;
+  c->mode = cfg.payload_mode;
+  c->delay.kind = static_cast<int32_t>(cfg.delay_kind);
+  c->delay.algo = static_cast<int32_t>(cfg.algo());
+  c->delay.alpha_us = cfg.link.alpha_us;
+  c->delay.beta_us_per_byte = cfg.link.beta_us_per_byte;
+  c->delay.gamma_us_per_byte = cfg.link.gamma_us_per_byte;
+  c->delay.fixed_us = cfg.delay_fixed_us;
+  c->delay.inject_us = cfg.delay_inject_us;
+  c->delay.gpus_per_node = cfg.gpus_per_node;
+  c->delay.intra_alpha_us = cfg.intra_alpha_us;
+  c->delay.intra_beta_us_per_byte = cfg.intra_beta_us_per_byte;
+  c->delay_active = cfg.delay_kind != DelayKind::kNone || cfg.delay_inject_us != 0.0;
+  if (c->mode == PayloadMode::kZero && c->k != 1) {
+    return fail(cemuInvalidUsage,
+                "payload.mode: zero reproduces the reference emulator, which serves exactly "
+                "one real rank (emulator.cpp:75-79)");
+  }
+  std::vector<uint32_t> keys;
+  for (uint32_t r = 0; r < c->W; ++r) {
+    if (!cfg.is_real(r)) {
+      c->virt.push_back(r);
+      keys.push_back(payload_key(c->seed, r));
+    }
+  }
+  c->cfg = std::move(cfg);
+  if (cudaSetDevice(device) != cudaSuccess) return fail(cemuUnhandledCudaError, "cudaSetDevice failed");
+  CUDA_OK(cudaMalloc(&c->d_virt_keys, keys.size() * 4));
+  CUDA_OK(cudaMalloc(&c->d_virt_ranks, c->virt.size() * 4));
+  CUDA_OK(cudaMemcpy(c->d_virt_keys, keys.data(), keys.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_OK(cudaMemcpy(c->d_virt_ranks, c->virt.data(), c->virt.size() * 4, cudaMemcpyHostToDevice));
+  for (int coll = 0; coll < 4; ++coll) c->kmax = std::max(c->kmax, to_real_count(coll, c->W, c->real));
+  CUDA_OK(cudaMalloc(&c->d_slots, cemuComm::kSlots * slot_words(c->kmax) * 8));
+  CUDA_OK(cudaMemset(c->d_slots, 0, cemuComm::kSlots * slot_words(c->kmax) * 8));
+  if (c->k > 1) {
+    const Nccl* n = nccl();
+    if (!n) {
+      return fail(cemuSystemError,
+                  "job places " + std::to_string(c->k) +
+                      " real ranks on this box but libnccl.so.2 could not be loaded");
+    }
+    ncclUniqueId nid;
+    static_assert(sizeof(nid) == sizeof(id), "unique id size");
+    std::memcpy(&nid, &id, sizeof nid);
+    NCCL_OK(n->CommInitRank(&c->inner, static_cast<int>(c->k), nid, static_cast<int>(c->li)));
+  }
+  *out = c.release();
+  return cemuSuccess;
+}
+
+// ----------------------------------------------------------------------------
+// collective bodies
+// ----------------------------------------------------------------------------
+cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, cemuComm* c,
+                          cudaStream_t s) {
+  const size_t es = dtype_size(dt);
+  if (count == 0) return cemuSuccess;
+  Call call(c, kAllReduce, count * es, s);
+  const auto* nv = c->d_virt_keys;
+  const uint32_t nk = static_cast<uint32_t>(c->virt.size());
+  if (c->mode == PayloadMode::kZero) {
+    // A10: zero replies; the real rank keeps chunk (rank+1) mod W
+    // (test_transport.cpp:129-167), every other chunk is gathered zeros.
+    CUDA_OK(call.stamp_now());
+    const uint64_t total = count * es;
+    const uint32_t keep = (c->rank + 1) % c->W;
+    const uint64_t off = chunk_offset_bytes(c->W, total, static_cast<uint32_t>(es), keep);
+    const uint64_t len = chunk_bytes(c->W, total, static_cast<uint32_t>(es), keep);
+    auto* r8 = static_cast<uint8_t*>(recv);
+    if (off) CUDA_OK(cudaMemsetAsync(r8, 0, off, s));
+    if (send != recv && len) {
+      CUDA_OK(cudaMemcpyAsync(r8 + off, static_cast<const uint8_t*>(send) + off, len,
+                              cudaMemcpyDeviceToDevice, s));
+    }
+    if (total - off - len) CUDA_OK(cudaMemsetAsync(r8 + off + len, 0, total - off - len, s));
+    CUDA_OK(call.finish(kAllReduce));
+    return cemuSuccess;
+  }
+  if (c->k == 1) {
+    CUDA_OK(launch_synth_reduce(dt, send, recv, count, 0, nv, nk, call.take_stamp(), s, &call.launches));
+    CUDA_OK(call.finish(kAllReduce));
+    return cemuSuccess;
+  }
+  // k real GPUs: NCCL reduce-scatter of the real part, synthesis on this
+  // GPU's 1/k shard only, NCCL allgather.
+  const Nccl* n = nccl();
+  CUDA_OK(call.stamp_now());
+  const size_t shard = count / c->k;
+  const size_t rem = count - shard * c->k;
+  auto* r8 = static_cast<uint8_t*>(recv);
+  const auto* s8 = static_cast<const uint8_t*>(send);
+  const auto ndt = static_cast<ncclDataType_t>(dt);
+  if (shard) NCCL_OK(n->ReduceScatter(send, r8 + c->li * shard * es, shard, ndt, ncclSum, c->inner, s));
+  if (rem) NCCL_OK(n->AllReduce(s8 + c->k * shard * es, r8 + c->k * shard * es, rem, ndt, ncclSum, c->inner, s));
+  if (shard) {
+    CUDA_OK(launch_synth_reduce(dt, r8 + c->li * shard * es, r8 + c->li * shard * es, shard,
+                                c->li * shard, nv, nk, nullptr, s, &call.launches));
+  }
+  if (rem) {
+    CUDA_OK(launch_synth_reduce(dt, r8 + c->k * shard * es, r8 + c->k * shard * es, rem,
+                                c->k * shard, nv, nk, nullptr, s, &call.launches));
+  }
+  if (shard) NCCL_OK(n->AllGather(r8 + c->li * shard * es, r8, shard, ndt, c->inner, s));
+  CUDA_OK(call.finish(kAllReduce));
+  return cemuSuccess;
+}
+
+cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuComm* c, cudaStream_t s) {
+  const size_t es = dtype_size(dt);
+  if (sc == 0) return cemuSuccess;
+  Call call(c, kAllGather, sc * es, s);
+  auto* r8 = static_cast<uint8_t*>(recv);
+  const uint32_t nvirt = static_cast<uint32_t>(c->virt.size());
+  const bool own_in_place = send == r8 + static_cast<uint64_t>(c->rank) * sc * es;
+  if (c->mode == PayloadMode::kZero) {
+    // test_transport.cpp:169-182: own block kept, every other block zeros
+    CUDA_OK(call.stamp_now());
+    const uint64_t blk = sc * es;
+    if (c->rank) CUDA_OK(cudaMemsetAsync(r8, 0, c->rank * blk, s));
+    if (c->rank + 1 < c->W) CUDA_OK(cudaMemsetAsync(r8 + (c->rank + 1) * blk, 0, (c->W - c->rank - 1) * blk, s));
+    if (!own_in_place) CUDA_OK(cudaMemcpyAsync(r8 + c->rank * blk, send, blk, cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(call.finish(kAllGather));
+    return cemuSuccess;
+  }
+  const void* own = (c->k == 1 && !own_in_place) ? send : nullptr;
+  CUDA_OK(launch_synth_fill(dt, recv, sc, c->d_virt_ranks, c->d_virt_keys, nvirt, 0, 0, own, c->rank,
+                            call.take_stamp(), s, &call.launches));
+  if (c->k > 1) {
+    const Nccl* n = nccl();
+    const auto ndt = static_cast<ncclDataType_t>(dt);
+    if (c->contiguous) {
+      NCCL_OK(n->AllGather(send, r8 + static_cast<uint64_t>(c->real[0]) * sc * es, sc, ndt, c->inner, s));
+    } else {
+      NCCL_OK(n->GroupStart());
+      for (uint32_t j = 0; j < c->k; ++j) {
+        NCCL_OK(n->Broadcast(send, r8 + static_cast<uint64_t>(c->real[j]) * sc * es, sc, ndt,
+                             static_cast<int>(j), c->inner, s));
+      }
+      NCCL_OK(n->GroupEnd());
+    }
+  }
+  CUDA_OK(call.finish(kAllGather));
+  return cemuSuccess;
+}
+
+cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, cemuComm* c,
+                              cudaStream_t s) {
+  const size_t es = dtype_size(dt);
+  if (rc == 0) return cemuSuccess;
+  Call call(c, kReduceScatter, rc * es * c->W, s);
+  const auto* s8 = static_cast<const uint8_t*>(send);
+  const uint64_t mine = static_cast<uint64_t>(c->rank) * rc;
+  if (c->mode == PayloadMode::kZero) {
+    // own contribution to chunk `rank` plus zero replies
+    CUDA_OK(launch_synth_fill(dt, recv, rc, nullptr, nullptr, 0, 0, 0, s8 + mine * es, 0,
+                              call.take_stamp(), s, &call.launches));
+    CUDA_OK(call.finish(kReduceScatter));
+    return cemuSuccess;
+  }
+  const uint32_t nk = static_cast<uint32_t>(c->virt.size());
+  if (c->k == 1) {
+    CUDA_OK(launch_synth_reduce(dt, s8 + mine * es, recv, rc, mine, c->d_virt_keys, nk,
+                                call.take_stamp(), s, &call.launches));
+    CUDA_OK(call.finish(kReduceScatter));
+    return cemuSuccess;
+  }
+  const Nccl* n = nccl();
+  const auto ndt = static_cast<ncclDataType_t>(dt);
+  CUDA_OK(call.stamp_now());
+  if (c->contiguous) {
+    NCCL_OK(n->ReduceScatter(s8 + static_cast<uint64_t>(c->real[0]) * rc * es, recv, rc, ndt, ncclSum,
+                             c->inner, s));
+  } else {
+    NCCL_OK(n->GroupStart());
+    for (uint32_t j = 0; j < c->k; ++j) {
+      NCCL_OK(n->Reduce(s8 + static_cast<uint64_t>(c->real[j]) * rc * es, recv, rc, ndt, ncclSum,
+                        static_cast<int>(j), c->inner, s));
+    }
+    NCCL_OK(n->GroupEnd());
+  }
+  CUDA_OK(launch_synth_reduce(dt, recv, recv, rc, mine, c->d_virt_keys, nk, nullptr, s, &call.launches));
+  CUDA_OK(call.finish(kReduceScatter));
+  return cemuSuccess;
+}
+
+cemuResult_t do_broadcast(const void* send, void* recv, size_t count, int dt, int root, cemuComm* c,
+                          cudaStream_t s) {
+  const size_t es = dtype_size(dt);
+  if (root < 0 || static_cast<uint32_t>(root) >= c->W) {
+    return fail(cemuInvalidArgument, "cemuBroadcast: root " + std::to_string(root) + " out of range [0," +
+                                         std::to_string(c->W - 1) + "]");
+  }
+  if (count == 0) return cemuSuccess;
+  Call call(c, kBroadcast, count * es, s);
+  const uint32_t r = static_cast<uint32_t>(root);
+  if (c->cfg.is_real(r)) {
+    if (c->k == 1) {
+      if (send != recv) {
+        CUDA_OK(launch_synth_fill(dt, recv, count, nullptr, nullptr, 0, 0, 0, send, 0, call.take_stamp(), s,
+                                  &call.launches));
+      }
+    } else {
+      CUDA_OK(call.stamp_now());
+      const int lroot = static_cast<int>(std::find(c->real.begin(), c->real.end(), r) - c->real.begin());
+      NCCL_OK(nccl()->Broadcast(send, recv, count, static_cast<ncclDataType_t>(dt), lroot, c->inner, s));
+    }
+  } else if (c->mode == PayloadMode::kZero) {
+    CUDA_OK(call.stamp_now());
+    CUDA_OK(cudaMemsetAsync(recv, 0, count * es, s));
+  } else {
+    CUDA_OK(launch_synth_fill(dt, recv, count, nullptr, nullptr, 1, 0, payload_key(c->seed, r), nullptr, 0,
+                              call.take_stamp(), s, &call.launches));
+  }
+  CUDA_OK(call.finish(kBroadcast));
+  return cemuSuccess;
+}
+
+template <typename F>
+cemuResult_t run_or_defer(F&& f) {
+  if (g_group_depth > 0) {
+    g_group_ops.emplace_back(std::forward<F>(f));
+    return cemuSuccess;
+  }
+  return f();
+}
+
+}  // namespace
+
+// =============================================================================
+// C-ABI
+// =============================================================================
+extern "C" {
+
+cemuResult_t cemuGetVersion(int* version) {
+  if (!version) return fail(cemuInvalidArgument, "cemuGetVersion: version is null");
+  *version = CEMU_B200_VERSION;
+  return cemuSuccess;
+}
+
+cemuResult_t cemuGetUniqueId(cemuUniqueId* uid) {
+  if (!uid) return fail(cemuInvalidArgument, "cemuGetUniqueId: uniqueId is null");
+  if (const Nccl* n = nccl()) {
+    ncclUniqueId id;
+    NCCL_OK(n->GetUniqueId(&id));
+    std::memcpy(uid, &id, sizeof id);
+    return cemuSuccess;
+  }
+  std::random_device rd;
+  for (auto& b : uid->internal) b = static_cast<char>(rd());
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommInitRankConfig(cemuComm_t* comm, const char* text, cemuUniqueId id, int rank,
+                                    int device) {
+  if (!text) return fail(cemuInvalidArgument, "cemuCommInitRankConfig: configText is null");
+  try {
+    return init_comm(comm, parse_job_config(text), id, rank, device);
+  } catch (const ConfigError& e) {
+    return fail(cemuInvalidArgument, e.what());
+  } catch (const std::exception& e) {
+    return fail(cemuInternalError, e.what());
+  }
+}
+
+cemuResult_t cemuCommInitRank(cemuComm_t* comm, int nranks, cemuUniqueId id, int rank) {
+  const char* path = std::getenv("CEMU_CONFIG");
+  if (!path || !*path) {
+    return fail(cemuInvalidUsage, "CEMU_CONFIG: must name the job config file");
+  }
+  try {
+    JobConfig cfg = load_job_config(path);
+    if (nranks != static_cast<int>(cfg.world_size)) {
+      return fail(cemuInvalidArgument, "nranks " + std::to_string(nranks) +
+                                           " does not match world_size " +
+                                           std::to_string(cfg.world_size) + " of " + path);
+    }
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(cemuUnhandledCudaError, "cudaGetDevice failed");
+    return init_comm(comm, std::move(cfg), id, rank, dev);
+  } catch (const ConfigError& e) {
+    return fail(cemuInvalidArgument, e.what());
+  } catch (const std::exception& e) {
+    return fail(cemuInternalError, e.what());
+  }
+}
+
+cemuResult_t cemuCommDestroy(cemuComm_t c) {
+  if (!c) return cemuSuccess;
+  cudaSetDevice(c->device);
+  if (c->inner && nccl()) nccl()->CommDestroy(c->inner);
+  cudaFree(c->d_virt_keys);
+  cudaFree(c->d_virt_ranks);
+  cudaFree(c->d_slots);
+  delete c;
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommCount(const cemuComm_t c, int* count) {
+  if (!c || !count) return fail(cemuInvalidArgument, "cemuCommCount: null argument");
+  *count = static_cast<int>(c->W);
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommUserRank(const cemuComm_t c, int* rank) {
+  if (!c || !rank) return fail(cemuInvalidArgument, "cemuCommUserRank: null argument");
+  *rank = static_cast<int>(c->rank);
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommCuDevice(const cemuComm_t c, int* device) {
+  if (!c || !device) return fail(cemuInvalidArgument, "cemuCommCuDevice: null argument");
+  *device = c->device;
+  return cemuSuccess;
+}
+
+const char* cemuGetErrorString(cemuResult_t r) {
+  switch (r) {
+    case cemuSuccess: return "no error";
+    case cemuUnhandledCudaError: return "unhandled cuda error";
+    case cemuSystemError: return "unhandled system error";
+    case cemuInternalError: return "internal error";
+    case cemuInvalidArgument: return "invalid argument";
+    case cemuInvalidUsage: return "invalid usage";
+    case cemuRemoteError: return "remote process exited or there was a network error";
+    case cemuInProgress: return "operation in progress";
+  }
+  return "unknown result code";
+}
+
+const char* cemuGetLastError(cemuComm_t) { return g_last_error.c_str(); }
+
+cemuResult_t cemuAllReduce(const void* send, void* recv, size_t count, cemuDataType_t dt, cemuRedOp_t op,
+                           cemuComm_t c, cemuStream_t stream) {
+  if (auto r = check_common(c, dt, "cemuAllReduce")) return r;
+  if (auto r = check_op(op, "cemuAllReduce")) return r;
+  if (count && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllReduce: null buffer");
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  return run_or_defer([=] { return do_allreduce(send, recv, count, dt, c, s); });
+}
+
+cemuResult_t cemuAllGather(const void* send, void* recv, size_t sc, cemuDataType_t dt, cemuComm_t c,
+                           cemuStream_t stream) {
+  if (auto r = check_common(c, dt, "cemuAllGather")) return r;
+  if (sc && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllGather: null buffer");
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  return run_or_defer([=] { return do_allgather(send, recv, sc, dt, c, s); });
+}
+
+cemuResult_t cemuReduceScatter(const void* send, void* recv, size_t rc, cemuDataType_t dt, cemuRedOp_t op,
+                               cemuComm_t c, cemuStream_t stream) {
+  if (auto r = check_common(c, dt, "cemuReduceScatter")) return r;
+  if (auto r = check_op(op, "cemuReduceScatter")) return r;
+  if (rc && (!send || !recv)) return fail(cemuInvalidArgument, "cemuReduceScatter: null buffer");
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  return run_or_defer([=] { return do_reducescatter(send, recv, rc, dt, c, s); });
+}
+
+cemuResult_t cemuBroadcast(const void* send, void* recv, size_t count, cemuDataType_t dt, int root,
+                           cemuComm_t c, cemuStream_t stream) {
+  if (auto r = check_common(c, dt, "cemuBroadcast")) return r;
+  if (count && !recv) return fail(cemuInvalidArgument, "cemuBroadcast: null recvbuff");
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  return run_or_defer([=] { return do_broadcast(send, recv, count, dt, root, c, s); });
+}
+
+cemuResult_t cemuGroupStart(void) {
+  ++g_group_depth;
+  return cemuSuccess;
+}
+
+cemuResult_t cemuGroupEnd(void) {
+  if (g_group_depth == 0) return fail(cemuInvalidUsage, "cemuGroupEnd: not in a group");
+  if (--g_group_depth > 0) return cemuSuccess;
+  std::vector<std::function<cemuResult_t()>> ops;
+  ops.swap(g_group_ops);
+  for (auto& f : ops) {
+    if (auto r = f()) return r;
+  }
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommLastCallId(cemuComm_t c, uint64_t* id) {
+  if (!c || !id) return fail(cemuInvalidArgument, "cemuCommLastCallId: null argument");
+  if (c->calls == 0) return fail(cemuInvalidUsage, "cemuCommLastCallId: no call issued yet");
+  *id = c->calls - 1;
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommCallRecord(cemuComm_t c, uint64_t id, cemuCallRecord* rec, int64_t* floors,
+                                int64_t* release, double* offsets, size_t cap) {
+  if (!c || !rec) return fail(cemuInvalidArgument, "cemuCommCallRecord: null argument");
+  const uint32_t i = static_cast<uint32_t>(id % cemuComm::kSlots);
+  const auto& m = c->meta[i];
+  if (m.call_id != id) {
+    return fail(cemuInvalidArgument, "cemuCommCallRecord: call " + std::to_string(id) +
+                                         " is no longer held (ring of " +
+                                         std::to_string(cemuComm::kSlots) + ")");
+  }
+  std::memset(rec, 0, sizeof *rec);
+  rec->call_id = id;
+  rec->coll = m.coll;
+  rec->delay_active = m.delay ? 1 : 0;
+  rec->steps = m.k;
+  rec->world = c->W;
+  rec->model_bytes = m.bytes;
+  rec->model_latency_us = m.latency;
+  if (!m.delay) return cemuSuccess;
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(cemuUnhandledCudaError, "cudaSetDevice");
+  std::vector<int64_t> h(slot_words(c->kmax));
+  CUDA_OK(cudaMemcpy(h.data(), c->d_slots + i * slot_words(c->kmax), h.size() * 8, cudaMemcpyDeviceToHost));
+  rec->t_start_ns = h[0];
+  rec->t_end_ns = h[1];
+  rec->device_latency_us = h[2];
+  const size_t n = std::min<size_t>(cap, m.k);
+  if (floors) std::memcpy(floors, h.data() + kSlotHeader, n * 8);
+  if (release) std::memcpy(release, h.data() + kSlotHeader + c->kmax, n * 8);
+  if (offsets) std::memcpy(offsets, h.data() + kSlotHeader + 2 * c->kmax, n * 8);
+  return cemuSuccess;
+}
+
+}  // extern "C"
+
+// launch counter for bench.py's gpu_launches (not part of the public header)
+extern "C" uint64_t cemuCommKernelLaunches(cemuComm_t c) { return c ? c->launches : 0; }

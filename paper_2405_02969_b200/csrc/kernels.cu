@@ -1,0 +1,646 @@
+// kernels.cu -- sm_100a kernels of the emulated collective.
+//
+// synth_reduce_vec   THE hot kernel.  One streaming pass over the real
+//                    rank's buffer: 128-bit non-allocating loads, the
+//                    emulated peers' contributions synthesised in registers
+//                    from the counter-based hash (payload.cuh) and summed in
+//                    SWAR 16-bit lanes, one fused add with the local value,
+//                    128-bit streaming stores.  HBM traffic is exactly the
+//                    algorithmic 2S bytes: synthesised peers cost no bytes.
+//                    Replaces, per call, the reference's 2(n-1) TCP frames,
+//                    FrameReader copies and reduce_add_i32/u8
+//                    (proj/src/collective.cpp:268-355, reduce.cpp:42-60).
+// synth_fill_vec     write-only synthesis of whole emulated blocks
+//                    (allgather blocks, a broadcast from an emulated root).
+// delay_spin_kernel  evaluates the alpha-beta model on the device
+//                    (delay_math.cuh, bit-exact with delay.cpp:5-47 and the
+//                    llround floors of engine.cpp:36-42), then releases the
+//                    K to-real steps in order on %globaltimer -- the device
+//                    analogue of the emulator's poller (emulator.cpp:165-191)
+//                    enqueued on the collective's stream.
+// *_scalar           element-wise fallbacks (misaligned pointers, 64-bit
+//                    types, tails).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
+#include "delay_math.cuh"
+#include "kernels.hpp"
+#include "payload.cuh"
+
+namespace cemu_b200 {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr uint32_t kMaxKeys = 4096;  // smem key table (16 KB) upper bound
+
+__device__ __forceinline__ int64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<int64_t>(t);
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// bytewise (mod 256) add of two packed words
+__device__ __forceinline__ uint32_t add_bytes(uint32_t a, uint32_t b) {
+  return ((a & 0x7F7F7F7Fu) + (b & 0x7F7F7F7Fu)) ^ ((a ^ b) & 0x80808080u);
+}
+
+__device__ __forceinline__ float f32_of(uint32_t u) { return __uint_as_float(u); }
+__device__ __forceinline__ uint32_t u32_of(float f) { return __float_as_uint(f); }
+
+// x (+) s * 2^-7 with a single rounding in fp32 (s*2^-7 is exact).
+__device__ __forceinline__ float fold_f32(float x, int32_t s) {
+  return __fadd_rn(x, __int2float_rn(s) * kDyadicScale);
+}
+
+__device__ __forceinline__ uint32_t fold_bf16x2(uint32_t packed, int32_t s_lo, int32_t s_hi) {
+  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&packed);
+  const float a = fold_f32(__bfloat162float(v.x), s_lo);
+  const float b = fold_f32(__bfloat162float(v.y), s_hi);
+  __nv_bfloat162 r;
+  r.x = __float2bfloat16_rn(a);
+  r.y = __float2bfloat16_rn(b);
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+__device__ __forceinline__ uint32_t fold_f16x2(uint32_t packed, int32_t s_lo, int32_t s_hi) {
+  __half2 v = *reinterpret_cast<__half2*>(&packed);
+  const float a = fold_f32(__half2float(v.x), s_lo);
+  const float b = fold_f32(__half2float(v.y), s_hi);
+  __half2 r;
+  r.x = __float2half_rn(a);
+  r.y = __float2half_rn(b);
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// ---------------------------------------------------------------------------
+// vector kinds
+// ---------------------------------------------------------------------------
+enum VKind { kF32 = 0, kF16 = 1, kBF16 = 2, kU8 = 3, kI32 = 4 };
+
+template <int K>
+struct VT;
+// EPV elements per 16-byte vector, WPV payload words per vector, U vectors
+// per thread per iteration (64 B in flight per thread for every kind).
+template <> struct VT<kF32>  { static constexpr int EPV = 4,  WPV = 1, U = 4; static constexpr bool kWords = false; };
+template <> struct VT<kF16>  { static constexpr int EPV = 8,  WPV = 2, U = 4; static constexpr bool kWords = false; };
+template <> struct VT<kBF16> { static constexpr int EPV = 8,  WPV = 2, U = 4; static constexpr bool kWords = false; };
+template <> struct VT<kU8>   { static constexpr int EPV = 16, WPV = 4, U = 4; static constexpr bool kWords = false; };
+template <> struct VT<kI32>  { static constexpr int EPV = 4,  WPV = 4, U = 4; static constexpr bool kWords = true; };
+
+// ---------------------------------------------------------------------------
+// generic per-element path (all 10 datatypes)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t pbyte(uint32_t key, uint64_t e) {
+  return (payload_word(key, e >> 2) >> (8 * (e & 3))) & 0xFFu;
+}
+
+template <int DT>
+__device__ void elem_reduce(const void* src, void* dst, uint64_t i, uint64_t e,
+                            const uint32_t* keys, uint32_t nkeys) {
+  if constexpr (DT == cemuInt8 || DT == cemuUint8) {
+    uint32_t acc = static_cast<const uint8_t*>(src)[i];
+    for (uint32_t q = 0; q < nkeys; ++q) acc += pbyte(keys[q], e);
+    static_cast<uint8_t*>(dst)[i] = static_cast<uint8_t>(acc);
+  } else if constexpr (DT == cemuInt32 || DT == cemuUint32) {
+    uint32_t acc = static_cast<const uint32_t*>(src)[i];
+    for (uint32_t q = 0; q < nkeys; ++q) acc += payload_word(keys[q], e);
+    static_cast<uint32_t*>(dst)[i] = acc;
+  } else if constexpr (DT == cemuInt64 || DT == cemuUint64) {
+    uint64_t acc = static_cast<const uint64_t*>(src)[i];
+    for (uint32_t q = 0; q < nkeys; ++q) {
+      acc += static_cast<uint64_t>(payload_word(keys[q], 2 * e)) |
+             (static_cast<uint64_t>(payload_word(keys[q], 2 * e + 1)) << 32);
+    }
+    static_cast<uint64_t*>(dst)[i] = acc;
+  } else {
+    int32_t s = 0;
+    for (uint32_t q = 0; q < nkeys; ++q) s += static_cast<int32_t>(pbyte(keys[q], e)) - 128;
+    if constexpr (DT == cemuFloat64) {
+      static_cast<double*>(dst)[i] =
+          __dadd_rn(static_cast<const double*>(src)[i], static_cast<double>(s) * 0.0078125);
+    } else if constexpr (DT == cemuFloat32) {
+      static_cast<float*>(dst)[i] = fold_f32(static_cast<const float*>(src)[i], s);
+    } else if constexpr (DT == cemuFloat16) {
+      const __half x = static_cast<const __half*>(src)[i];
+      static_cast<__half*>(dst)[i] = __float2half_rn(fold_f32(__half2float(x), s));
+    } else {
+      const __nv_bfloat16 x = static_cast<const __nv_bfloat16*>(src)[i];
+      static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(fold_f32(__bfloat162float(x), s));
+    }
+  }
+}
+
+template <int DT>
+__device__ void elem_fill(void* dst, uint64_t i, uint64_t e, uint32_t key) {
+  if constexpr (DT == cemuInt8 || DT == cemuUint8) {
+    static_cast<uint8_t*>(dst)[i] = static_cast<uint8_t>(pbyte(key, e));
+  } else if constexpr (DT == cemuInt32 || DT == cemuUint32) {
+    static_cast<uint32_t*>(dst)[i] = payload_word(key, e);
+  } else if constexpr (DT == cemuInt64 || DT == cemuUint64) {
+    static_cast<uint64_t*>(dst)[i] = static_cast<uint64_t>(payload_word(key, 2 * e)) |
+                                     (static_cast<uint64_t>(payload_word(key, 2 * e + 1)) << 32);
+  } else {
+    const int32_t s = static_cast<int32_t>(pbyte(key, e)) - 128;
+    if constexpr (DT == cemuFloat64) {
+      static_cast<double*>(dst)[i] = static_cast<double>(s) * 0.0078125;
+    } else if constexpr (DT == cemuFloat32) {
+      static_cast<float*>(dst)[i] = __int2float_rn(s) * kDyadicScale;
+    } else if constexpr (DT == cemuFloat16) {
+      static_cast<__half*>(dst)[i] = __float2half_rn(__int2float_rn(s) * kDyadicScale);
+    } else {
+      static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(__int2float_rn(s) * kDyadicScale);
+    }
+  }
+}
+
+__device__ __forceinline__ void load_keys(uint32_t* skeys, const uint32_t* keys, uint32_t nkeys) {
+  for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x) skeys[i] = keys[i];
+  __syncthreads();
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads) synth_reduce_scalar(const void* src, void* dst,
+                                                                uint64_t count, uint64_t elem_base,
+                                                                const uint32_t* keys,
+                                                                uint32_t nkeys, int64_t* stamp) {
+  extern __shared__ uint32_t skeys[];
+  if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
+  load_keys(skeys, keys, nkeys);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += stride) {
+    elem_reduce<DT>(src, dst, i, elem_base + i, skeys, nkeys);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the hot kernel
+// ---------------------------------------------------------------------------
+template <int K, int DT, bool kMulti>
+__global__ void __launch_bounds__(kThreads) synth_reduce_vec(
+    const uint4* __restrict__ src, uint4* dst, uint64_t nvec, uint64_t word_base,
+    const uint32_t* __restrict__ keys, uint32_t nkeys, int64_t* stamp, const void* tail_src,
+    void* tail_dst, uint32_t ntail, uint64_t tail_e0) {
+  using T = VT<K>;
+  constexpr int U = T::U, W = T::WPV, NW = U * W;
+  extern __shared__ uint32_t skeys[];
+  if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
+  load_keys(skeys, keys, nkeys);
+
+  const uint64_t tile = static_cast<uint64_t>(kThreads) * U;
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * tile; base < nvec;
+       base += static_cast<uint64_t>(gridDim.x) * tile) {
+    // 1. issue every load of the tile first: synthesis below never depends
+    //    on them, so the whole peer loop hides the HBM latency.
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
+      if (v < nvec) x[u] = ld_stream(src + v);
+    }
+    uint32_t ctr[NW];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
+#pragma unroll
+      for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_ctr(word_base + v * W + w);
+    }
+
+    uint4 y[U];
+    if constexpr (T::kWords) {
+      // int32 lanes: plain wrapping sums, one payload word per element
+      uint32_t acc[NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) acc[i] = 0;
+#pragma unroll 2
+      for (uint32_t q = 0; q < nkeys; ++q) {
+        const uint32_t key = skeys[q];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) acc[i] += payload_mix(key, ctr[i]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        y[u].x = x[u].x + acc[u * 4 + 0];
+        y[u].y = x[u].y + acc[u * 4 + 1];
+        y[u].z = x[u].z + acc[u * 4 + 2];
+        y[u].w = x[u].w + acc[u * 4 + 3];
+      }
+    } else {
+      // byte payloads summed in SWAR 16-bit lanes: lo = (b0, b2), hi = (b1, b3)
+      int32_t s[NW * 4];
+      uint32_t lo[NW], hi[NW];
+      const uint32_t groups = kMulti ? (nkeys + 255) / 256 : 1;
+#pragma unroll
+      for (int i = 0; i < NW * 4; ++i) s[i] = 0;
+      for (uint32_t g = 0; g < groups; ++g) {
+        const uint32_t q0 = g * 256;
+        const uint32_t q1 = kMulti ? min(nkeys, q0 + 256) : nkeys;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) lo[i] = hi[i] = 0;
+#pragma unroll 2
+        for (uint32_t q = q0; q < q1; ++q) {
+          const uint32_t key = skeys[q];
+#pragma unroll
+          for (int i = 0; i < NW; ++i) {
+            const uint32_t h = payload_mix(key, ctr[i]);
+            lo[i] += h & 0x00FF00FFu;
+            hi[i] += __byte_perm(h, 0u, 0x4341);
+          }
+        }
+        if constexpr (K == kU8) {
+          // mod-2^16 lanes keep every byte sum exact mod 256: no grouping
+#pragma unroll
+          for (int i = 0; i < NW; ++i) {
+            s[i * 4 + 0] = static_cast<int32_t>((lo[i] & 0x00FF00FFu) | ((hi[i] & 0x00FF00FFu) << 8));
+          }
+        } else {
+          const int32_t bias = 128 * static_cast<int32_t>(q1 - q0);
+#pragma unroll
+          for (int i = 0; i < NW; ++i) {
+            s[i * 4 + 0] += static_cast<int32_t>(lo[i] & 0xFFFFu) - bias;
+            s[i * 4 + 1] += static_cast<int32_t>(hi[i] & 0xFFFFu) - bias;
+            s[i * 4 + 2] += static_cast<int32_t>(lo[i] >> 16) - bias;
+            s[i * 4 + 3] += static_cast<int32_t>(hi[i] >> 16) - bias;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if constexpr (K == kF32) {
+          const int32_t* t = s + u * 4;
+          y[u].x = u32_of(fold_f32(f32_of(x[u].x), t[0]));
+          y[u].y = u32_of(fold_f32(f32_of(x[u].y), t[1]));
+          y[u].z = u32_of(fold_f32(f32_of(x[u].z), t[2]));
+          y[u].w = u32_of(fold_f32(f32_of(x[u].w), t[3]));
+        } else if constexpr (K == kBF16 || K == kF16) {
+          const int32_t* t0 = s + (u * 2) * 4;      // elements 0..3
+          const int32_t* t1 = s + (u * 2 + 1) * 4;  // elements 4..7
+          if constexpr (K == kBF16) {
+            y[u].x = fold_bf16x2(x[u].x, t0[0], t0[1]);
+            y[u].y = fold_bf16x2(x[u].y, t0[2], t0[3]);
+            y[u].z = fold_bf16x2(x[u].z, t1[0], t1[1]);
+            y[u].w = fold_bf16x2(x[u].w, t1[2], t1[3]);
+          } else {
+            y[u].x = fold_f16x2(x[u].x, t0[0], t0[1]);
+            y[u].y = fold_f16x2(x[u].y, t0[2], t0[3]);
+            y[u].z = fold_f16x2(x[u].z, t1[0], t1[1]);
+            y[u].w = fold_f16x2(x[u].w, t1[2], t1[3]);
+          }
+        } else {  // kU8
+          y[u].x = add_bytes(x[u].x, static_cast<uint32_t>(s[(u * 4 + 0) * 4]));
+          y[u].y = add_bytes(x[u].y, static_cast<uint32_t>(s[(u * 4 + 1) * 4]));
+          y[u].z = add_bytes(x[u].z, static_cast<uint32_t>(s[(u * 4 + 2) * 4]));
+          y[u].w = add_bytes(x[u].w, static_cast<uint32_t>(s[(u * 4 + 3) * 4]));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
+      if (v < nvec) st_stream(dst + v, y[u]);
+    }
+  }
+  // ragged tail (< one vector): the last block's first threads
+  if (ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < ntail) {
+    elem_reduce<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, skeys, nkeys);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fills
+// ---------------------------------------------------------------------------
+template <int K>
+__device__ __forceinline__ uint4 synth_vector(uint32_t key, uint64_t word0) {
+  using T = VT<K>;
+  uint32_t wd[T::WPV];
+#pragma unroll
+  for (int w = 0; w < T::WPV; ++w) wd[w] = payload_word(key, word0 + w);
+  uint4 r;
+  if constexpr (K == kU8 || K == kI32) {
+    r.x = wd[0];
+    r.y = wd[1];
+    r.z = wd[2];
+    r.w = wd[3];
+  } else if constexpr (K == kF32) {
+    const uint32_t h = wd[0];
+    r.x = u32_of(__int2float_rn(static_cast<int32_t>(h & 0xFFu) - 128) * kDyadicScale);
+    r.y = u32_of(__int2float_rn(static_cast<int32_t>((h >> 8) & 0xFFu) - 128) * kDyadicScale);
+    r.z = u32_of(__int2float_rn(static_cast<int32_t>((h >> 16) & 0xFFu) - 128) * kDyadicScale);
+    r.w = u32_of(__int2float_rn(static_cast<int32_t>(h >> 24) - 128) * kDyadicScale);
+  } else {
+    uint32_t out[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {  // pair p = elements 2p, 2p+1
+      const uint32_t h = wd[p >> 1];
+      const int sh = (p & 1) * 16;
+      const float a = __int2float_rn(static_cast<int32_t>((h >> sh) & 0xFFu) - 128) * kDyadicScale;
+      const float b = __int2float_rn(static_cast<int32_t>((h >> (sh + 8)) & 0xFFu) - 128) * kDyadicScale;
+      if constexpr (K == kBF16) {
+        __nv_bfloat162 v;
+        v.x = __float2bfloat16_rn(a);
+        v.y = __float2bfloat16_rn(b);
+        out[p] = *reinterpret_cast<uint32_t*>(&v);
+      } else {
+        __half2 v;
+        v.x = __float2half_rn(a);
+        v.y = __float2half_rn(b);
+        out[p] = *reinterpret_cast<uint32_t*>(&v);
+      }
+    }
+    r = make_uint4(out[0], out[1], out[2], out[3]);
+  }
+  return r;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) synth_fill_vec(uint4* dst, uint64_t nvec_per_block,
+                                                           const uint32_t* __restrict__ index,
+                                                           const uint32_t* __restrict__ keys,
+                                                           uint32_t nblocks, uint32_t index0,
+                                                           uint32_t key0, const uint4* own_src,
+                                                           uint32_t own_index, int64_t* stamp) {
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
+  const uint32_t b = blockIdx.y;
+  const bool copy = b == nblocks;
+  const uint32_t idx = copy ? own_index : (index ? index[b] : index0);
+  const uint32_t key = copy ? 0u : (keys ? keys[b] : key0);
+  uint4* out = dst + static_cast<uint64_t>(idx) * nvec_per_block;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec_per_block;
+       v += stride) {
+    if (copy) {
+      st_stream(out + v, ld_stream(own_src + v));
+    } else {
+      st_stream(out + v, synth_vector<K>(key, v * VT<K>::WPV));
+    }
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads) synth_fill_scalar(void* dst, uint64_t block_elems,
+                                                              const uint32_t* index,
+                                                              const uint32_t* keys, uint32_t nblocks,
+                                                              uint32_t index0, uint32_t key0,
+                                                              const void* own_src, uint32_t own_index,
+                                                              int64_t* stamp, int elem_size) {
+  if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
+  const uint32_t b = blockIdx.y;
+  const bool copy = b == nblocks;
+  const uint32_t idx = copy ? own_index : (index ? index[b] : index0);
+  const uint32_t key = copy ? 0u : (keys ? keys[b] : key0);
+  uint8_t* out = static_cast<uint8_t*>(dst) + static_cast<uint64_t>(idx) * block_elems * elem_size;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  if (copy) {
+    const uint64_t nbytes = block_elems * elem_size;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nbytes;
+         i += stride) {
+      out[i] = static_cast<const uint8_t*>(own_src)[i];
+    }
+    return;
+  }
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < block_elems;
+       i += stride) {
+    elem_fill<DT>(out, i, i, key);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// delay
+// ---------------------------------------------------------------------------
+__global__ void stamp_kernel(int64_t* slot) { slot[0] = globaltimer_ns(); }
+
+__global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int64_t* slot) {
+  int64_t* floors = slot + kSlotHeader;
+  int64_t* release = floors + d.kmax;
+  double* offs = reinterpret_cast<double*>(release + d.kmax);
+  __shared__ int64_t t0_s;
+  if (threadIdx.x == 0) {
+    t0_s = d.self_stamp ? globaltimer_ns() : slot[0];
+    if (d.self_stamp) slot[0] = t0_s;
+  }
+  // Evaluate the model on the device: delay.cpp:23-47 offsets and
+  // engine.cpp:41 llround floors, strided over the block.
+  const double total = d.model.kind == 1 ? model_total_us(d.model, d.coll, d.n, d.bytes) : 0.0;
+  for (uint32_t j = threadIdx.x; j < d.k; j += blockDim.x) {
+    const double o = release_offset_us(d.model, total, j, d.k);
+    offs[j] = o;
+    floors[j] = llround(o);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int64_t lat = 0;
+  for (uint32_t j = 0; j < d.k; ++j) lat = max(lat, floors[j]);
+  slot[2] = lat;
+  slot[3] = d.k;
+  // Head-of-line release (engine.cpp:58-70): step j leaves once its floor
+  // has passed and step j-1 has left.
+  const int64_t t0 = t0_s;
+  int64_t t = globaltimer_ns();
+  for (uint32_t j = 0; j < d.k; ++j) {
+    const int64_t target = t0 + floors[j] * 1000;
+    while (t < target) {
+      if (target - t > 8000) __nanosleep(2000);
+      t = globaltimer_ns();
+    }
+    release[j] = t;
+  }
+  slot[1] = globaltimer_ns();
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+int sm_count() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+template <typename Kern>
+int blocks_per_sm(Kern k, size_t smem) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kThreads, smem) != cudaSuccess || b < 1) {
+    cudaGetLastError();
+    b = 1;
+  }
+  return b;
+}
+
+template <int K, int DT>
+cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_base,
+                    const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
+  using T = VT<K>;
+  const uint64_t nvec = count / T::EPV;
+  const uint32_t ntail = static_cast<uint32_t>(count - nvec * T::EPV);
+  const size_t es = T::kWords ? 4 : (K == kF32 ? 4 : (K == kU8 ? 1 : 2));
+  const uint64_t word_base = T::kWords ? elem_base : elem_base / 4;
+  const size_t smem = static_cast<size_t>(nkeys) * 4;
+  const bool multi = !T::kWords && K != kU8 && nkeys > 256;
+  auto kern = multi ? synth_reduce_vec<K, DT, true> : synth_reduce_vec<K, DT, false>;
+  static int per_sm[2] = {0, 0};
+  int& bps = per_sm[multi ? 1 : 0];
+  if (!bps) bps = blocks_per_sm(kern, kMaxKeys * 4);
+  const uint64_t tiles = (nvec + static_cast<uint64_t>(kThreads) * T::U - 1) /
+                         (static_cast<uint64_t>(kThreads) * T::U);
+  const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * bps));
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(
+      static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, keys, nkeys,
+      stamp, static_cast<const uint8_t*>(src) + nvec * T::EPV * es,
+      static_cast<uint8_t*>(dst) + nvec * T::EPV * es, ntail, elem_base + nvec * T::EPV);
+  return cudaGetLastError();
+}
+
+template <int DT>
+cudaError_t run_scalar(const void* src, void* dst, uint64_t count, uint64_t elem_base,
+                       const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
+  const uint64_t blocks = std::max<uint64_t>(
+      1, std::min<uint64_t>((count + kThreads - 1) / kThreads, static_cast<uint64_t>(sm_count()) * 8));
+  synth_reduce_scalar<DT><<<static_cast<unsigned>(blocks), kThreads, static_cast<size_t>(nkeys) * 4, s>>>(
+      src, dst, count, elem_base, keys, nkeys, stamp);
+  return cudaGetLastError();
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t count,
+                                uint64_t elem_base, const uint32_t* d_keys, uint32_t nkeys,
+                                int64_t* stamp, cudaStream_t s, int* launches) {
+  if (nkeys > kMaxKeys) return cudaErrorInvalidValue;
+  if (count == 0) return cudaSuccess;
+  ++*launches;
+  // vector path: 16-byte aligned pointers, payload words aligned to vectors
+  const bool al = aligned16(src) && aligned16(dst);
+  const bool word_al = (elem_base % 4) == 0;
+  switch (dtype) {
+    case cemuFloat32:
+      if (al && word_al) return run_vec<kF32, cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      return run_scalar<cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    case cemuBfloat16:
+      if (al && word_al) return run_vec<kBF16, cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      return run_scalar<cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    case cemuFloat16:
+      if (al && word_al) return run_vec<kF16, cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      return run_scalar<cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    case cemuUint8:
+      if (al && word_al) return run_vec<kU8, cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      return run_scalar<cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    case cemuInt8:
+      if (al && word_al) return run_vec<kU8, cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      return run_scalar<cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    case cemuInt32:
+      if (al) return run_vec<kI32, cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      return run_scalar<cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    case cemuUint32:
+      if (al) return run_vec<kI32, cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      return run_scalar<cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    case cemuInt64: return run_scalar<cemuInt64>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    case cemuUint64: return run_scalar<cemuUint64>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    case cemuFloat64: return run_scalar<cemuFloat64>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+    default: --*launches; return cudaErrorInvalidValue;
+  }
+}
+
+namespace {
+template <int K>
+cudaError_t fill_vec(void* dst, uint64_t block_elems, const uint32_t* idx, const uint32_t* keys,
+                     uint32_t nblocks, uint32_t index0, uint32_t key0, const void* own,
+                     uint32_t own_index, int64_t* stamp, cudaStream_t s) {
+  const uint64_t nvec = block_elems / VT<K>::EPV;
+  const uint32_t ny = nblocks + (own ? 1 : 0);
+  const uint64_t want = (nvec + kThreads - 1) / kThreads;
+  const uint64_t cap = std::max<uint64_t>(1, static_cast<uint64_t>(sm_count()) * 8 / std::max<uint32_t>(ny, 1));
+  const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(1, std::min(want, cap)));
+  synth_fill_vec<K><<<dim3(gx, ny), kThreads, 0, s>>>(static_cast<uint4*>(dst), nvec, idx, keys, nblocks,
+                                                      index0, key0, static_cast<const uint4*>(own),
+                                                      own_index, stamp);
+  return cudaGetLastError();
+}
+
+template <int DT>
+cudaError_t fill_scalar(void* dst, uint64_t block_elems, const uint32_t* idx, const uint32_t* keys,
+                        uint32_t nblocks, uint32_t index0, uint32_t key0, const void* own,
+                        uint32_t own_index, int64_t* stamp, cudaStream_t s, int es) {
+  const uint32_t ny = nblocks + (own ? 1 : 0);
+  const uint64_t want = (block_elems * es + kThreads - 1) / kThreads;
+  const uint64_t cap = std::max<uint64_t>(1, static_cast<uint64_t>(sm_count()) * 8 / std::max<uint32_t>(ny, 1));
+  const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(1, std::min(want, cap)));
+  synth_fill_scalar<DT><<<dim3(gx, ny), kThreads, 0, s>>>(dst, block_elems, idx, keys, nblocks, index0,
+                                                          key0, own, own_index, stamp, es);
+  return cudaGetLastError();
+}
+
+int dsize(int dt) {
+  switch (dt) {
+    case cemuInt8: case cemuUint8: return 1;
+    case cemuFloat16: case cemuBfloat16: return 2;
+    case cemuInt32: case cemuUint32: case cemuFloat32: return 4;
+    default: return 8;
+  }
+}
+}  // namespace
+
+cudaError_t launch_synth_fill(int dtype, void* dst, uint64_t block_elems, const uint32_t* d_index,
+                              const uint32_t* d_keys, uint32_t nblocks, uint32_t index0,
+                              uint32_t key0, const void* own_src, uint32_t own_index,
+                              int64_t* stamp, cudaStream_t s, int* launches) {
+  if (block_elems == 0 || (nblocks == 0 && !own_src)) return cudaSuccess;
+  if (nblocks + 1 > 65535) return cudaErrorInvalidValue;
+  ++*launches;
+  const int es = dsize(dtype);
+  const bool al = aligned16(dst) && (!own_src || aligned16(own_src)) && (block_elems * es) % 16 == 0;
+  switch (dtype) {
+    case cemuFloat32:
+      if (al) return fill_vec<kF32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
+      return fill_scalar<cemuFloat32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+    case cemuBfloat16:
+      if (al) return fill_vec<kBF16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
+      return fill_scalar<cemuBfloat16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+    case cemuFloat16:
+      if (al) return fill_vec<kF16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
+      return fill_scalar<cemuFloat16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+    case cemuInt8: case cemuUint8:
+      if (al) return fill_vec<kU8>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
+      return fill_scalar<cemuUint8>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+    case cemuInt32: case cemuUint32:
+      if (al) return fill_vec<kI32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
+      return fill_scalar<cemuUint32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+    case cemuInt64: case cemuUint64:
+      return fill_scalar<cemuUint64>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+    case cemuFloat64:
+      return fill_scalar<cemuFloat64>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+    default: --*launches; return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_stamp(int64_t* slot, cudaStream_t s, int* launches) {
+  ++*launches;
+  stamp_kernel<<<1, 1, 0, s>>>(slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t s, int* launches) {
+  ++*launches;
+  delay_spin_kernel<<<1, kThreads, 0, s>>>(d, slot);
+  return cudaGetLastError();
+}
+
+}  // namespace cemu_b200

@@ -1,0 +1,53 @@
+// kernels.hpp -- launch API of the sm_100a kernels (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cemu_b200.h"
+
+namespace cemu_b200 {
+
+// Per-call record slot in device memory (int64 words):
+//   [0] t_start_ns  [1] t_end_ns  [2] device max floor (us)  [3] K
+//   [4..7] reserved
+//   [8 .. 8+kmax)            floors_us[j]
+//   [8+kmax .. 8+2kmax)      release_ns[j]   (%globaltimer at release)
+//   [8+2kmax .. 8+3kmax)     offsets_us[j]   (double bits)
+constexpr int kSlotHeader = 8;
+inline size_t slot_words(uint32_t kmax) { return kSlotHeader + 3 * static_cast<size_t>(kmax); }
+
+struct DelayLaunch {
+  cemuDelayModel model;
+  int32_t coll;
+  uint32_t n;
+  uint64_t bytes;
+  uint32_t k;
+  uint32_t kmax;
+  int32_t self_stamp;  // 1: this kernel records t_start itself
+};
+
+// dst[i] = src[i] (+) sum over `nkeys` emulated peers of their payload at
+// element elem_base + i.  src may equal dst.  Returns the number of kernel
+// launches issued through *launches.
+cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t count,
+                                uint64_t elem_base, const uint32_t* d_keys, uint32_t nkeys,
+                                int64_t* stamp, cudaStream_t stream, int* launches);
+
+// Writes whole per-rank blocks: for b in [0, nblocks) block dst_index[b]
+// (elements [dst_index[b]*block_elems, +block_elems) of dst) is filled with
+// the payload of key[b]; if own_src != nullptr, block own_index is copied
+// from own_src.  d_index/d_keys may be null when nblocks == 1, then
+// index0/key0 are used.
+cudaError_t launch_synth_fill(int dtype, void* dst, uint64_t block_elems,
+                              const uint32_t* d_index, const uint32_t* d_keys, uint32_t nblocks,
+                              uint32_t index0, uint32_t key0, const void* own_src,
+                              uint32_t own_index, int64_t* stamp, cudaStream_t stream,
+                              int* launches);
+
+cudaError_t launch_stamp(int64_t* slot, cudaStream_t stream, int* launches);
+cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t stream,
+                              int* launches);
+
+}  // namespace cemu_b200
