@@ -1,0 +1,430 @@
+"""Benchmark of the emulated-collective hot path (one JSON line on stdout).
+
+Workload (BASELINE.json north-star target): an emulated 1 GiB fp32 allreduce
+per real GPU in a world of 8 ranks per real GPU (N=1: 1 real + 7 emulated
+ranks), ring, payload = counter-based hash, delay model off for throughput
+(the injected-delay error is measured separately and reported in
+`delay_error`).  A "step" is one allreduce of the 1 GiB buffer.
+
+  value   whole-job emulated-allreduce throughput in algorithmic HBM GB/s
+          (2 x buffer bytes per step per GPU: read local, write result;
+          synthesised peers cost no bytes), inputs resident in HBM
+  e2e     the same metric through the C-ABI with the buffer coming from and
+          going back to pinned HOST memory every step (H2D + call + D2H)
+
+`python bench.py --impl reference` times the reference's own CPU emulator
+(cemu_core from /root/reference, prebuilt in oracle/_ref) on the same
+config over loopback TCP.  Under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "emulated allreduce GB/s vs HBM roofline"
+UNIT = "GB/s"
+PEAK_FALLBACK_GBS = 6650.0
+RANKS_PER_GPU = 8
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--mib", type=int, default=1024, help="buffer per real GPU (MiB)")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def world_config(n_gpus: int, extra: str = "") -> str:
+    W = RANKS_PER_GPU * n_gpus
+    real = ",".join(str(r) for r in range(n_gpus))
+    return f"world_size = {W}\nreal_ranks = {real}\nbucket_bytes = 26214400\n" + extra
+
+
+def workload(args, n):
+    return {"workload": f"allreduce fp32 {args.mib} MiB per real GPU, world {RANKS_PER_GPU * n} "
+                        f"({n} real + {RANKS_PER_GPU * n - n} emulated ranks), ring, hash payload, "
+                        "delay model off (delay error reported separately)",
+            "buffer_bytes_per_gpu": args.mib << 20, "world": RANKS_PER_GPU * n, "real_gpus": n,
+            "emulated_ranks": RANKS_PER_GPU * n - n, "dtype": "fp32",
+            "l2_policy": "inputs larger than L2 (1 GiB >> 126 MB)",
+            "parallelism": f"{n} real GPU(s), NCCL RS/AG among them + per-GPU synthesis"}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU emulator (oracle/_ref = cemu_core built from /root/reference)
+# ---------------------------------------------------------------------------
+REF_SAMPLE_MIB = 64  # the reference's 64 MiB frame cap rejects 1 GiB at world 8
+
+
+def time_reference(steps: int, warmup: int, world: int):
+    import numpy as np
+    from oracle import ref
+    sample = REF_SAMPLE_MIB << 20
+    buf = np.random.default_rng(1).integers(0, 2**31, size=sample // 4, dtype=np.int64).astype(np.int32)
+    times = ref.emulated_collective(world, 0, buf, sample, 4, kind=0, warmup=warmup, reps=steps)
+    mean_us = float(np.mean(times))
+    return {"value": 2 * sample / (mean_us * 1e-6) / 1e9, "mean_ms": mean_us / 1e3,
+            "best_ms": float(np.min(times)) / 1e3, "sample_bytes": sample, "calls": steps}
+
+
+def cpu_baseline_block(steps: int, warmup: int, world: int):
+    from oracle import ref
+    if ref.available():
+        r = time_reference(steps, warmup, world)
+        return {"value": round(r["value"], 4), "unit": UNIT, "cores": 5, "kind": "reference",
+                "sample": (f"reference cemu WorkerSession(rank 0) + in-thread EmulatorServer over loopback "
+                           f"TCP, world {world}, {REF_SAMPLE_MIB} MiB elem_size=4 allreduce (1 GiB exceeds its "
+                           f"64 MiB frame cap at world 8), {steps} timed calls after {warmup} warm-up; "
+                           f"mean {r['mean_ms']:.1f} ms/call, best {r['best_ms']:.1f} ms; 5 threads "
+                           f"(engine, reader, acceptor, emulator receive, poller) on a {os.cpu_count()}-core host"),
+                "mean_ms_per_call": round(r["mean_ms"], 3)}
+    # the port, single thread (only if the reference was never built)
+    import numpy as np
+    from oracle import port
+    n = (REF_SAMPLE_MIB << 20) // 4
+    x = np.zeros(n, dtype=np.float32)
+    t0 = time.perf_counter()
+    for _ in range(max(1, steps // 10)):
+        port.allreduce(7, 0, world, [0], 0, 1, [x], n)
+    dt = (time.perf_counter() - t0) / max(1, steps // 10)
+    return {"value": round(2 * n * 4 / dt / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle C port, {REF_SAMPLE_MIB} MiB fp32, world {world}"}
+
+
+def run_reference_arm(args, rank):
+    n = args.gpus
+    if rank != 0:
+        return
+    world = RANKS_PER_GPU * n
+    from oracle import ref
+    if ref.available():
+        r = time_reference(args.steps, args.warmup, world)
+        cb = {"value": round(r["value"], 4), "unit": UNIT, "cores": 5, "kind": "reference",
+              "sample": (f"each step = one reference emulated allreduce of {REF_SAMPLE_MIB} MiB (elem_size 4) "
+                         f"at world {world} over loopback TCP; 1 GiB exceeds the reference's 64 MiB frame cap")}
+    else:
+        cb = cpu_baseline_block(args.steps, args.warmup, world)
+        r = {"mean_ms": None}
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["mean_ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32 (elem_size 4 lanes)", "data": "synthetic",
+            "config": workload(args, n), "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = [r.split(", ") for r in getattr(self, "out", "").strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+def clocks_ok(c):
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if bad & set(c.get("reasons", [])):
+        return False
+    if c.get("sm_mhz") and c.get("sm_max_mhz") and c["sm_mhz"] < 0.6 * c["sm_max_mhz"] and not c["reasons"]:
+        return False
+    return True
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except (OSError, KeyError, ValueError):
+        return PEAK_FALLBACK_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(buffer_bytes):
+    """dram bytes per launch of the hot kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        if int(d.get("buffer_bytes", -1)) == buffer_bytes:
+            return int(d["dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        pass
+    return None
+
+
+def delay_error_block(torch, pb, device):
+    """Second half of the metric: injected-delay error vs the model."""
+    out = {}
+    cfg = world_config(1, "delay.kind = alpha_beta\nlink.alpha_us = 10\nlink.beta_us_per_byte = 0.001\n"
+                          "link.gamma_us_per_byte = 0.0001\n")
+    comm = pb.Communicator(cfg, 0, device)
+    x = torch.zeros(16 << 20, device=device)
+    errs, meas = [], []
+    for _ in range(4):
+        comm.all_reduce(x, x)
+        torch.cuda.synchronize(device)
+        rec = comm.call_record()
+        m = (rec["t_end_ns"] - rec["t_start_ns"]) / 1e3
+        meas.append(round(m, 3))
+        errs.append(abs(m - rec["model_latency_us"]))
+    out["config1_alpha_beta_64MiB_world8"] = {
+        "model_us": rec["model_latency_us"], "measured_us": meas,
+        "max_err_us": round(max(errs), 3), "max_err_pct": round(100 * max(errs) / rec["model_latency_us"], 5),
+        "floors_us": rec["floors_us"].tolist()}
+    comm.close()
+    probes = {}
+    for inject in (100, 1000, 5000):
+        comm = pb.Communicator("world_size = 2\nreal_ranks = 0\nbucket_bytes = 1\n"
+                               f"delay.inject_us = {inject}\n", 0, device)
+        y = torch.zeros(1024, device=device)
+        es = []
+        for _ in range(10):
+            comm.all_reduce(y, y)
+            torch.cuda.synchronize(device)
+            rec = comm.call_record()
+            es.append((rec["t_end_ns"] - rec["t_start_ns"]) / 1e3 - inject)
+        probes[f"inject_{inject}us_world2_4KiB"] = {"mean_err_us": round(statistics.mean(es), 3),
+                                                    "max_abs_err_us": round(max(abs(e) for e in es), 3)}
+        comm.close()
+    out["whatif_inject_probes"] = probes
+    out["tolerance"] = "max(1% of model, 2 us)"
+    model = out["config1_alpha_beta_64MiB_world8"]["model_us"]
+    out["pass"] = max(errs) <= max(0.01 * model, 2.0) and \
+        all(p["max_abs_err_us"] <= max(0.01 * int(k.split("_")[1][:-2]), 2.0) for k, p in probes.items())
+    return out
+
+
+def sweep_block(torch, pb, device):
+    """Config 2 shape (single B200 emulating a 64-rank ring): algorithmic HBM
+    GB/s per collective, fp32 and bf16, 4 KiB .. 1 GiB (powers of 4)."""
+    comm = pb.Communicator("world_size = 64\nreal_ranks = 0\nbucket_bytes = 1\n", 0, device)
+    res = {}
+    sizes = [4 << 10 << (2 * i) for i in range(10)]  # 4 KiB .. 1 GiB
+    for dname, dt in (("fp32", torch.float32), ("bf16", torch.bfloat16)):
+        es = torch.empty(0, dtype=dt).element_size()
+        for coll in ("allreduce", "allgather", "reducescatter"):
+            pts = []
+            for size in sizes:
+                n = size // es
+                if coll == "allreduce":
+                    x = torch.zeros(n, dtype=dt, device=device)
+                    fn, algo = (lambda: comm.all_reduce(x, x)), 2 * size
+                elif coll == "allgather":
+                    s = max(n // 64, 1)
+                    x = torch.zeros(s * 64, dtype=dt, device=device)
+                    fn, algo = (lambda: comm.all_gather(x[:s], x)), (64 - 1) * s * es  # in place
+                else:
+                    r = max(n // 64, 1)
+                    x = torch.zeros(r * 64, dtype=dt, device=device)
+                    y = torch.zeros(r, dtype=dt, device=device)
+                    fn, algo = (lambda: comm.reduce_scatter(x, y)), 2 * r * es
+                reps = 20 if size <= (64 << 20) else 5
+                for _ in range(3):
+                    fn()
+                e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+                e0.record()
+                for _ in range(reps):
+                    fn()
+                e1.record()
+                torch.cuda.synchronize(device)
+                us = e0.elapsed_time(e1) * 1e3 / reps
+                pts.append([size, round(us, 2), round(algo / (us * 1e-6) / 1e9, 1)])
+                del x
+            res[f"{coll}_{dname}"] = pts
+    comm.close()
+    return {"world": 64, "columns": ["buffer_bytes", "us_per_call", "algorithmic_GB/s"],
+            "note": "allgather: in place, (n-1)*block written; reduce-scatter: own chunk read + written; "
+                    "small sizes are launch-latency bound (L2-resident, back-to-back)", **res}
+
+
+def run_ours(args, rank, world_size, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_02969_b200 as pb
+
+    n = args.gpus
+    device = local_rank
+    torch.cuda.set_device(device)
+    if n > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        obj = [pb.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    else:
+        uid = None
+    comm = pb.Communicator(world_config(n), rank, device, uid)
+    nbytes = args.mib << 20
+    count = nbytes // 4
+    g = torch.Generator(device="cuda").manual_seed(rank)
+    x = torch.randn(count, device="cuda", generator=g)
+    y = torch.empty_like(x)
+
+    def barrier():
+        if n > 1:
+            dist.barrier(device_ids=[device])
+        torch.cuda.synchronize(device)
+
+    def max_over_ranks(v):
+        if n == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.current_stream(device)
+    for _ in range(args.warmup):
+        comm.all_reduce(x, y)
+    barrier()
+
+    def timed():
+        launches0 = comm.kernel_launches
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        barrier()
+        with Clocks(device) as clk:
+            evs[0].record(stream)
+            for i in range(args.steps):
+                comm.all_reduce(x, y)
+                evs[i + 1].record(stream)
+            torch.cuda.synchronize(device)
+        barrier()
+        per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+        return sum(per), per, comm.kernel_launches - launches0, clk.summary()
+
+    total_ms, per_ms, launches, clocks = timed()
+    if not clocks_ok(clocks):
+        total_ms, per_ms, launches, clocks = timed()
+        clocks["remeasured"] = True
+    total_ms = max_over_ranks(total_ms)
+    ms_per_step = total_ms / args.steps
+    value = n * 2 * nbytes * args.steps / (total_ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (synth_reduce_vec<fp32>): at N=1 the call
+    # is exactly one launch of it, so the per-launch duration is the step time
+    peak, peak_src = measured_peak()
+    kernel_ms = statistics.mean(per_ms) if n == 1 else None
+    if n == 1:
+        achieved = 2 * nbytes / (kernel_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic(nbytes),
+                    "kernel": "synth_reduce_vec<fp32> (1 launch per step)",
+                    "algorithmic_bytes_per_launch": 2 * nbytes, "peak_source": peak_src,
+                    "kernel_ms_mean": round(kernel_ms, 5), "kernel_ms_min": round(min(per_ms), 5)}
+    else:
+        achieved = 2 * nbytes / (ms_per_step * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": None,
+                    "kernel": "per-GPU step: NCCL reduce-scatter + synth_reduce_vec<fp32> + NCCL allgather",
+                    "peak_source": peak_src}
+
+    # e2e: pinned host buffers in and out every step, through the C-ABI
+    h_in = torch.randn(count, generator=torch.Generator().manual_seed(rank)).pin_memory()
+    h_out = torch.empty(count, dtype=torch.float32).pin_memory()
+    e2e_steps = max(1, min(args.steps, 10))
+    for _ in range(2):
+        x.copy_(h_in, non_blocking=True)
+        comm.all_reduce(x, y)
+        h_out.copy_(y, non_blocking=True)
+    barrier()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        x.copy_(h_in, non_blocking=True)
+        comm.all_reduce(x, y)
+        h_out.copy_(y, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+    e2e = {"value": round(n * 2 * nbytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": UNIT,
+           "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(e2e_ms, 3),
+           "path": "pinned host -> cudaMemcpyAsync -> cemuAllReduce (C-ABI) -> cudaMemcpyAsync -> pinned host"}
+
+    extra = {}
+    if rank == 0 and n == 1:
+        extra["delay_error"] = delay_error_block(torch, pb, device)
+        if not args.no_sweep:
+            extra["sweep_config2"] = sweep_block(torch, pb, device)
+        if not args.no_cpu_baseline:
+            extra["cpu_baseline"] = cpu_baseline_block(20, 2, RANKS_PER_GPU)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": n, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+                "config": workload(args, n), "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clocks, **extra}
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if n > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world_size != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world_size}")
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+    else:
+        run_ours(args, rank, world_size, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -350,15 +350,15 @@ uint32_t or_payload_key(uint64_t seed, uint32_t rank) {
 }
 
 /* Counter-based 32-bit word j of a rank's payload stream: a Weyl counter
- * XOR the key, then two multiply/xorshift rounds. */
+ * plus the key, a multiply, an xorshift, a multiply by the (odd) key, and an
+ * add-shift. */
 uint32_t or_payload_word(uint32_t key, uint64_t j) {
   uint32_t ctr = (uint32_t)j * 0x9E3779B9u;
   ctr ^= (uint32_t)(j >> 32) * 0x85EBCA77u;
-  uint32_t x = key ^ ctr;
-  x *= 0x7FEB352Du;
+  uint32_t x = (key + ctr) * 0x7FEB352Du;
   x ^= x >> 15;
-  x *= 0x846CA68Bu;
-  x ^= x >> 16;
+  x *= key | 1u;
+  x += x >> 16;
   return x;
 }
 

@@ -148,7 +148,7 @@ class Communicator:
             raise CemuError(_capi.INVALID_ARGUMENT,
                             f"reduce_scatter: send has {send.numel()} elements, expected "
                             f"{recv.numel()} x {self.world_size}")
-        self._check_same(send, recv, send.numel())
+        self._check_same(send, recv, recv.numel())
         check(lib.cemuReduceScatter(_ptr(send), _ptr(recv), recv.numel(), dtype_code(send.dtype), 0,
                                     self._h, _stream_ptr(stream)), self._h)
         return recv

@@ -33,7 +33,7 @@ namespace cemu_b200 {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr uint32_t kMaxKeys = 4096;  // smem key table (16 KB) upper bound
+constexpr uint32_t kMaxKeys = 4096;  // smem (k1, km) table (32 KB) upper bound
 
 __device__ __forceinline__ int64_t globaltimer_ns() {
   uint64_t t;
@@ -106,26 +106,33 @@ template <> struct VT<kI32>  { static constexpr int EPV = 4,  WPV = 4, U = 4; st
 // ---------------------------------------------------------------------------
 // generic per-element path (all 10 datatypes)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t pbyte(uint32_t key, uint64_t e) {
-  return (payload_word(key, e >> 2) >> (8 * (e & 3))) & 0xFFu;
+// per-peer hash constants live in shared memory as (k1, km) pairs
+__device__ __forceinline__ uint32_t pword(uint2 k, uint64_t j) { return payload_mix(k.x, k.y, payload_c1(j)); }
+
+__device__ __forceinline__ uint32_t pbyte(uint2 k, uint64_t e) {
+  return (pword(k, e >> 2) >> (8 * (e & 3))) & 0xFFu;
+}
+
+__device__ __forceinline__ uint2 peer_consts(uint32_t key) {
+  return make_uint2(payload_k1(key), payload_km(key));
 }
 
 template <int DT>
 __device__ void elem_reduce(const void* src, void* dst, uint64_t i, uint64_t e,
-                            const uint32_t* keys, uint32_t nkeys) {
+                            const uint2* keys, uint32_t nkeys) {
   if constexpr (DT == cemuInt8 || DT == cemuUint8) {
     uint32_t acc = static_cast<const uint8_t*>(src)[i];
     for (uint32_t q = 0; q < nkeys; ++q) acc += pbyte(keys[q], e);
     static_cast<uint8_t*>(dst)[i] = static_cast<uint8_t>(acc);
   } else if constexpr (DT == cemuInt32 || DT == cemuUint32) {
     uint32_t acc = static_cast<const uint32_t*>(src)[i];
-    for (uint32_t q = 0; q < nkeys; ++q) acc += payload_word(keys[q], e);
+    for (uint32_t q = 0; q < nkeys; ++q) acc += pword(keys[q], e);
     static_cast<uint32_t*>(dst)[i] = acc;
   } else if constexpr (DT == cemuInt64 || DT == cemuUint64) {
     uint64_t acc = static_cast<const uint64_t*>(src)[i];
     for (uint32_t q = 0; q < nkeys; ++q) {
-      acc += static_cast<uint64_t>(payload_word(keys[q], 2 * e)) |
-             (static_cast<uint64_t>(payload_word(keys[q], 2 * e + 1)) << 32);
+      acc += static_cast<uint64_t>(pword(keys[q], 2 * e)) |
+             (static_cast<uint64_t>(pword(keys[q], 2 * e + 1)) << 32);
     }
     static_cast<uint64_t*>(dst)[i] = acc;
   } else {
@@ -147,14 +154,15 @@ __device__ void elem_reduce(const void* src, void* dst, uint64_t i, uint64_t e,
 }
 
 template <int DT>
-__device__ void elem_fill(void* dst, uint64_t i, uint64_t e, uint32_t key) {
+__device__ void elem_fill(void* dst, uint64_t i, uint64_t e, uint32_t raw_key) {
+  const uint2 key = peer_consts(raw_key);
   if constexpr (DT == cemuInt8 || DT == cemuUint8) {
     static_cast<uint8_t*>(dst)[i] = static_cast<uint8_t>(pbyte(key, e));
   } else if constexpr (DT == cemuInt32 || DT == cemuUint32) {
-    static_cast<uint32_t*>(dst)[i] = payload_word(key, e);
+    static_cast<uint32_t*>(dst)[i] = pword(key, e);
   } else if constexpr (DT == cemuInt64 || DT == cemuUint64) {
-    static_cast<uint64_t*>(dst)[i] = static_cast<uint64_t>(payload_word(key, 2 * e)) |
-                                     (static_cast<uint64_t>(payload_word(key, 2 * e + 1)) << 32);
+    static_cast<uint64_t*>(dst)[i] = static_cast<uint64_t>(pword(key, 2 * e)) |
+                                     (static_cast<uint64_t>(pword(key, 2 * e + 1)) << 32);
   } else {
     const int32_t s = static_cast<int32_t>(pbyte(key, e)) - 128;
     if constexpr (DT == cemuFloat64) {
@@ -169,8 +177,8 @@ __device__ void elem_fill(void* dst, uint64_t i, uint64_t e, uint32_t key) {
   }
 }
 
-__device__ __forceinline__ void load_keys(uint32_t* skeys, const uint32_t* keys, uint32_t nkeys) {
-  for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x) skeys[i] = keys[i];
+__device__ __forceinline__ void load_keys(uint2* skeys, const uint32_t* keys, uint32_t nkeys) {
+  for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x) skeys[i] = peer_consts(keys[i]);
   __syncthreads();
 }
 
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_scalar(const void* src,
                                                                 uint64_t count, uint64_t elem_base,
                                                                 const uint32_t* keys,
                                                                 uint32_t nkeys, int64_t* stamp) {
-  extern __shared__ uint32_t skeys[];
+  extern __shared__ uint2 skeys[];
   if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
   load_keys(skeys, keys, nkeys);
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     void* tail_dst, uint32_t ntail, uint64_t tail_e0) {
   using T = VT<K>;
   constexpr int U = T::U, W = T::WPV, NW = U * W;
-  extern __shared__ uint32_t skeys[];
+  extern __shared__ uint2 skeys[];
   if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
   load_keys(skeys, keys, nkeys);
 
@@ -219,7 +227,7 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
 #pragma unroll
-      for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_ctr(word_base + v * W + w);
+      for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(word_base + v * W + w);
     }
 
     uint4 y[U];
@@ -230,9 +238,9 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
       for (int i = 0; i < NW; ++i) acc[i] = 0;
 #pragma unroll 2
       for (uint32_t q = 0; q < nkeys; ++q) {
-        const uint32_t key = skeys[q];
+        const uint2 key = skeys[q];
 #pragma unroll
-        for (int i = 0; i < NW; ++i) acc[i] += payload_mix(key, ctr[i]);
+        for (int i = 0; i < NW; ++i) acc[i] += payload_mix(key.x, key.y, ctr[i]);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -255,22 +263,17 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
         for (int i = 0; i < NW; ++i) lo[i] = hi[i] = 0;
 #pragma unroll 2
         for (uint32_t q = q0; q < q1; ++q) {
-          const uint32_t key = skeys[q];
+          const uint2 key = skeys[q];
 #pragma unroll
           for (int i = 0; i < NW; ++i) {
-            const uint32_t h = payload_mix(key, ctr[i]);
+            const uint32_t h = payload_mix(key.x, key.y, ctr[i]);
             lo[i] += h & 0x00FF00FFu;
             hi[i] += __byte_perm(h, 0u, 0x4341);
           }
         }
-        if constexpr (K == kU8) {
-          // mod-2^16 lanes keep every byte sum exact mod 256: no grouping
-#pragma unroll
-          for (int i = 0; i < NW; ++i) {
-            s[i * 4 + 0] = static_cast<int32_t>((lo[i] & 0x00FF00FFu) | ((hi[i] & 0x00FF00FFu) << 8));
-          }
-        } else {
-          const int32_t bias = 128 * static_cast<int32_t>(q1 - q0);
+        {
+          // float kinds carry the -128 offset of the dyadic value; bytes wrap
+          const int32_t bias = K == kU8 ? 0 : 128 * static_cast<int32_t>(q1 - q0);
 #pragma unroll
           for (int i = 0; i < NW; ++i) {
             s[i * 4 + 0] += static_cast<int32_t>(lo[i] & 0xFFFFu) - bias;
@@ -302,11 +305,18 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
             y[u].z = fold_f16x2(x[u].z, t1[0], t1[1]);
             y[u].w = fold_f16x2(x[u].w, t1[2], t1[3]);
           }
-        } else {  // kU8
-          y[u].x = add_bytes(x[u].x, static_cast<uint32_t>(s[(u * 4 + 0) * 4]));
-          y[u].y = add_bytes(x[u].y, static_cast<uint32_t>(s[(u * 4 + 1) * 4]));
-          y[u].z = add_bytes(x[u].z, static_cast<uint32_t>(s[(u * 4 + 2) * 4]));
-          y[u].w = add_bytes(x[u].w, static_cast<uint32_t>(s[(u * 4 + 3) * 4]));
+        } else {  // kU8: byte e of word i is lane sum s[4i + e] mod 256
+          uint32_t p[4];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int32_t* t = s + (u * 4 + w) * 4;
+            p[w] = (static_cast<uint32_t>(t[0]) & 0xFFu) | ((static_cast<uint32_t>(t[1]) & 0xFFu) << 8) |
+                   ((static_cast<uint32_t>(t[2]) & 0xFFu) << 16) | (static_cast<uint32_t>(t[3]) << 24);
+          }
+          y[u].x = add_bytes(x[u].x, p[0]);
+          y[u].y = add_bytes(x[u].y, p[1]);
+          y[u].z = add_bytes(x[u].z, p[2]);
+          y[u].w = add_bytes(x[u].w, p[3]);
         }
       }
     }
@@ -326,11 +336,11 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
 // fills
 // ---------------------------------------------------------------------------
 template <int K>
-__device__ __forceinline__ uint4 synth_vector(uint32_t key, uint64_t word0) {
+__device__ __forceinline__ uint4 synth_vector(uint2 key, uint64_t word0) {
   using T = VT<K>;
   uint32_t wd[T::WPV];
 #pragma unroll
-  for (int w = 0; w < T::WPV; ++w) wd[w] = payload_word(key, word0 + w);
+  for (int w = 0; w < T::WPV; ++w) wd[w] = pword(key, word0 + w);
   uint4 r;
   if constexpr (K == kU8 || K == kI32) {
     r.x = wd[0];
@@ -379,7 +389,7 @@ __global__ void __launch_bounds__(kThreads) synth_fill_vec(uint4* dst, uint64_t 
   const uint32_t b = blockIdx.y;
   const bool copy = b == nblocks;
   const uint32_t idx = copy ? own_index : (index ? index[b] : index0);
-  const uint32_t key = copy ? 0u : (keys ? keys[b] : key0);
+  const uint2 key = peer_consts(copy ? 0u : (keys ? keys[b] : key0));
   uint4* out = dst + static_cast<uint64_t>(idx) * nvec_per_block;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec_per_block;
@@ -467,10 +477,16 @@ __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int
 // launch helpers
 // ---------------------------------------------------------------------------
 int sm_count() {
-  int dev = 0, sms = 0;
+  static int cached[64] = {0};
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms > 0 ? sms : 148;
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = sms > 0 ? sms : 148;
+  }
+  return cached[dev];
 }
 
 template <typename Kern>
@@ -491,12 +507,12 @@ cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_ba
   const uint32_t ntail = static_cast<uint32_t>(count - nvec * T::EPV);
   const size_t es = T::kWords ? 4 : (K == kF32 ? 4 : (K == kU8 ? 1 : 2));
   const uint64_t word_base = T::kWords ? elem_base : elem_base / 4;
-  const size_t smem = static_cast<size_t>(nkeys) * 4;
-  const bool multi = !T::kWords && K != kU8 && nkeys > 256;
+  const size_t smem = static_cast<size_t>(nkeys) * 8;
+  const bool multi = !T::kWords && nkeys > 256;  // 16-bit lanes hold <= 257 bytes
   auto kern = multi ? synth_reduce_vec<K, DT, true> : synth_reduce_vec<K, DT, false>;
   static int per_sm[2] = {0, 0};
   int& bps = per_sm[multi ? 1 : 0];
-  if (!bps) bps = blocks_per_sm(kern, kMaxKeys * 4);
+  if (!bps) bps = blocks_per_sm(kern, kMaxKeys * 8);
   const uint64_t tiles = (nvec + static_cast<uint64_t>(kThreads) * T::U - 1) /
                          (static_cast<uint64_t>(kThreads) * T::U);
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * bps));
@@ -512,7 +528,7 @@ cudaError_t run_scalar(const void* src, void* dst, uint64_t count, uint64_t elem
                        const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
   const uint64_t blocks = std::max<uint64_t>(
       1, std::min<uint64_t>((count + kThreads - 1) / kThreads, static_cast<uint64_t>(sm_count()) * 8));
-  synth_reduce_scalar<DT><<<static_cast<unsigned>(blocks), kThreads, static_cast<size_t>(nkeys) * 4, s>>>(
+  synth_reduce_scalar<DT><<<static_cast<unsigned>(blocks), kThreads, static_cast<size_t>(nkeys) * 8, s>>>(
       src, dst, count, elem_base, keys, nkeys, stamp);
   return cudaGetLastError();
 }

@@ -5,8 +5,15 @@
 //
 //   key(seed, rank)   32-bit per-rank key: the splitmix64 finalizer `mix` of
 //                     proj/tools/cemu_coll.cpp:22-31 (trial 0), folded to 32.
-//   word(key, j)      32-bit word j of the rank's stream: Weyl counter XOR
-//                     key, then two multiply/xorshift rounds.
+//   word(key, j)      32-bit word j of the rank's stream:
+//                       x  = (key + ctr(j)) * M1        ctr = Weyl counter of j
+//                       x ^= x >> 15
+//                       x *= key | 1                    key-dependent odd multiplier
+//                       x += x >> 16
+//                     (key + ctr) * M1 == key*M1 + ctr*M1, so kernels hoist
+//                     key*M1 per peer and ctr*M1 per word: per peer-word the
+//                     hash is 1 add, 1 xorshift, 1 IMAD, 1 IMAD.HI -- split
+//                     across the FMA and ALU pipes.
 //   byte(key, e)      byte (e & 3) of word(key, e >> 2).
 //
 // Element e of a rank's contribution, by datatype:
@@ -28,7 +35,6 @@ namespace cemu_b200 {
 constexpr uint32_t kWeyl = 0x9E3779B9u;
 constexpr uint32_t kWeylHi = 0x85EBCA77u;
 constexpr uint32_t kMul1 = 0x7FEB352Du;
-constexpr uint32_t kMul2 = 0x846CA68Bu;
 constexpr float kDyadicScale = 0.0078125f;  // 2^-7
 
 CEMU_HD uint32_t payload_key(uint64_t seed, uint32_t rank) {
@@ -41,23 +47,29 @@ CEMU_HD uint32_t payload_key(uint64_t seed, uint32_t rank) {
   return static_cast<uint32_t>(h ^ (h >> 32));
 }
 
-// The per-word counter; split out so kernels hoist it across peers.
-CEMU_HD uint32_t payload_ctr(uint64_t j) {
-  return static_cast<uint32_t>(j) * kWeyl ^
-         static_cast<uint32_t>(j >> 32) * kWeylHi;
+// The per-word counter, premultiplied by M1; kernels hoist it across peers.
+CEMU_HD uint32_t payload_c1(uint64_t j) {
+  return (static_cast<uint32_t>(j) * kWeyl ^ static_cast<uint32_t>(j >> 32) * kWeylHi) * kMul1;
 }
 
-CEMU_HD uint32_t payload_mix(uint32_t key, uint32_t ctr) {
-  uint32_t x = key ^ ctr;
-  x *= kMul1;
+// Per-peer constants: k1 = key * M1, km = key | 1.
+CEMU_HD uint32_t payload_k1(uint32_t key) { return key * kMul1; }
+CEMU_HD uint32_t payload_km(uint32_t key) { return key | 1u; }
+
+CEMU_HD uint32_t payload_mix(uint32_t k1, uint32_t km, uint32_t c1) {
+  uint32_t x = k1 + c1;
   x ^= x >> 15;
-  x *= kMul2;
-  x ^= x >> 16;
+  x *= km;
+#if defined(__CUDA_ARCH__)
+  x = __umulhi(x, 0x10000u) + x;  // x + (x >> 16) as one IMAD.HI (FMA pipe)
+#else
+  x += x >> 16;
+#endif
   return x;
 }
 
 CEMU_HD uint32_t payload_word(uint32_t key, uint64_t j) {
-  return payload_mix(key, payload_ctr(j));
+  return payload_mix(payload_k1(key), payload_km(key), payload_c1(j));
 }
 
 }  // namespace cemu_b200
