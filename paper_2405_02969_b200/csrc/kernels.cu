@@ -24,6 +24,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "delay_math.cuh"
 #include "kernels.hpp"
@@ -95,13 +96,12 @@ enum VKind { kF32 = 0, kF16 = 1, kBF16 = 2, kU8 = 3, kI32 = 4 };
 
 template <int K>
 struct VT;
-// EPV elements per 16-byte vector, WPV payload words per vector, U vectors
-// per thread per iteration (64 B in flight per thread for every kind).
-template <> struct VT<kF32>  { static constexpr int EPV = 4,  WPV = 1, U = 4; static constexpr bool kWords = false; };
-template <> struct VT<kF16>  { static constexpr int EPV = 8,  WPV = 2, U = 4; static constexpr bool kWords = false; };
-template <> struct VT<kBF16> { static constexpr int EPV = 8,  WPV = 2, U = 4; static constexpr bool kWords = false; };
-template <> struct VT<kU8>   { static constexpr int EPV = 16, WPV = 4, U = 4; static constexpr bool kWords = false; };
-template <> struct VT<kI32>  { static constexpr int EPV = 4,  WPV = 4, U = 4; static constexpr bool kWords = true; };
+// EPV elements per 16-byte vector, WPV payload words per vector.
+template <> struct VT<kF32>  { static constexpr int EPV = 4,  WPV = 1; static constexpr bool kWords = false; };
+template <> struct VT<kF16>  { static constexpr int EPV = 8,  WPV = 2; static constexpr bool kWords = false; };
+template <> struct VT<kBF16> { static constexpr int EPV = 8,  WPV = 2; static constexpr bool kWords = false; };
+template <> struct VT<kU8>   { static constexpr int EPV = 16, WPV = 4; static constexpr bool kWords = false; };
+template <> struct VT<kI32>  { static constexpr int EPV = 4,  WPV = 4; static constexpr bool kWords = true; };
 
 // ---------------------------------------------------------------------------
 // generic per-element path (all 10 datatypes)
@@ -200,13 +200,37 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_scalar(const void* src,
 // ---------------------------------------------------------------------------
 // the hot kernel
 // ---------------------------------------------------------------------------
-template <int K, int DT, bool kMulti>
+// acc + a on the FMA pipe: `one` is a runtime 1 (kernel argument), so ptxas
+// keeps an IMAD instead of folding it into an ALU-pipe IADD3.  The hash and
+// the byte extraction already saturate the ALU pipe (ncu: 93% ALU / 17% FMA
+// at 63 peers before this split).
+__device__ __forceinline__ uint32_t mad_add(uint32_t a, uint32_t one, uint32_t acc) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(one), "r"(acc));
+  return d;
+}
+
+// Per-word byte sums from the two accumulators of one peer group (<= 257
+// peers): A = sum of whole words (mod 2^32), H = sum of odd bytes in 16-bit
+// lanes (S1, S3).  The even-byte lanes follow exactly:
+//   S0 + S2 * 2^16 = A - S1 * 2^8 - S3 * 2^24  (mod 2^32)
+// so the mask of the even bytes is never computed per peer.
+__device__ __forceinline__ void decode_byte_sums(uint32_t a, uint32_t h, uint32_t s[4]) {
+  const uint32_t s1 = h & 0xFFFFu, s3 = h >> 16;
+  const uint32_t even = a - (s1 << 8) - (s3 << 24);
+  s[0] = even & 0xFFFFu;
+  s[1] = s1;
+  s[2] = even >> 16;
+  s[3] = s3;
+}
+
+template <int K, int DT, int U, bool kMulti>
 __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     const uint4* __restrict__ src, uint4* dst, uint64_t nvec, uint64_t word_base,
     const uint32_t* __restrict__ keys, uint32_t nkeys, int64_t* stamp, const void* tail_src,
-    void* tail_dst, uint32_t ntail, uint64_t tail_e0) {
+    void* tail_dst, uint32_t ntail, uint64_t tail_e0, uint32_t one) {
   using T = VT<K>;
-  constexpr int U = T::U, W = T::WPV, NW = U * W;
+  constexpr int W = T::WPV, NW = U * W;
   extern __shared__ uint2 skeys[];
   if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
   load_keys(skeys, keys, nkeys);
@@ -240,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
       for (uint32_t q = 0; q < nkeys; ++q) {
         const uint2 key = skeys[q];
 #pragma unroll
-        for (int i = 0; i < NW; ++i) acc[i] += payload_mix(key.x, key.y, ctr[i]);
+        for (int i = 0; i < NW; ++i) acc[i] = mad_add(payload_mix(key.x, key.y, ctr[i]), one, acc[i]);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -250,39 +274,39 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
         y[u].w = x[u].w + acc[u * 4 + 3];
       }
     } else {
-      // byte payloads summed in SWAR 16-bit lanes: lo = (b0, b2), hi = (b1, b3)
+      // 2. per-peer byte sums: S_e = sum over peers of byte e of the word,
+      //    accumulated as A (whole words) and H (odd bytes, 16-bit lanes)
       int32_t s[NW * 4];
-      uint32_t lo[NW], hi[NW];
       const uint32_t groups = kMulti ? (nkeys + 255) / 256 : 1;
 #pragma unroll
       for (int i = 0; i < NW * 4; ++i) s[i] = 0;
       for (uint32_t g = 0; g < groups; ++g) {
         const uint32_t q0 = g * 256;
         const uint32_t q1 = kMulti ? min(nkeys, q0 + 256) : nkeys;
+        uint32_t a[NW], h[NW];
 #pragma unroll
-        for (int i = 0; i < NW; ++i) lo[i] = hi[i] = 0;
+        for (int i = 0; i < NW; ++i) a[i] = h[i] = 0;
 #pragma unroll 2
         for (uint32_t q = q0; q < q1; ++q) {
           const uint2 key = skeys[q];
 #pragma unroll
           for (int i = 0; i < NW; ++i) {
-            const uint32_t h = payload_mix(key.x, key.y, ctr[i]);
-            lo[i] += h & 0x00FF00FFu;
-            hi[i] += __byte_perm(h, 0u, 0x4341);
+            const uint32_t w = payload_mix(key.x, key.y, ctr[i]);
+            a[i] = mad_add(w, one, a[i]);
+            h[i] = mad_add(__byte_perm(w, 0u, 0x4341), one, h[i]);
           }
         }
-        {
-          // float kinds carry the -128 offset of the dyadic value; bytes wrap
-          const int32_t bias = K == kU8 ? 0 : 128 * static_cast<int32_t>(q1 - q0);
+        // float kinds carry the -128 offset of the dyadic value; bytes wrap
+        const int32_t bias = K == kU8 ? 0 : 128 * static_cast<int32_t>(q1 - q0);
 #pragma unroll
-          for (int i = 0; i < NW; ++i) {
-            s[i * 4 + 0] += static_cast<int32_t>(lo[i] & 0xFFFFu) - bias;
-            s[i * 4 + 1] += static_cast<int32_t>(hi[i] & 0xFFFFu) - bias;
-            s[i * 4 + 2] += static_cast<int32_t>(lo[i] >> 16) - bias;
-            s[i * 4 + 3] += static_cast<int32_t>(hi[i] >> 16) - bias;
-          }
+        for (int i = 0; i < NW; ++i) {
+          uint32_t t[4];
+          decode_byte_sums(a[i], h[i], t);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s[i * 4 + e] += static_cast<int32_t>(t[e]) - bias;
         }
       }
+      // 3. one rounding per element: local (+) S * 2^-7
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if constexpr (K == kF32) {
@@ -305,7 +329,7 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
             y[u].z = fold_f16x2(x[u].z, t1[0], t1[1]);
             y[u].w = fold_f16x2(x[u].w, t1[2], t1[3]);
           }
-        } else {  // kU8: byte e of word i is lane sum s[4i + e] mod 256
+        } else {  // kU8: byte e of word i is S[4i + e] mod 256
           uint32_t p[4];
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
@@ -499,9 +523,35 @@ int blocks_per_sm(Kern k, size_t smem) {
   return b;
 }
 
-template <int K, int DT>
-cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_base,
-                    const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
+// Launch shape of the hot kernel: U vectors per thread per tile and resident
+// blocks per SM.  Few peers -> memory bound: small U, many resident warps
+// (ncu at 7 peers: 6.47 TB/s with U=2 x 4 blocks/SM).  Many peers -> ALU
+// bound: U=8 amortises the shared-memory key loads over more words.
+// CEMU_SYNTH_U / CEMU_SYNTH_BPS override both (tuning only).
+struct Shape {
+  int u;
+  int bps;
+};
+
+Shape pick_shape(int words_per_vec, uint32_t nkeys) {
+  static const int env_u = [] {
+    const char* e = std::getenv("CEMU_SYNTH_U");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int env_bps = [] {
+    const char* e = std::getenv("CEMU_SYNTH_BPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int u_max = 8 / words_per_vec;  // <= 8 payload words per thread per tile
+  Shape sh{nkeys * static_cast<uint32_t>(words_per_vec) <= 8 ? 2 : std::max(2, u_max), 0};
+  if ((env_u == 2 || env_u == 4 || env_u == 8) && env_u <= std::max(2, u_max)) sh.u = env_u;
+  if (env_bps > 0) sh.bps = env_bps;
+  return sh;
+}
+
+template <int K, int DT, int U>
+cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_base,
+                      const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s, int bps_req) {
   using T = VT<K>;
   const uint64_t nvec = count / T::EPV;
   const uint32_t ntail = static_cast<uint32_t>(count - nvec * T::EPV);
@@ -509,18 +559,32 @@ cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_ba
   const uint64_t word_base = T::kWords ? elem_base : elem_base / 4;
   const size_t smem = static_cast<size_t>(nkeys) * 8;
   const bool multi = !T::kWords && nkeys > 256;  // 16-bit lanes hold <= 257 bytes
-  auto kern = multi ? synth_reduce_vec<K, DT, true> : synth_reduce_vec<K, DT, false>;
+  auto kern = multi ? synth_reduce_vec<K, DT, U, true> : synth_reduce_vec<K, DT, U, false>;
   static int per_sm[2] = {0, 0};
-  int& bps = per_sm[multi ? 1 : 0];
-  if (!bps) bps = blocks_per_sm(kern, kMaxKeys * 8);
-  const uint64_t tiles = (nvec + static_cast<uint64_t>(kThreads) * T::U - 1) /
-                         (static_cast<uint64_t>(kThreads) * T::U);
+  int& occ = per_sm[multi ? 1 : 0];
+  if (!occ) occ = blocks_per_sm(kern, kMaxKeys * 8);
+  const int bps = bps_req > 0 ? std::min(bps_req, occ) : std::min(occ, 4);
+  const uint64_t tiles = (nvec + static_cast<uint64_t>(kThreads) * U - 1) / (static_cast<uint64_t>(kThreads) * U);
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * bps));
   kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(
       static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, keys, nkeys,
       stamp, static_cast<const uint8_t*>(src) + nvec * T::EPV * es,
-      static_cast<uint8_t*>(dst) + nvec * T::EPV * es, ntail, elem_base + nvec * T::EPV);
+      static_cast<uint8_t*>(dst) + nvec * T::EPV * es, ntail, elem_base + nvec * T::EPV, 1u);
   return cudaGetLastError();
+}
+
+template <int K, int DT>
+cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_base,
+                    const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
+  constexpr int W = VT<K>::WPV;
+  const Shape sh = pick_shape(W, nkeys);
+  if constexpr (8 / W >= 8) {
+    if (sh.u == 8) return run_vec_u<K, DT, 8>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
+  }
+  if constexpr (8 / W >= 4) {
+    if (sh.u == 4) return run_vec_u<K, DT, 4>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
+  }
+  return run_vec_u<K, DT, 2>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
 }
 
 template <int DT>
