@@ -190,6 +190,15 @@ int cemuReleaseFloors(const cemuDelayModel* m, int coll, uint32_t n, uint64_t by
 int64_t cemuCallLatencyUs(const cemuDelayModel* m, int coll, uint32_t n, uint64_t bytes,
                           uint32_t k);
 
+/* Multi-GPU decomposition of one allreduce over k real GPUs:
+ * real GPU li reduce-scatters, synthesises and all-gathers elements
+ * [shardOffset, +shardCount); the tail [tailOffset, +tailCount) (< k
+ * elements) is all-reduced and synthesised by every real GPU. */
+typedef struct {
+  uint64_t shardOffset, shardCount, tailOffset, tailCount;
+} cemuShardPlan;
+void cemuPlanShards(uint64_t count, uint32_t k, uint32_t li, cemuShardPlan* plan);
+
 /* Payload generator (see paper_2405_02969_b200/csrc/payload.cuh). */
 uint32_t cemuPayloadKey(uint64_t seed, uint32_t rank);
 uint32_t cemuPayloadWord(uint32_t key, uint64_t wordIndex);

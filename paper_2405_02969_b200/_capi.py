@@ -38,6 +38,11 @@ class DelayModel(C.Structure):
     ]
 
 
+class ShardPlan(C.Structure):
+    _fields_ = [("shardOffset", C.c_uint64), ("shardCount", C.c_uint64),
+                ("tailOffset", C.c_uint64), ("tailCount", C.c_uint64)]
+
+
 class CallRecord(C.Structure):
     _fields_ = [
         ("call_id", C.c_uint64), ("coll", C.c_int32), ("delay_active", C.c_int32),
@@ -92,6 +97,7 @@ def _load():
         "cemuReleaseOffsets": (i32, [C.POINTER(DelayModel), i32, u32, u64, u32, vp]),
         "cemuReleaseFloors": (i32, [C.POINTER(DelayModel), i32, u32, u64, u32, i64, vp]),
         "cemuCallLatencyUs": (i64, [C.POINTER(DelayModel), i32, u32, u64, u32]),
+        "cemuPlanShards": (None, [u64, u32, u32, C.POINTER(ShardPlan)]),
         "cemuPayloadKey": (u32, [u64, u32]),
         "cemuPayloadWord": (u32, [u32, u64]),
     }

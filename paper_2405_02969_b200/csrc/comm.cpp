@@ -347,8 +347,10 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   // GPU's 1/k shard only, NCCL allgather.
   const Nccl* n = nccl();
   CUDA_OK(call.stamp_now());
-  const size_t shard = count / c->k;
-  const size_t rem = count - shard * c->k;
+  cemuShardPlan plan;
+  cemuPlanShards(count, c->k, c->li, &plan);
+  const size_t shard = plan.shardCount;
+  const size_t rem = plan.tailCount;
   auto* r8 = static_cast<uint8_t*>(recv);
   const auto* s8 = static_cast<const uint8_t*>(send);
   const auto ndt = static_cast<ncclDataType_t>(dt);
@@ -492,6 +494,16 @@ cemuResult_t run_or_defer(F&& f) {
 // C-ABI
 // =============================================================================
 extern "C" {
+
+void cemuPlanShards(uint64_t count, uint32_t k, uint32_t li, cemuShardPlan* p) {
+  // equal shards for NCCL reduce-scatter/allgather; the remainder (< k
+  // elements) is all-reduced by NCCL and synthesised by every rank alike
+  const uint64_t shard = k ? count / k : count;
+  p->shardOffset = shard * li;
+  p->shardCount = shard;
+  p->tailOffset = shard * k;
+  p->tailCount = count - shard * k;
+}
 
 cemuResult_t cemuGetVersion(int* version) {
   if (!version) return fail(cemuInvalidArgument, "cemuGetVersion: version is null");

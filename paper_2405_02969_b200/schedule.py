@@ -5,7 +5,7 @@ import ctypes as C
 
 import numpy as np
 
-from ._capi import DelayModel, lib
+from ._capi import DelayModel, ShardPlan, lib
 
 ALLREDUCE, ALLGATHER, REDUCESCATTER, BROADCAST = 0, 1, 2, 3
 NONE, ALPHA_BETA, FIXED = 0, 1, 2
@@ -73,3 +73,10 @@ def payload_key(seed, rank) -> int:
 
 def payload_word(key, j) -> int:
     return lib.cemuPayloadWord(key, j)
+
+
+def plan_shards(count, k, li) -> dict:
+    """Which elements real GPU `li` of `k` owns in a multi-GPU allreduce."""
+    p = ShardPlan()
+    lib.cemuPlanShards(count, k, li, C.byref(p))
+    return {"shard": (p.shardOffset, p.shardCount), "tail": (p.tailOffset, p.tailCount)}

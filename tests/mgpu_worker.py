@@ -1,0 +1,81 @@
+"""One rank of the multi-GPU parity check (launched by test_gpu_multigpu.py
+under torch.distributed.run).  Real ranks 0..N-1 of a world of 8N (or a
+non-contiguous real set), NCCL inside libcemu_b200 for the real part."""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import paper_2405_02969_b200 as pb  # noqa: E402
+from gpu_util import TORCH, assert_bit_equal, to_np  # noqa: E402
+from oracle import port as P  # noqa: E402
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    n = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    layouts = [list(range(n)), [2 * i + 1 for i in range(n)]]  # contiguous, strided
+    for real in layouts:
+        W = 8 * n
+        me = real[local]
+        obj = [pb.get_unique_id() if local == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        cfg = f"world_size = {W}\nreal_ranks = {','.join(map(str, real))}\nbucket_bytes = 1\n"
+        comm = pb.Communicator(cfg, me, local, obj[0])
+        for dt in (7, 9, 2):
+            for count in (1, n * 1000 + 3, (1 << 20) + 7):
+                sends = []
+                for i in range(n):
+                    g = np.random.default_rng(1000 * i + count)
+                    if dt in (7, 9):  # dyadic: the real sum is exact in any order
+                        v = torch.from_numpy((g.integers(-256, 256, size=count) / 64).astype(np.float32)).to(TORCH[dt])
+                    else:
+                        v = torch.from_numpy(g.integers(-2**31, 2**31, size=count).astype(np.int32))
+                    sends.append(v)
+                x = sends[local].cuda()
+                y = torch.empty_like(x)
+                comm.all_reduce(x, y)
+                torch.cuda.synchronize()
+                want = P.allreduce(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(s) for s in sends], count)
+                assert_bit_equal(to_np(y), want, f"allreduce real={real} dt={dt} n={count}")
+                # allgather
+                blk = max(count // 8, 1)
+                recv = torch.empty(blk * W, dtype=x.dtype, device="cuda")
+                comm.all_gather(x[:blk].contiguous(), recv)
+                torch.cuda.synchronize()
+                want = P.allgather(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(s[:blk]) for s in sends], blk)
+                assert_bit_equal(to_np(recv), want, f"allgather real={real} dt={dt}")
+                # reduce-scatter over a buffer of W chunks
+                rc = max(count // 16, 1)
+                full = [torch.cat([s] * 16)[: rc * W] for s in sends]
+                out = torch.empty(rc, dtype=x.dtype, device="cuda")
+                comm.reduce_scatter(full[local].cuda(), out)
+                torch.cuda.synchronize()
+                want = P.reducescatter(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(f) for f in full], rc)
+                assert_bit_equal(to_np(out), want, f"reducescatter real={real} dt={dt}")
+                # broadcast from a real and from an emulated root
+                for root in (real[-1], (real[-1] + 1) % W):
+                    b = torch.empty_like(x)
+                    src = x if me == root else None
+                    comm.broadcast(src if src is not None else torch.empty_like(x), b, root)
+                    torch.cuda.synchronize()
+                    rs = to_np(sends[real.index(root)]) if root in real else None
+                    want = P.broadcast(dt, P.PAYLOAD_HASH, W, real, me, root, 1, rs, count)
+                    assert_bit_equal(to_np(b), want, f"broadcast root={root} dt={dt}")
+        comm.close()
+        dist.barrier()
+    if local == 0:
+        print("MGPU OK", n)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
