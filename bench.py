@@ -123,7 +123,7 @@ def run_reference_arm(args, rank):
             "vs_baseline": None, "dtype": "int32 (elem_size 4 lanes)", "data": "synthetic",
             "config": workload(args, n), "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -405,13 +405,35 @@ def run_ours(args, rank, world_size, local_rank):
                 "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
                 "config": workload(args, n), "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks, **extra}
-        print(json.dumps(line), flush=True)
+        if n > 1:
+            # real part: bytes each GPU moves over NVLink per step (ring RS + AG)
+            nv = 2 * (n - 1) / n * nbytes
+            line["nvlink"] = {"bytes_per_gpu_per_step_each_direction": int(nv),
+                              "achieved_GBps": round(nv / (ms_per_step * 1e-3) / 1e9, 1),
+                              "peer_peak_GBps": 770.0, "peak_source": "B200_PROFILING.md measured peer copy",
+                              "frac": round(nv / (ms_per_step * 1e-3) / 1e9 / 770.0, 4)}
+        emit(line)
     comm.close()
     if n > 1:
         dist.destroy_process_group()
 
 
+_JSON_FD = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line, on the real stdout (fd 1 is redirected to stderr for
+    the whole run so library banners -- e.g. NCCL's version line -- cannot
+    interleave with it)."""
+    data = (json.dumps(line) + "\n").encode()
+    os.write(_JSON_FD if _JSON_FD is not None else 1, data)
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world_size = int(os.environ.get("WORLD_SIZE", "1"))

@@ -100,7 +100,8 @@ class JobConfig:
 def get_unique_id() -> bytes:
     uid = UniqueId()
     check(lib.cemuGetUniqueId(C.byref(uid)))
-    return bytes(uid.internal)
+    # raw 128 bytes: reading `uid.internal` would stop at the first NUL
+    return C.string_at(C.addressof(uid), C.sizeof(uid))
 
 
 def _stream_ptr(stream) -> int:
@@ -123,7 +124,9 @@ class Communicator:
         self._h = C.c_void_p()
         uid = UniqueId()
         if unique_id is not None:
-            uid.internal = unique_id
+            if len(unique_id) != C.sizeof(uid):
+                raise CemuError(_capi.INVALID_ARGUMENT, f"unique id must be {C.sizeof(uid)} bytes")
+            C.memmove(C.addressof(uid), unique_id, C.sizeof(uid))
         check(lib.cemuCommInitRankConfig(C.byref(self._h), config_text.encode(), uid, rank, device))
         self.config = JobConfig.parse(config_text)
         self.rank = rank
