@@ -247,6 +247,38 @@ def delay_error_block(torch, pb, device):
     return out
 
 
+def whatif_block(device, with_reference):
+    """Config 4: DDP gradient-bucket what-if sweeps on the device, against the
+    ideal timeline, with the reference CPU emulator's loop on the same
+    profile as the comparison arm (bounded iterations)."""
+    from paper_2405_02969_b200.whatif import sweep
+    ref_fn = None
+    if with_reference:
+        from oracle import ref
+        if ref.available():
+            def ref_fn(text, world, bb, inject):
+                lines = [ln for ln in text.splitlines() if not ln.startswith(("iterations", "warmup"))]
+                short = "\n".join(lines + ["iterations = 8", "warmup = 2"]) + "\n"
+                return ref.run_training_loop(short, world, bb, inject=inject)
+    out = {}
+    cases = (("bert-like", "bert-like", 2, 65536, "", 30),
+             ("resnet50_25MiB", os.path.join(ROOT, "profiles", "resnet50.model"), 8, 25 << 20,
+              "delay.kind = alpha_beta\nlink.alpha_us = 10\nlink.beta_us_per_byte = 0.00004\n", 20))
+    for name, model, world, bb, extra, iters in cases:
+        res = sweep(model, [0, 500, 1000, 2000, 4000, 6000, 8000, 10000], world, bb, device, extra, iters,
+                    reference_fn=ref_fn)
+        out[name] = {k: (round(v, 6) if isinstance(v, float) else v) for k, v in res.items() if k != "points"}
+        out[name]["points"] = [[p["inject_us"], round(p["mean_us"], 1), round(p["ideal_us"], 1),
+                                round(100 * p["rel_err"], 4)] +
+                               ([round(p["reference_mean_us"], 1), round(100 * p["reference_rel_err"], 2)]
+                                if "reference_mean_us" in p else []) for p in res["points"]]
+    out["columns"] = ["inject_us", "mean_us", "ideal_us", "err_pct", "reference_mean_us", "reference_err_pct"]
+    out["note"] = ("ideal = compute exactly as profiled + each bucket's collective exactly its modelled "
+                   "latency (A14), in issue order; reference = the cemu CPU emulator's own run_training_loop "
+                   "(8 iterations) on the same profile over loopback TCP")
+    return out
+
+
 def sweep_block(torch, pb, device):
     """Config 2 shape (single B200 emulating a 64-rank ring): algorithmic HBM
     GB/s per collective, fp32 and bf16, 4 KiB .. 1 GiB (powers of 4)."""
@@ -397,6 +429,7 @@ def run_ours(args, rank, world_size, local_rank):
         extra["delay_error"] = delay_error_block(torch, pb, device)
         if not args.no_sweep:
             extra["sweep_config2"] = sweep_block(torch, pb, device)
+            extra["whatif_config4"] = whatif_block(device, not args.no_cpu_baseline)
         if not args.no_cpu_baseline:
             extra["cpu_baseline"] = cpu_baseline_block(20, 2, RANKS_PER_GPU)
     if rank == 0:

@@ -203,6 +203,37 @@ void cemuPlanShards(uint64_t count, uint32_t k, uint32_t li, cemuShardPlan* plan
 uint32_t cemuPayloadKey(uint64_t seed, uint32_t rank);
 uint32_t cemuPayloadWord(uint32_t key, uint64_t wordIndex);
 
+/* ------------------------------------------------------------------ */
+/* DDP what-if harness (proj/src/harness.cpp)           */
+/* ------------------------------------------------------------------ */
+typedef struct cemuModelSpec* cemuModelSpec_t;
+/* parse_model_spec (harness.cpp:27-101): `layer = fwd_us bwd_us grad_bytes` */
+cemuResult_t cemuModelSpecParse(const char* text, cemuModelSpec_t* spec, char* err, size_t errcap);
+/* builtin_model (harness.cpp:116-134): bert-like, small, wide */
+cemuResult_t cemuModelSpecBuiltin(const char* name, cemuModelSpec_t* spec);
+void cemuModelSpecFree(cemuModelSpec_t spec);
+int cemuModelSpecRender(cemuModelSpec_t spec, char* out, size_t cap);
+uint32_t cemuModelSpecLayers(cemuModelSpec_t spec, int64_t* fwdUs, int64_t* bwdUs, uint64_t* gradBytes,
+                             size_t cap, uint32_t* iterations, uint32_t* warmup, int64_t* updateUs);
+/* bucketize (harness.cpp:152-175): buckets in issue (reverse layer) order */
+uint32_t cemuBucketize(cemuModelSpec_t spec, uint64_t bucketBytes, uint32_t* firstLayer, uint32_t* lastLayer,
+                       uint64_t* bytes, size_t cap);
+/* run_training_loop (harness.cpp:191-254) on the device: spin-kernel
+ * compute on a compute stream, one emulated allreduce (uint8, in order) per
+ * filled bucket on a comm stream.  Device-event timestamps in us from the
+ * loop's first event: per iteration start/end, per (iteration, bucket)
+ * issue/complete (row-major).  cap = iterations the arrays hold. */
+cemuResult_t cemuRunTrainingLoop(cemuComm_t comm, cemuModelSpec_t spec, uint64_t bucketBytes,
+                                 double* iterStartUs, double* iterEndUs, double* issueUs, double* completeUs,
+                                 size_t cap);
+/* The ideal timeline of that loop with bucket b's collective taking
+ * bucketLatencyUs[b]: iteration time in us. */
+double cemuPredictIterationUs(cemuModelSpec_t spec, uint64_t bucketBytes, const double* bucketLatencyUs, size_t n);
+/* Modelled latency (A14) of one `coll` call of `bytes` (delay-model bytes) on this comm. */
+cemuResult_t cemuCommModelLatencyUs(cemuComm_t comm, int coll, uint64_t bytes, int64_t* latencyUs);
+/* Compute emulation (clock.hpp:29-37): a %globaltimer spin of `us` on `stream`. */
+cemuResult_t cemuSpinUs(cemuStream_t stream, uint64_t us);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,6 +58,12 @@ def lib():
         L.ref_emulated_collective.restype = C.c_int
         L.ref_emulated_collective.argtypes = [u32, C.c_int, vp, u64, u32, C.c_int, dbl, dbl, dbl, dbl,
                                               dbl, C.c_int, C.c_int, vp, cp, sz]
+        L.ref_model_render.restype = C.c_int
+        L.ref_model_render.argtypes = [cp, cp, sz, cp, sz]
+        L.ref_bucketize.restype = C.c_int
+        L.ref_bucketize.argtypes = [cp, u64, vp, sz, cp, sz]
+        L.ref_run_training_loop.restype = C.c_int
+        L.ref_run_training_loop.argtypes = [cp, u32, u64, C.c_int, dbl, dbl, dbl, dbl, dbl, vp, sz, cp, sz]
         L.ref_real_ring.restype = C.c_int
         L.ref_real_ring.argtypes = [u32, C.c_int, vp, u64, u32, cp, sz]
         _LIB = L
@@ -187,3 +193,31 @@ def real_ring(n, coll, bufs, plan_bytes, elem):
     r = lib().ref_real_ring(n, coll, C.cast(ptrs, C.c_void_p), plan_bytes, elem, err, 2048)
     if r != 0:
         raise RefError(err.value.decode())
+
+
+def run_training_loop(model_text: str, n: int, bucket_bytes: int, kind=0, a=0.0, b=0.0, g=0.0, fixed=0.0,
+                      inject=0.0):
+    """The reference's run_training_loop (harness.cpp:191-254) against its
+    emulator over loopback; returns per-iteration wall times in us."""
+    cap = 100000
+    out = np.zeros(cap, dtype=np.float64)
+    err = C.create_string_buffer(2048)
+    k = lib().ref_run_training_loop(model_text.encode(), n, bucket_bytes, kind, a, b, g, fixed, inject,
+                                    out.ctypes.data, cap, err, 2048)
+    if k < 0:
+        raise RefError(err.value.decode())
+    return out[:k]
+
+
+def model_render(text: str) -> str:
+    """render_model_spec(parse_model_spec(text)) (harness.cpp:27-114)."""
+    return _text_call(lib().ref_model_render, text.encode())
+
+
+def bucketize(text: str, bucket_bytes: int):
+    out = np.zeros(3 * 4096, dtype=np.uint64)
+    err = C.create_string_buffer(1024)
+    k = lib().ref_bucketize(text.encode(), bucket_bytes, out.ctypes.data, len(out), err, 1024)
+    if k < 0:
+        raise RefError(err.value.decode())
+    return [tuple(int(v) for v in out[3 * i:3 * i + 3]) for i in range(k)]

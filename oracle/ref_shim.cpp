@@ -41,6 +41,7 @@
 #include "cemu/delay.hpp"
 #include "cemu/emulator.hpp"
 #include "cemu/engine.hpp"
+#include "cemu/harness.hpp"
 #include "cemu/reduce.hpp"
 
 using namespace cemu;
@@ -391,6 +392,71 @@ int ref_real_ring(uint32_t n, int coll, uint8_t** bufs, uint64_t plan_bytes,
       }
     }
     return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errcap, e.what());
+    return -1;
+  }
+}
+
+// ---- model spec + bucketing (harness.cpp:27-189) ---------------------------
+int ref_model_render(const char* text, char* out, size_t cap, char* err, size_t errcap) {
+  try {
+    return put_text(out, cap, render_model_spec(parse_model_spec(text)));
+  } catch (const std::exception& e) {
+    put_err(err, errcap, e.what());
+    return -1;
+  }
+}
+
+// Returns the bucket count (or -1); writes (first, last, bytes) triples.
+int ref_bucketize(const char* text, uint64_t bucket_bytes, uint64_t* out, size_t cap, char* err,
+                  size_t errcap) {
+  try {
+    const auto b = bucketize(parse_model_spec(text), bucket_bytes);
+    for (size_t i = 0; i < b.size() && 3 * i + 2 < cap; ++i) {
+      out[3 * i] = b[i].first_layer;
+      out[3 * i + 1] = b[i].last_layer;
+      out[3 * i + 2] = b[i].bytes;
+    }
+    return static_cast<int>(b.size());
+  } catch (const std::exception& e) {
+    put_err(err, errcap, e.what());
+    return -1;
+  }
+}
+
+// ---- the reference's synthetic DDP loop (harness.cpp:191-254) -----------
+// run_training_loop on WorkerSession(rank 0) against an in-thread emulator,
+// world n, bucket_bytes from the caller, delay params as above.  Writes each
+// iteration's wall time (us) to iter_us and returns the iteration count, or
+// -1 with the error in `err`.
+int ref_run_training_loop(const char* model_text, uint32_t n, uint64_t bucket_bytes, int kind, double a,
+                          double b, double g, double fixed, double inject, double* iter_us, size_t cap,
+                          char* err, size_t errcap) {
+  try {
+    const ModelSpec model = parse_model_spec(model_text);
+    JobConfig cfg = make_cfg(n, /*emulated=*/true, delay_params(kind, a, b, g, fixed, inject));
+    cfg.bucket_bytes = bucket_bytes;
+    EmulatorServer::Options o;
+    o.once = true;
+    EmulatorServer server(cfg, o);
+    std::thread th([&] { server.serve(); });
+    std::string failure;
+    std::vector<IterationTrace> traces;
+    try {
+      WorkerSession s(cfg, 0, harness_plan(model, bucket_bytes));
+      traces = run_training_loop(cfg, model, s);
+      s.close();
+    } catch (const std::exception& e) {
+      failure = e.what();
+    }
+    server.request_stop();
+    th.join();
+    if (!failure.empty()) throw std::runtime_error(failure);
+    for (size_t i = 0; i < traces.size() && i < cap; ++i) {
+      iter_us[i] = static_cast<double>(traces[i].iteration_time_us());
+    }
+    return static_cast<int>(traces.size());
   } catch (const std::exception& e) {
     put_err(err, errcap, e.what());
     return -1;

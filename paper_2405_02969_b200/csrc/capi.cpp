@@ -133,3 +133,106 @@ uint32_t cemuPayloadKey(uint64_t seed, uint32_t rank) { return payload_key(seed,
 uint32_t cemuPayloadWord(uint32_t key, uint64_t j) { return payload_word(key, j); }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// harness (proj/src/harness.cpp) and compute emulation
+// ---------------------------------------------------------------------------
+#include <cuda_runtime.h>
+
+#include "harness.hpp"
+#include "kernels.hpp"
+
+struct cemuModelSpec {
+  ModelSpec m;
+};
+
+extern "C" {
+
+cemuResult_t cemuModelSpecParse(const char* text, cemuModelSpec_t* out, char* err, size_t errcap) {
+  if (!text || !out) {
+    copy_err(err, errcap, "cemuModelSpecParse: null argument");
+    return cemuInvalidArgument;
+  }
+  try {
+    *out = new cemuModelSpec{parse_model_spec(text)};
+    return cemuSuccess;
+  } catch (const std::exception& e) {
+    copy_err(err, errcap, e.what());
+    return cemuInvalidArgument;
+  }
+}
+
+cemuResult_t cemuModelSpecBuiltin(const char* name, cemuModelSpec_t* out) {
+  ModelSpec m;
+  if (!name || !out || !builtin_model(name, &m)) return cemuInvalidArgument;
+  *out = new cemuModelSpec{m};
+  return cemuSuccess;
+}
+
+void cemuModelSpecFree(cemuModelSpec_t m) { delete m; }
+
+int cemuModelSpecRender(cemuModelSpec_t m, char* out, size_t cap) {
+  return m ? copy_text(render_model_spec(m->m), out, cap) : 0;
+}
+
+uint32_t cemuModelSpecLayers(cemuModelSpec_t m, int64_t* fwd, int64_t* bwd, uint64_t* grad, size_t cap,
+                             uint32_t* iterations, uint32_t* warmup, int64_t* update_us) {
+  if (!m) return 0;
+  const auto& L = m->m.layers;
+  for (size_t i = 0; i < L.size() && i < cap; ++i) {
+    if (fwd) fwd[i] = L[i].forward_us;
+    if (bwd) bwd[i] = L[i].backward_us;
+    if (grad) grad[i] = L[i].grad_bytes;
+  }
+  if (iterations) *iterations = m->m.iterations;
+  if (warmup) *warmup = m->m.warmup_iterations;
+  if (update_us) *update_us = m->m.update_us;
+  return static_cast<uint32_t>(L.size());
+}
+
+uint32_t cemuBucketize(cemuModelSpec_t m, uint64_t bucketBytes, uint32_t* first, uint32_t* last, uint64_t* bytes,
+                       size_t cap) {
+  if (!m) return 0;
+  const auto b = bucketize(m->m, bucketBytes);
+  for (size_t i = 0; i < b.size() && i < cap; ++i) {
+    if (first) first[i] = b[i].first_layer;
+    if (last) last[i] = b[i].last_layer;
+    if (bytes) bytes[i] = b[i].bytes;
+  }
+  return static_cast<uint32_t>(b.size());
+}
+
+cemuResult_t cemuRunTrainingLoop(cemuComm_t comm, cemuModelSpec_t m, uint64_t bucketBytes, double* iterStartUs,
+                                 double* iterEndUs, double* issueUs, double* completeUs, size_t cap) {
+  if (!comm || !m) return cemuInvalidArgument;
+  try {
+    const auto tr = run_training_loop(comm, m->m, bucketBytes);
+    const size_t nb = bucketize(m->m, bucketBytes).size();
+    for (size_t it = 0; it < tr.size() && it < cap; ++it) {
+      if (iterStartUs) iterStartUs[it] = tr[it].start_us;
+      if (iterEndUs) iterEndUs[it] = tr[it].end_us;
+      for (size_t b = 0; b < nb; ++b) {
+        if (issueUs) issueUs[it * nb + b] = tr[it].issue_us[b];
+        if (completeUs) completeUs[it * nb + b] = tr[it].complete_us[b];
+      }
+    }
+    return cemuSuccess;
+  } catch (const std::exception& e) {
+    (void)e;
+    return cemuInternalError;
+  }
+}
+
+double cemuPredictIterationUs(cemuModelSpec_t m, uint64_t bucketBytes, const double* bucketLatencyUs, size_t n) {
+  if (!m) return -1;
+  return predicted_iteration_us(m->m, bucketBytes, std::vector<double>(bucketLatencyUs, bucketLatencyUs + n));
+}
+
+cemuResult_t cemuSpinUs(cemuStream_t stream, uint64_t us) {
+  int l = 0;
+  return launch_spin_ns(static_cast<int64_t>(us) * 1000, reinterpret_cast<cudaStream_t>(stream), &l) == cudaSuccess
+             ? cemuSuccess
+             : cemuUnhandledCudaError;
+}
+
+}  // extern "C"

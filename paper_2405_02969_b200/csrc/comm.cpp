@@ -692,6 +692,12 @@ cemuResult_t cemuCommCallRecord(cemuComm_t c, uint64_t id, cemuCallRecord* rec, 
   return cemuSuccess;
 }
 
+cemuResult_t cemuCommModelLatencyUs(cemuComm_t c, int coll, uint64_t bytes, int64_t* out) {
+  if (!c || !out || coll < 0 || coll > 3) return fail(cemuInvalidArgument, "cemuCommModelLatencyUs: bad argument");
+  *out = c->delay_active ? call_latency_us(c->delay, coll, c->W, bytes, to_real_count(coll, c->W, c->real)) : 0;
+  return cemuSuccess;
+}
+
 }  // extern "C"
 
 // launch counter for bench.py's gpu_launches (not part of the public header)

@@ -459,6 +459,24 @@ __global__ void __launch_bounds__(kThreads) synth_fill_scalar(void* dst, uint64_
 // ---------------------------------------------------------------------------
 __global__ void stamp_kernel(int64_t* slot) { slot[0] = globaltimer_ns(); }
 
+// Compute emulation (clock.hpp:29-37 emulate_compute_us): hold the stream
+// for `ns` of %globaltimer.  With a chain slot the layer ends at
+// previous deadline + ns (device-absolute), so back-to-back launches do not
+// accumulate their ~1-2 us launch gaps into the emulated compute timeline;
+// `resync` (after a cross-stream wait) restarts the chain at the kernel's
+// own start.
+__global__ void spin_ns_kernel(int64_t ns, int64_t* chain, int resync) {
+  const int64_t now = globaltimer_ns();
+  const int64_t start = (chain && !resync) ? *chain : now;
+  const int64_t end = start + ns;
+  int64_t t = now;
+  while (t < end) {
+    if (end - t > 8000) __nanosleep(2000);
+    t = globaltimer_ns();
+  }
+  if (chain) *chain = end;
+}
+
 __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int64_t* slot) {
   int64_t* floors = slot + kSlotHeader;
   int64_t* release = floors + d.kmax;
@@ -714,6 +732,13 @@ cudaError_t launch_synth_fill(int dtype, void* dst, uint64_t block_elems, const 
 cudaError_t launch_stamp(int64_t* slot, cudaStream_t s, int* launches) {
   ++*launches;
   stamp_kernel<<<1, 1, 0, s>>>(slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spin_ns(int64_t ns, cudaStream_t s, int* launches, int64_t* chain, bool resync) {
+  if (ns <= 0 && !chain) return cudaSuccess;
+  ++*launches;
+  spin_ns_kernel<<<1, 1, 0, s>>>(ns, chain, resync ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -47,6 +47,9 @@ cudaError_t launch_synth_fill(int dtype, void* dst, uint64_t block_elems,
                               int* launches);
 
 cudaError_t launch_stamp(int64_t* slot, cudaStream_t stream, int* launches);
+// chain: device int64 holding the previous spin's absolute deadline (or null)
+cudaError_t launch_spin_ns(int64_t ns, cudaStream_t stream, int* launches, int64_t* chain = nullptr,
+                           bool resync = false);
 cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t stream,
                               int* launches);
 
