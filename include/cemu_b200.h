@@ -233,6 +233,11 @@ double cemuPredictIterationUs(cemuModelSpec_t spec, uint64_t bucketBytes, const 
 cemuResult_t cemuCommModelLatencyUs(cemuComm_t comm, int coll, uint64_t bytes, int64_t* latencyUs);
 /* Compute emulation (clock.hpp:29-37): a %globaltimer spin of `us` on `stream`. */
 cemuResult_t cemuSpinUs(cemuStream_t stream, uint64_t us);
+/* Chained compute emulation: `deviceChain` (one int64 in device memory)
+ * holds the previous spin's absolute deadline; this spin ends at
+ * deadline + us, so launch gaps do not accumulate.  resync != 0 restarts the
+ * chain at this kernel's start (use after a cross-stream wait). */
+cemuResult_t cemuSpinChainUs(cemuStream_t stream, uint64_t us, int64_t* deviceChain, int resync);
 
 #ifdef __cplusplus
 }

@@ -213,6 +213,22 @@ static double tree_allreduce_us(uint32_t n, uint64_t bytes, double a, double b,
   return steps * a + 2.0 * m * b + m * g;
 }
 
+/* NEW: tree-scheduled (PAT-style) allgather / reduce-scatter: log-depth
+ * latency, ring bandwidth. */
+static double tree_allgather_us(uint32_t n, uint64_t bytes, double a, double b) {
+  const double steps = (double)ceil_log2(n);
+  const double m = (double)bytes;
+  return steps * a + (double)(n - 1) * m * b;
+}
+
+static double tree_reducescatter_us(uint32_t n, uint64_t bytes, double a,
+                                    double b, double g) {
+  const double steps = (double)ceil_log2(n);
+  const double frac = (double)(n - 1) / n;
+  const double m = (double)bytes;
+  return steps * a + frac * m * b + frac * m * g;
+}
+
 static double tree_broadcast_us(uint32_t n, uint64_t bytes, double a,
                                 double b) {
   const double steps = (double)ceil_log2(n);
@@ -242,10 +258,11 @@ static double hier_us(const or_delay_model* M, int coll, uint32_t n,
       double intra_ag = gm1 * ai + fi * m * bi;
       return intra_rs + inter_ar + intra_ag;
     }
-    case OR_ALLGATHER: { /* bytes = per-rank block */
-      double intra_ag = gm1 * ai + gm1 * m * bi;
-      double inter_ag = nm1 * ae + nm1 * (G * m) * be;
-      return intra_ag + inter_ag;
+    case OR_ALLGATHER: { /* bytes = per-rank block: G parallel inter-node
+                            rings, then a node-local gather of N blocks */
+      double inter_ag = nm1 * ae + nm1 * m * be;
+      double intra_ag = gm1 * ai + gm1 * (N * m) * bi;
+      return inter_ag + intra_ag;
     }
     case OR_REDUCESCATTER: {
       double intra_rs = gm1 * ai + fi * m * bi + fi * m * g;
@@ -267,9 +284,12 @@ double or_model_total_us(const or_delay_model* M, int coll, uint32_t n,
     if (coll == OR_ALLREDUCE)
       return tree_allreduce_us(n, bytes, M->alpha_us, M->beta_us_per_byte,
                                M->gamma_us_per_byte);
-    if (coll == OR_BROADCAST)
-      return tree_broadcast_us(n, bytes, M->alpha_us, M->beta_us_per_byte);
-    /* allgather / reduce-scatter have no tree form: ring, as NCCL does */
+    if (coll == OR_ALLGATHER)
+      return tree_allgather_us(n, bytes, M->alpha_us, M->beta_us_per_byte);
+    if (coll == OR_REDUCESCATTER)
+      return tree_reducescatter_us(n, bytes, M->alpha_us, M->beta_us_per_byte,
+                                   M->gamma_us_per_byte);
+    return tree_broadcast_us(n, bytes, M->alpha_us, M->beta_us_per_byte);
   }
   switch (coll) {
     case OR_ALLREDUCE:

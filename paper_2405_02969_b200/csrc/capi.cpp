@@ -235,4 +235,13 @@ cemuResult_t cemuSpinUs(cemuStream_t stream, uint64_t us) {
              : cemuUnhandledCudaError;
 }
 
+cemuResult_t cemuSpinChainUs(cemuStream_t stream, uint64_t us, int64_t* chain, int resync) {
+  if (!chain) return cemuInvalidArgument;
+  int l = 0;
+  return launch_spin_ns(static_cast<int64_t>(us) * 1000, reinterpret_cast<cudaStream_t>(stream), &l, chain,
+                        resync != 0) == cudaSuccess
+             ? cemuSuccess
+             : cemuUnhandledCudaError;
+}
+
 }  // extern "C"

@@ -72,6 +72,21 @@ CEMU_DM_HD double tree_allreduce_us(uint32_t n, uint64_t bytes, double a, double
   return DADD(DADD(DMUL(steps, a), DMUL(DMUL(2.0, m), b)), DMUL(m, g));
 }
 
+// NEW: tree-scheduled (PAT-style) allgather / reduce-scatter: ceil(log2 n)
+// latency terms, the ring's bandwidth term (every byte still crosses once).
+CEMU_DM_HD double tree_allgather_us(uint32_t n, uint64_t bytes, double a, double b) {
+  const double steps = static_cast<double>(ceil_log2_u32(n));
+  const double m = static_cast<double>(bytes);
+  return DADD(DMUL(steps, a), DMUL(DMUL(static_cast<double>(n - 1), m), b));
+}
+
+CEMU_DM_HD double tree_reducescatter_us(uint32_t n, uint64_t bytes, double a, double b, double g) {
+  const double steps = static_cast<double>(ceil_log2_u32(n));
+  const double frac = DDIV(static_cast<double>(n - 1), static_cast<double>(n));
+  const double m = static_cast<double>(bytes);
+  return DADD(DADD(DMUL(steps, a), DMUL(DMUL(frac, m), b)), DMUL(DMUL(frac, m), g));
+}
+
 CEMU_DM_HD double tree_broadcast_us(uint32_t n, uint64_t bytes, double a, double b) {
   const double steps = static_cast<double>(ceil_log2_u32(n));
   const double m = static_cast<double>(bytes);
@@ -99,10 +114,10 @@ CEMU_DM_HD double hier_us(const cemuDelayModel& M, int coll, uint32_t n, uint64_
       const double intra_ag = DADD(DMUL(gm1, ai), DMUL(DMUL(fi, m), bi));
       return DADD(DADD(intra_rs, inter_ar), intra_ag);
     }
-    case kAllGather: {
-      const double intra_ag = DADD(DMUL(gm1, ai), DMUL(DMUL(gm1, m), bi));
-      const double inter_ag = DADD(DMUL(nm1, ae), DMUL(DMUL(nm1, DMUL(static_cast<double>(G), m)), be));
-      return DADD(intra_ag, inter_ag);
+    case kAllGather: {  // m = per-rank block: G parallel inter-node rings, then a node-local gather
+      const double inter_ag = DADD(DMUL(nm1, ae), DMUL(DMUL(nm1, m), be));
+      const double intra_ag = DADD(DMUL(gm1, ai), DMUL(DMUL(gm1, DMUL(static_cast<double>(N), m)), bi));
+      return DADD(inter_ag, intra_ag);
     }
     case kReduceScatter: {
       const double intra_rs = DADD(DADD(DMUL(gm1, ai), DMUL(DMUL(fi, m), bi)), DMUL(DMUL(fi, m), g));
@@ -120,8 +135,13 @@ CEMU_DM_HD double hier_us(const cemuDelayModel& M, int coll, uint32_t n, uint64_
 CEMU_DM_HD double model_total_us(const cemuDelayModel& M, int coll, uint32_t n, uint64_t bytes) {
   if (M.algo == 2) return hier_us(M, coll, n, bytes);
   if (M.algo == 1) {
-    if (coll == kAllReduce) return tree_allreduce_us(n, bytes, M.alpha_us, M.beta_us_per_byte, M.gamma_us_per_byte);
-    if (coll == kBroadcast) return tree_broadcast_us(n, bytes, M.alpha_us, M.beta_us_per_byte);
+    switch (coll) {
+      case kAllReduce: return tree_allreduce_us(n, bytes, M.alpha_us, M.beta_us_per_byte, M.gamma_us_per_byte);
+      case kAllGather: return tree_allgather_us(n, bytes, M.alpha_us, M.beta_us_per_byte);
+      case kReduceScatter:
+        return tree_reducescatter_us(n, bytes, M.alpha_us, M.beta_us_per_byte, M.gamma_us_per_byte);
+      default: return tree_broadcast_us(n, bytes, M.alpha_us, M.beta_us_per_byte);
+    }
   }
   switch (coll) {
     case kAllReduce: return ring_allreduce_us(n, bytes, M.alpha_us, M.beta_us_per_byte, M.gamma_us_per_byte);

@@ -53,6 +53,8 @@ lib.cemuCommModelLatencyUs.restype = C.c_int
 lib.cemuCommModelLatencyUs.argtypes = [C_VOID, C.c_int, C.c_uint64, C.POINTER(C.c_int64)]
 lib.cemuSpinUs.restype = C.c_int
 lib.cemuSpinUs.argtypes = [C_VOID, C.c_uint64]
+lib.cemuSpinChainUs.restype = C.c_int
+lib.cemuSpinChainUs.argtypes = [C_VOID, C.c_uint64, C_VOID, C.c_int]
 
 
 class ModelSpec:
