@@ -430,6 +430,10 @@ def run_ours(args, rank, world_size, local_rank):
         if not args.no_sweep:
             extra["sweep_config2"] = sweep_block(torch, pb, device)
             extra["whatif_config4"] = whatif_block(device, not args.no_cpu_baseline)
+            from paper_2405_02969_b200 import fsdp
+            fs = fsdp.whatif_table(1024, iterations=2, device=device)
+            fs["rel_err_note"] = "measured device iteration vs ideal timeline of the same schedule"
+            extra["fsdp_config5"] = fs
         if not args.no_cpu_baseline:
             extra["cpu_baseline"] = cpu_baseline_block(20, 2, RANKS_PER_GPU)
     if rank == 0:

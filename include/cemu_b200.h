@@ -134,6 +134,12 @@ cemuResult_t cemuCommCallRecord(cemuComm_t comm, uint64_t callId, cemuCallRecord
                                 int64_t* floorsUs, int64_t* releaseNs, double* offsetsUs,
                                 size_t cap);
 
+/* The call's per-step schedule as EventLog lines (proj/include/cemu/
+ * trace.hpp:10-34: "<ts_us> <op_id> <event> <direction> <step> <chunk>"):
+ * register, from_real / to_real per step, complete -- device %globaltimer
+ * times.  Returns the text length, -(needed) if cap is short, -1 on error. */
+int cemuCommEventLog(cemuComm_t comm, uint64_t callId, char* out, size_t cap);
+
 /* ------------------------------------------------------------------ */
 /* Job config (proj/src/config.cpp) -- bit-compatible render + digest    */
 /* ------------------------------------------------------------------ */

@@ -58,6 +58,8 @@ def lib():
         L.ref_emulated_collective.restype = C.c_int
         L.ref_emulated_collective.argtypes = [u32, C.c_int, vp, u64, u32, C.c_int, dbl, dbl, dbl, dbl,
                                               dbl, C.c_int, C.c_int, vp, cp, sz]
+        L.ref_trace_open.restype = None
+        L.ref_trace_open.argtypes = [cp]
         L.ref_model_render.restype = C.c_int
         L.ref_model_render.argtypes = [cp, cp, sz, cp, sz]
         L.ref_bucketize.restype = C.c_int
@@ -221,3 +223,8 @@ def bucketize(text: str, bucket_bytes: int):
     if k < 0:
         raise RefError(err.value.decode())
     return [tuple(int(v) for v in out[3 * i:3 * i + 3]) for i in range(k)]
+
+
+def trace_open(path: str) -> None:
+    """Opens the reference's process-wide EventLog (trace.cpp:9-19)."""
+    lib().ref_trace_open(path.encode())

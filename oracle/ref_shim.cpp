@@ -43,6 +43,7 @@
 #include "cemu/engine.hpp"
 #include "cemu/harness.hpp"
 #include "cemu/reduce.hpp"
+#include "cemu/trace.hpp"
 
 using namespace cemu;
 
@@ -397,6 +398,9 @@ int ref_real_ring(uint32_t n, int coll, uint8_t** bufs, uint64_t plan_bytes,
     return -1;
   }
 }
+
+// ---- EventLog (trace.cpp:9-46) ----------------------------------------------
+void ref_trace_open(const char* path) { global_event_log().open(path ? path : ""); }
 
 // ---- model spec + bucketing (harness.cpp:27-189) ---------------------------
 int ref_model_render(const char* text, char* out, size_t cap, char* err, size_t errcap) {

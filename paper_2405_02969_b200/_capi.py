@@ -80,6 +80,7 @@ def _load():
         "cemuCommLastCallId": (i32, [vp, C.POINTER(u64)]),
         "cemuCommCallRecord": (i32, [vp, u64, C.POINTER(CallRecord), vp, vp, vp, sz]),
         "cemuCommKernelLaunches": (u64, [vp]),
+        "cemuCommEventLog": (i32, [vp, u64, cp, sz]),
         "cemuConfigParse": (i32, [cp, C.POINTER(vp), cp, sz]),
         "cemuConfigLoad": (i32, [cp, C.POINTER(vp), cp, sz]),
         "cemuConfigFree": (None, [vp]),

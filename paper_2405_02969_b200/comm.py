@@ -200,6 +200,17 @@ class Communicator:
             "offsets_us": offsets[:k].copy(),
         }
 
+    def event_log(self, call_id: int | None = None) -> list[str]:
+        """EventLog lines (trace.hpp:10-34) of one delayed call."""
+        if call_id is None:
+            call_id = self.last_call_id
+        n = lib.cemuCommEventLog(self._h, call_id, None, 0)
+        if n == -1:
+            raise CemuError(_capi.INVALID_USAGE, lib.cemuGetLastError(self._h).decode())
+        buf = C.create_string_buffer(-n)
+        lib.cemuCommEventLog(self._h, call_id, buf, -n)
+        return buf.value.decode().splitlines()
+
     @property
     def kernel_launches(self) -> int:
         return lib.cemuCommKernelLaunches(self._h)

@@ -698,6 +698,48 @@ cemuResult_t cemuCommModelLatencyUs(cemuComm_t c, int coll, uint64_t bytes, int6
   return cemuSuccess;
 }
 
+// EventLog lines (trace.hpp:10-34: "<ts_us> <op_id> <event> <direction>
+// <step> <chunk>") of one call, as the reference emulator would log them:
+// register, the real node's from_real sends (an instantaneous real node
+// sends step p when step p-1's reply was released), every to_real release
+// at its device %globaltimer instant, complete.  Chunks are given for a
+// single real rank (ring schedule, dag.cpp:73-82), "-" otherwise.
+int cemuCommEventLog(cemuComm_t c, uint64_t id, char* out, size_t cap) {
+  cemuCallRecord rec;
+  std::vector<int64_t> floors, rel;
+  if (!c) return -1;
+  const uint32_t i = static_cast<uint32_t>(id % cemuComm::kSlots);
+  const uint32_t k = c->meta[i].k;
+  floors.resize(k ? k : 1);
+  rel.resize(k ? k : 1);
+  if (cemuCommCallRecord(c, id, &rec, floors.data(), rel.data(), nullptr, k) != cemuSuccess) return -1;
+  if (!rec.delay_active) return fail(cemuInvalidUsage, "cemuCommEventLog: call ran without the delay model"), -1;
+  const bool single = c->k == 1;
+  const int coll = rec.coll == kReduceScatter || rec.coll == kBroadcast ? -1 : rec.coll;
+  const uint32_t W = c->W, R = c->rank, prev = (R + W - 1) % W;
+  std::string s;
+  char line[160];
+  auto emit = [&](int64_t ns, const char* ev, const char* dir, int64_t step, int64_t chunk) {
+    char st[24], ch[24];
+    if (step >= 0) std::snprintf(st, sizeof st, "%lld", static_cast<long long>(step)); else std::snprintf(st, sizeof st, "-");
+    if (chunk >= 0) std::snprintf(ch, sizeof ch, "%lld", static_cast<long long>(chunk)); else std::snprintf(ch, sizeof ch, "-");
+    std::snprintf(line, sizeof line, "%lld %llu %s %s %s %s\n", static_cast<long long>(ns / 1000),
+                  static_cast<unsigned long long>(id), ev, dir, st, ch);
+    s += line;
+  };
+  emit(rec.t_start_ns, "register", "-", -1, -1);
+  for (uint32_t j = 0; j < k; ++j) {
+    // the real node's send of step j (forwarding what arrived at step j-1)
+    const int64_t t_fr = j == 0 ? rec.t_start_ns : rel[j - 1];
+    emit(t_fr, "recv", "from_real", j, single && coll >= 0 ? send_chunk_at(coll, W, R, j) : -1);
+    emit(rel[j], "send", "to_real", j, single && coll >= 0 ? send_chunk_at(coll, W, prev, j) : -1);
+  }
+  emit(rec.t_end_ns, "complete", "-", -1, -1);
+  if (!out || s.size() + 1 > cap) return -static_cast<int>(s.size() + 1);
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
+}
+
 }  // extern "C"
 
 // launch counter for bench.py's gpu_launches (not part of the public header)

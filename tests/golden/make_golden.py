@@ -210,6 +210,31 @@ def real_ring_hash():
     dump("real_ring_hash.json", out)
 
 
+def eventlog():
+    """The reference emulator's own EventLog of delayed calls: the emulator-side
+    events (register, recv from_real, send to_real, complete) in log order."""
+    import tempfile
+    out = {"cases": []}
+    path = tempfile.mktemp(suffix=".trace")
+    R.trace_open(path)
+    cases = [(4, 0, 64 << 10, 4, 1, 10.0, 0.001, 0.0001, 0.0, 0.0),
+             (3, 1, 4096, 4, 2, 0.0, 0.0, 0.0, 300.0, 0.0),
+             (8, 0, 1 << 20, 4, 1, 5.0, 0.0005, 0.0, 0.0, 1000.0)]
+    for n, coll, plan_bytes, elem, kind, a, b, g, fx, inj in cases:
+        start = sum(1 for _ in open(path)) if os.path.exists(path) else 0
+        buf = np.zeros((plan_bytes * (n if coll == 1 else 1)) // 4, dtype=np.int32)
+        R.emulated_collective(n, coll, buf, plan_bytes, elem, kind, a, b, g, fx, inj, warmup=0, reps=1)
+        lines = open(path).read().splitlines()[start:]
+        ev = []
+        for ln in lines:
+            f = ln.split()
+            if len(f) == 6 and f[3] in ("to_real", "from_real", "-") and f[2] in ("register", "send", "recv", "complete"):
+                ev.append(f[2:])
+        out["cases"].append({"n": n, "coll": coll, "bytes": plan_bytes, "elem": elem, "kind": kind, "alpha": a,
+                             "beta": b, "gamma": g, "fixed": fx, "inject": inj, "events": ev})
+    dump("eventlog.json", out)
+
+
 def payload_vectors():
     """Self-pinned regression vectors of the (new) payload spec."""
     out = {"keys": [], "words": []}
@@ -230,4 +255,5 @@ if __name__ == "__main__":
     delay()
     emulated_zero()
     real_ring_hash()
+    eventlog()
     payload_vectors()

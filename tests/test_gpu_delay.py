@@ -184,3 +184,36 @@ def test_no_spin_kernel_when_delay_inactive(cuda):
     assert comm.kernel_launches - before == 1  # the synth-reduce kernel only
     assert not comm.call_record()["delay_active"]
     comm.close()
+
+
+def _by_direction(events):
+    out = {"to_real": [], "from_real": []}
+    for ev in events:
+        if ev[1] in out:
+            out[ev[1]].append((ev[0], ev[2], ev[3]))
+    return out
+
+
+def test_event_log_matches_reference_emulator_trace(cuda):
+    """The per-step schedule, dumped in the reference's EventLog format
+    (trace.hpp:10-34), carries exactly the (event, step, chunk) sequences the
+    reference emulator logs for the same call (tests/golden/eventlog.json)."""
+    from conftest import golden
+    for c in golden("eventlog.json")["cases"]:
+        comm = pb.Communicator(delay_config(c["n"], c["kind"], 0, c["alpha"], c["beta"], c["gamma"],
+                                            c["fixed"], c["inject"]), 0, 0)
+        count = c["bytes"] // 4
+        x = torch.zeros(count * (c["n"] if c["coll"] == 1 else 1), dtype=torch.int32, device="cuda")
+        if c["coll"] == 0:
+            comm.all_reduce(x, x)
+        else:
+            comm.all_gather(x[:count], x)
+        torch.cuda.synchronize()
+        lines = comm.event_log()
+        ours = [ln.split()[2:] for ln in lines]
+        assert ours[0][0] == "register" and ours[-1][0] == "complete"
+        assert _by_direction(ours) == _by_direction(c["events"]), (c["n"], c["coll"])
+        for d in ("to_real", "from_real"):
+            t = [int(ln.split()[0]) for ln in lines if ln.split()[3] == d]
+            assert t == sorted(t)
+        comm.close()
