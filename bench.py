@@ -342,8 +342,14 @@ def run_ours(args, rank, world_size, local_rank):
     nbytes = args.mib << 20
     count = nbytes // 4
     g = torch.Generator(device="cuda").manual_seed(rank)
-    x = torch.randn(count, device="cuda", generator=g)
-    y = torch.empty_like(x)
+    if n > 1:
+        # symmetric buffers: the allreduce runs as one fused kernel over
+        # NVLink peer memory (CEMU_FUSED=0 selects the NCCL RS/AG path)
+        x, y = comm.alloc(count, torch.float32), comm.alloc(count, torch.float32)
+        x.copy_(torch.randn(count, device="cuda", generator=g))
+    else:
+        x = torch.randn(count, device="cuda", generator=g)
+        y = torch.empty_like(x)
 
     def barrier():
         if n > 1:
@@ -397,9 +403,12 @@ def run_ours(args, rank, world_size, local_rank):
                     "kernel_ms_mean": round(kernel_ms, 5), "kernel_ms_min": round(min(per_ms), 5)}
     else:
         achieved = 2 * nbytes / (ms_per_step * 1e-3) / 1e9
+        fused = os.environ.get("CEMU_FUSED", "1") != "0"
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": None,
-                    "kernel": "per-GPU step: NCCL reduce-scatter + synth_reduce_vec<fp32> + NCCL allgather",
+                    "kernel": ("fused_allreduce_vec<fp32>: P2P pull of every real GPU's shard + synthesis + "
+                               "P2P push of the result, one launch per step") if fused else
+                              "NCCL reduce-scatter + synth_reduce_vec<fp32> + NCCL allgather",
                     "peak_source": peak_src}
 
     # e2e: pinned host buffers in and out every step, through the C-ABI

@@ -106,6 +106,18 @@ cemuResult_t cemuBroadcast(const void* sendbuff, void* recvbuff, size_t count,
 cemuResult_t cemuGroupStart(void);
 cemuResult_t cemuGroupEnd(void);
 
+/* Symmetric device memory (ncclMemAlloc / window-registration analogue).
+ * Collective over the job's real ranks on this box: each allocates `bytes`
+ * and maps every peer's allocation (CUDA IPC).  An allreduce whose send and
+ * recv lie in such buffers -- at the same offsets on every real rank -- runs
+ * as ONE fused kernel over NVLink peer memory instead of NCCL
+ * reduce-scatter + synthesis + NCCL allgather.  One real GPU: plain memory. */
+cemuResult_t cemuMemAlloc(cemuComm_t comm, size_t bytes, void** ptr);
+cemuResult_t cemuMemFree(cemuComm_t comm, void* ptr);
+/* Errors raised inside the fused kernel (a peer that never arrived at a
+ * barrier within CEMU_FUSED_TIMEOUT_S); synchronous read. */
+cemuResult_t cemuCommGetAsyncError(cemuComm_t comm, cemuResult_t* asyncError);
+
 /* ------------------------------------------------------------------ */
 /* Emulation observability: the per-call schedule record                */
 /* ------------------------------------------------------------------ */

@@ -75,6 +75,9 @@ def _load():
         "cemuAllGather": (i32, [vp, vp, sz, i32, vp, vp]),
         "cemuReduceScatter": (i32, [vp, vp, sz, i32, i32, vp, vp]),
         "cemuBroadcast": (i32, [vp, vp, sz, i32, i32, vp, vp]),
+        "cemuMemAlloc": (i32, [vp, sz, C.POINTER(vp)]),
+        "cemuMemFree": (i32, [vp, vp]),
+        "cemuCommGetAsyncError": (i32, [vp, C.POINTER(i32)]),
         "cemuGroupStart": (i32, []),
         "cemuGroupEnd": (i32, []),
         "cemuCommLastCallId": (i32, [vp, C.POINTER(u64)]),

@@ -104,6 +104,19 @@ def get_unique_id() -> bytes:
     return C.string_at(C.addressof(uid), C.sizeof(uid))
 
 
+class _DeviceBuffer:
+    """__cuda_array_interface__ view of a cemuMemAlloc allocation."""
+
+    def __init__(self, ptr: int, numel: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+_TYPESTR = {torch.float32: ("<f4", None), torch.int32: ("<i4", None), torch.uint8: ("|u1", None),
+            torch.int8: ("|i1", None), torch.float16: ("<f2", None), torch.bfloat16: ("<i2", torch.bfloat16),
+            torch.float64: ("<f8", None), torch.int64: ("<i8", None)}
+
+
 def _stream_ptr(stream) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
@@ -170,6 +183,31 @@ class Communicator:
         for t in (send, recv):
             if not t.is_cuda or not t.is_contiguous():
                 raise CemuError(_capi.INVALID_ARGUMENT, "buffers must be contiguous CUDA tensors")
+
+    # -- symmetric memory (fused multi-GPU path) -------------------------------
+    def alloc(self, numel: int, dtype: torch.dtype) -> torch.Tensor:
+        """Tensor in cemuMemAlloc memory (collective across the real ranks).
+        Allreduces between such buffers (same offsets on every rank) run as
+        one fused kernel over NVLink peer memory."""
+        es = torch.empty(0, dtype=dtype).element_size()
+        p = C.c_void_p()
+        check(lib.cemuMemAlloc(self._h, max(numel * es, 1), C.byref(p)), self._h)
+        self._allocs = getattr(self, "_allocs", [])
+        self._allocs.append(p.value)
+        typestr, view = _TYPESTR[dtype]
+        with torch.cuda.device(self.device):
+            t = torch.as_tensor(_DeviceBuffer(p.value, numel, typestr), device=f"cuda:{self.device}")
+        return t.view(view) if view is not None else t
+
+    def free(self, t: torch.Tensor) -> None:
+        ptr = t.data_ptr()
+        check(lib.cemuMemFree(self._h, C.c_void_p(ptr)), self._h)
+        self._allocs.remove(ptr)
+
+    def async_error(self) -> str | None:
+        e = C.c_int()
+        check(lib.cemuCommGetAsyncError(self._h, C.byref(e)), self._h)
+        return None if e.value == 0 else lib.cemuGetLastError(self._h).decode()
 
     # -- observability --------------------------------------------------------
     @property

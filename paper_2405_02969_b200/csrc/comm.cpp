@@ -154,6 +154,18 @@ struct cemuComm {
   uint64_t calls = 0;
   ncclComm_t inner = nullptr;
   uint64_t launches = 0;
+  // fused multi-GPU path (k > 1): IPC-mapped signal areas and symmetric buffers
+  uint8_t* sig = nullptr;                 // local: flags[16] u64 | counter u32 | error u32
+  uint8_t* peer_sig[kMaxReal] = {};       // every real GPU's area (own = sig)
+  uint64_t epoch = 0;
+  bool fused = true;
+  int64_t fused_timeout_ns = 30'000'000'000LL;
+  struct Region {
+    uint8_t* base = nullptr;
+    size_t bytes = 0;
+    uint8_t* peer[kMaxReal] = {};  // own = base
+  };
+  std::vector<Region> regions;
 };
 
 namespace {
@@ -206,6 +218,75 @@ struct Call {
     return e;
   }
 };
+
+namespace {
+
+// All-gather `rec` (bytes each) among the k real GPUs through the inner NCCL
+// comm; synchronous (setup / registration only, never on the hot path).
+cudaError_t exchange_records(cemuComm* c, const void* rec, size_t bytes, std::vector<uint8_t>* all, ncclResult_t* nr) {
+  const Nccl* n = nccl();
+  uint8_t* d = nullptr;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaMalloc(&d, bytes * c->k);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) { cudaFree(d); return e; }
+  if ((e = cudaMemcpy(d + bytes * c->li, rec, bytes, cudaMemcpyHostToDevice)) == cudaSuccess) {
+    *nr = n->AllGather(d + bytes * c->li, d, bytes, ncclUint8, c->inner, st);
+    if (*nr == ncclSuccess) {
+      e = cudaStreamSynchronize(st);
+      all->resize(bytes * c->k);
+      if (e == cudaSuccess) e = cudaMemcpy(all->data(), d, bytes * c->k, cudaMemcpyDeviceToHost);
+    }
+  }
+  cudaStreamDestroy(st);
+  cudaFree(d);
+  return e;
+}
+
+struct IpcRecord {
+  cudaIpcMemHandle_t handle;
+  uint64_t bytes;
+};
+
+// Maps every real GPU's allocation `local` (collectively) into this process.
+cemuResult_t map_peers(cemuComm* c, void* local, size_t bytes, uint8_t** peers) {
+  IpcRecord mine{};
+  cudaError_t e = cudaIpcGetMemHandle(&mine.handle, local);
+  if (e != cudaSuccess) return fail(cemuUnhandledCudaError, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  mine.bytes = bytes;
+  std::vector<uint8_t> all;
+  ncclResult_t nr = ncclSuccess;
+  e = exchange_records(c, &mine, sizeof mine, &all, &nr);
+  if (nr != ncclSuccess) return fail(static_cast<cemuResult_t>(nr), "ipc handle exchange: nccl error");
+  if (e != cudaSuccess) return fail(cemuUnhandledCudaError, std::string("ipc handle exchange: ") + cudaGetErrorString(e));
+  for (uint32_t g = 0; g < c->k; ++g) {
+    IpcRecord r;
+    std::memcpy(&r, all.data() + g * sizeof r, sizeof r);
+    if (r.bytes != bytes) {
+      return fail(cemuInvalidUsage, "cemuMemAlloc: real ranks asked for different sizes (" + std::to_string(bytes) +
+                                        " vs " + std::to_string(r.bytes) + ")");
+    }
+    if (g == c->li) {
+      peers[g] = static_cast<uint8_t*>(local);
+      continue;
+    }
+    void* p = nullptr;
+    e = cudaIpcOpenMemHandle(&p, r.handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(cemuUnhandledCudaError, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    peers[g] = static_cast<uint8_t*>(p);
+  }
+  return cemuSuccess;
+}
+
+const cemuComm::Region* find_region(const cemuComm* c, const void* p, size_t bytes) {
+  const auto* b = static_cast<const uint8_t*>(p);
+  for (const auto& r : c->regions) {
+    if (b >= r.base && b + bytes <= r.base + r.bytes) return &r;
+  }
+  return nullptr;
+}
+
+}  // namespace
 
 #define CUDA_OK(expr)                                                                   \
   do {                                                                                  \
@@ -305,6 +386,14 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
     static_assert(sizeof(nid) == sizeof(id), "unique id size");
     std::memcpy(&nid, &id, sizeof nid);
     NCCL_OK(n->CommInitRank(&c->inner, static_cast<int>(c->k), nid, static_cast<int>(c->li)));
+    const char* fe = std::getenv("CEMU_FUSED");
+    c->fused = c->k <= static_cast<uint32_t>(kMaxReal) && !(fe && std::string(fe) == "0");
+    if (const char* t = std::getenv("CEMU_FUSED_TIMEOUT_S")) c->fused_timeout_ns = std::atoll(t) * 1'000'000'000LL;
+    if (c->fused) {
+      CUDA_OK(cudaMalloc(&c->sig, 4096));
+      CUDA_OK(cudaMemset(c->sig, 0, 4096));
+      if (auto r = map_peers(c.get(), c->sig, 4096, c->peer_sig)) return r;
+    }
   }
   *out = c.release();
   return cemuSuccess;
@@ -342,6 +431,43 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
     CUDA_OK(launch_synth_reduce(dt, send, recv, count, 0, nv, nk, call.take_stamp(), s, &call.launches));
     CUDA_OK(call.finish(kAllReduce));
     return cemuSuccess;
+  }
+  // k real GPUs, buffers from cemuMemAlloc: one fused kernel over peer memory
+  const cemuComm::Region* rs = c->fused ? find_region(c, send, count * es) : nullptr;
+  const cemuComm::Region* rr = c->fused ? find_region(c, recv, count * es) : nullptr;
+  if (rs && rr && dtype_size(dt) <= 4 && dt != cemuInt64) {
+    FusedArgs a;
+    const uint64_t epv = 16 / es;
+    const uint64_t nvec = count / epv;
+    const uint64_t per = nvec / c->k;
+    a.k = static_cast<int>(c->k);
+    a.me = static_cast<int>(c->li);
+    a.v_begin = per * c->li;
+    a.v_end = c->li + 1 == c->k ? nvec : per * (c->li + 1);
+    const bool last = c->li + 1 == c->k;
+    a.ntail = last ? static_cast<uint32_t>(count - nvec * epv) : 0;
+    a.tail_e0 = nvec * epv;
+    const uint64_t soff = static_cast<const uint8_t*>(send) - rs->base;
+    const uint64_t roff = static_cast<uint8_t*>(recv) - rr->base;
+    for (uint32_t g = 0; g < c->k; ++g) {
+      a.src[g] = reinterpret_cast<const uint4*>(rs->peer[g] + soff);
+      a.dst[g] = reinterpret_cast<uint4*>(rr->peer[g] + roff);
+      a.peer_flags[g] = reinterpret_cast<uint64_t*>(c->peer_sig[g]);
+    }
+    a.keys = c->d_virt_keys;
+    a.nkeys = static_cast<uint32_t>(c->virt.size());
+    a.flags = reinterpret_cast<uint64_t*>(c->sig);
+    a.counter = reinterpret_cast<uint32_t*>(c->sig + 256);
+    a.error = reinterpret_cast<uint32_t*>(c->sig + 260);
+    a.epoch = ++c->epoch;
+    a.stamp = call.take_stamp();
+    a.timeout_ns = c->fused_timeout_ns;
+    if ((soff | roff) % 16 == 0) {
+      CUDA_OK(launch_fused_allreduce(dt, a, s, &call.launches));
+      CUDA_OK(call.finish(kAllReduce));
+      return cemuSuccess;
+    }
+    --c->epoch;  // misaligned offsets: the NCCL path below
   }
   // k real GPUs: NCCL reduce-scatter of the real part, synthesis on this
   // GPU's 1/k shard only, NCCL allgather.
@@ -561,6 +687,16 @@ cemuResult_t cemuCommInitRank(cemuComm_t* comm, int nranks, cemuUniqueId id, int
 cemuResult_t cemuCommDestroy(cemuComm_t c) {
   if (!c) return cemuSuccess;
   cudaSetDevice(c->device);
+  for (auto& r : c->regions) {
+    for (uint32_t g = 0; g < c->k; ++g) {
+      if (g != c->li && r.peer[g]) cudaIpcCloseMemHandle(r.peer[g]);
+    }
+    cudaFree(r.base);
+  }
+  for (uint32_t g = 0; g < c->k; ++g) {
+    if (g != c->li && c->peer_sig[g]) cudaIpcCloseMemHandle(c->peer_sig[g]);
+  }
+  if (c->sig) cudaFree(c->sig);
   if (c->inner && nccl()) nccl()->CommDestroy(c->inner);
   cudaFree(c->d_virt_keys);
   cudaFree(c->d_virt_ranks);
@@ -689,6 +825,64 @@ cemuResult_t cemuCommCallRecord(cemuComm_t c, uint64_t id, cemuCallRecord* rec, 
   if (floors) std::memcpy(floors, h.data() + kSlotHeader, n * 8);
   if (release) std::memcpy(release, h.data() + kSlotHeader + c->kmax, n * 8);
   if (offsets) std::memcpy(offsets, h.data() + kSlotHeader + 2 * c->kmax, n * 8);
+  return cemuSuccess;
+}
+
+cemuResult_t cemuMemAlloc(cemuComm_t c, size_t bytes, void** ptr) {
+  if (!c || !ptr || bytes == 0) return fail(cemuInvalidArgument, "cemuMemAlloc: bad argument");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(cemuUnhandledCudaError, "cemuMemAlloc: cudaSetDevice");
+  const size_t rounded = (bytes + (2u << 20) - 1) & ~static_cast<size_t>((2u << 20) - 1);
+  void* p = nullptr;
+  CUDA_OK(cudaMalloc(&p, rounded));
+  cemuComm::Region r;
+  r.base = static_cast<uint8_t*>(p);
+  r.bytes = rounded;
+  r.peer[c->li] = r.base;
+  if (c->k > 1 && c->fused) {
+    if (auto e = map_peers(c, p, rounded, r.peer)) {
+      cudaFree(p);
+      return e;
+    }
+  }
+  c->regions.push_back(r);
+  *ptr = p;
+  return cemuSuccess;
+}
+
+cemuResult_t cemuMemFree(cemuComm_t c, void* ptr) {
+  if (!c || !ptr) return fail(cemuInvalidArgument, "cemuMemFree: bad argument");
+  for (size_t i = 0; i < c->regions.size(); ++i) {
+    auto& r = c->regions[i];
+    if (r.base != ptr) continue;
+    cudaSetDevice(c->device);
+    for (uint32_t g = 0; g < c->k; ++g) {
+      if (g != c->li && r.peer[g]) cudaIpcCloseMemHandle(r.peer[g]);
+    }
+    if (c->k > 1 && c->fused) {  // every peer unmapped before anyone frees
+      std::vector<uint8_t> all;
+      ncclResult_t nr = ncclSuccess;
+      const uint8_t one = 1;
+      exchange_records(c, &one, 1, &all, &nr);
+    }
+    cudaFree(r.base);
+    c->regions.erase(c->regions.begin() + static_cast<long>(i));
+    return cemuSuccess;
+  }
+  return fail(cemuInvalidArgument, "cemuMemFree: pointer was not returned by cemuMemAlloc");
+}
+
+cemuResult_t cemuCommGetAsyncError(cemuComm_t c, cemuResult_t* err) {
+  if (!c || !err) return fail(cemuInvalidArgument, "cemuCommGetAsyncError: null argument");
+  *err = cemuSuccess;
+  if (!c->sig) return cemuSuccess;
+  uint32_t e = 0;
+  cudaSetDevice(c->device);
+  CUDA_OK(cudaMemcpy(&e, c->sig + 260, 4, cudaMemcpyDeviceToHost));
+  if (e) {
+    *err = cemuRemoteError;
+    g_last_error = e == 1 ? "fused allreduce: a peer never started (start barrier timed out)"
+                          : "fused allreduce: a peer never finished (done barrier timed out)";
+  }
   return cemuSuccess;
 }
 

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "delay_math.cuh"
 #include "kernels.hpp"
@@ -86,6 +87,25 @@ __device__ __forceinline__ uint32_t fold_f16x2(uint32_t packed, int32_t s_lo, in
   __half2 r;
   r.x = __float2half_rn(a);
   r.y = __float2half_rn(b);
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// a + b per element of packed 16-bit pairs: fp32 add, one rounding to T
+__device__ __forceinline__ uint32_t fold_bf16x2_add(uint32_t a, uint32_t b) {
+  __nv_bfloat162 va = *reinterpret_cast<__nv_bfloat162*>(&a);
+  __nv_bfloat162 vb = *reinterpret_cast<__nv_bfloat162*>(&b);
+  __nv_bfloat162 r;
+  r.x = __float2bfloat16_rn(__fadd_rn(__bfloat162float(va.x), __bfloat162float(vb.x)));
+  r.y = __float2bfloat16_rn(__fadd_rn(__bfloat162float(va.y), __bfloat162float(vb.y)));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+__device__ __forceinline__ uint32_t fold_f16x2_add(uint32_t a, uint32_t b) {
+  __half2 va = *reinterpret_cast<__half2*>(&a);
+  __half2 vb = *reinterpret_cast<__half2*>(&b);
+  __half2 r;
+  r.x = __float2half_rn(__fadd_rn(__half2float(va.x), __half2float(vb.x)));
+  r.y = __float2half_rn(__fadd_rn(__half2float(va.y), __half2float(vb.y)));
   return *reinterpret_cast<uint32_t*>(&r);
 }
 
@@ -224,6 +244,97 @@ __device__ __forceinline__ void decode_byte_sums(uint32_t a, uint32_t h, uint32_
   s[3] = s3;
 }
 
+// Emulated-peer sums for the U vectors of one thread-tile.  Byte kinds:
+// s[4i + e] = sum over peers of (byte e of word i) - bias, in int32; word
+// kinds: acc[i] = wrapping sum of word i.  ctr[] holds the hoisted c1 values.
+template <int K, int U, bool kMulti>
+__device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skeys, uint32_t nkeys,
+                                          uint32_t one, int32_t* s, uint32_t* acc) {
+  using T = VT<K>;
+  constexpr int NW = U * T::WPV;
+  if constexpr (T::kWords) {
+#pragma unroll
+    for (int i = 0; i < NW; ++i) acc[i] = 0;
+#pragma unroll 2
+    for (uint32_t q = 0; q < nkeys; ++q) {
+      const uint2 key = skeys[q];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) acc[i] = mad_add(payload_mix(key.x, key.y, ctr[i]), one, acc[i]);
+    }
+  } else {
+    const uint32_t groups = kMulti ? (nkeys + 255) / 256 : 1;
+#pragma unroll
+    for (int i = 0; i < NW * 4; ++i) s[i] = 0;
+    for (uint32_t g = 0; g < groups; ++g) {
+      const uint32_t q0 = g * 256;
+      const uint32_t q1 = kMulti ? min(nkeys, q0 + 256) : nkeys;
+      uint32_t a[NW], h[NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) a[i] = h[i] = 0;
+#pragma unroll 2
+      for (uint32_t q = q0; q < q1; ++q) {
+        const uint2 key = skeys[q];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          const uint32_t w = payload_mix(key.x, key.y, ctr[i]);
+          a[i] = mad_add(w, one, a[i]);
+          h[i] = mad_add(__byte_perm(w, 0u, 0x4341), one, h[i]);
+        }
+      }
+      // float kinds carry the -128 offset of the dyadic value; bytes wrap
+      const int32_t bias = K == kU8 ? 0 : 128 * static_cast<int32_t>(q1 - q0);
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        uint32_t t[4];
+        decode_byte_sums(a[i], h[i], t);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[i * 4 + e] += static_cast<int32_t>(t[e]) - bias;
+      }
+    }
+  }
+}
+
+// One rounding per element: x (+) S * 2^-7 (floats), x + sum (integers).
+// `s`/`acc` point at the sums of this vector's words.
+template <int K>
+__device__ __forceinline__ uint4 fold_vec(const uint4& x, const int32_t* s, const uint32_t* acc) {
+  uint4 y;
+  if constexpr (VT<K>::kWords) {
+    y.x = x.x + acc[0];
+    y.y = x.y + acc[1];
+    y.z = x.z + acc[2];
+    y.w = x.w + acc[3];
+  } else if constexpr (K == kF32) {
+    y.x = u32_of(fold_f32(f32_of(x.x), s[0]));
+    y.y = u32_of(fold_f32(f32_of(x.y), s[1]));
+    y.z = u32_of(fold_f32(f32_of(x.z), s[2]));
+    y.w = u32_of(fold_f32(f32_of(x.w), s[3]));
+  } else if constexpr (K == kBF16) {  // words 0 (elements 0..3) and 1 (4..7)
+    y.x = fold_bf16x2(x.x, s[0], s[1]);
+    y.y = fold_bf16x2(x.y, s[2], s[3]);
+    y.z = fold_bf16x2(x.z, s[4], s[5]);
+    y.w = fold_bf16x2(x.w, s[6], s[7]);
+  } else if constexpr (K == kF16) {
+    y.x = fold_f16x2(x.x, s[0], s[1]);
+    y.y = fold_f16x2(x.y, s[2], s[3]);
+    y.z = fold_f16x2(x.z, s[4], s[5]);
+    y.w = fold_f16x2(x.w, s[6], s[7]);
+  } else {  // kU8: byte e of word i is S[4i + e] mod 256
+    uint32_t p[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int32_t* t = s + w * 4;
+      p[w] = (static_cast<uint32_t>(t[0]) & 0xFFu) | ((static_cast<uint32_t>(t[1]) & 0xFFu) << 8) |
+             ((static_cast<uint32_t>(t[2]) & 0xFFu) << 16) | (static_cast<uint32_t>(t[3]) << 24);
+    }
+    y.x = add_bytes(x.x, p[0]);
+    y.y = add_bytes(x.y, p[1]);
+    y.z = add_bytes(x.z, p[2]);
+    y.w = add_bytes(x.w, p[3]);
+  }
+  return y;
+}
+
 template <int K, int DT, int U, bool kMulti>
 __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     const uint4* __restrict__ src, uint4* dst, uint64_t nvec, uint64_t word_base,
@@ -253,106 +364,201 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
 #pragma unroll
       for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(word_base + v * W + w);
     }
-
-    uint4 y[U];
-    if constexpr (T::kWords) {
-      // int32 lanes: plain wrapping sums, one payload word per element
-      uint32_t acc[NW];
-#pragma unroll
-      for (int i = 0; i < NW; ++i) acc[i] = 0;
-#pragma unroll 2
-      for (uint32_t q = 0; q < nkeys; ++q) {
-        const uint2 key = skeys[q];
-#pragma unroll
-        for (int i = 0; i < NW; ++i) acc[i] = mad_add(payload_mix(key.x, key.y, ctr[i]), one, acc[i]);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        y[u].x = x[u].x + acc[u * 4 + 0];
-        y[u].y = x[u].y + acc[u * 4 + 1];
-        y[u].z = x[u].z + acc[u * 4 + 2];
-        y[u].w = x[u].w + acc[u * 4 + 3];
-      }
-    } else {
-      // 2. per-peer byte sums: S_e = sum over peers of byte e of the word,
-      //    accumulated as A (whole words) and H (odd bytes, 16-bit lanes)
-      int32_t s[NW * 4];
-      const uint32_t groups = kMulti ? (nkeys + 255) / 256 : 1;
-#pragma unroll
-      for (int i = 0; i < NW * 4; ++i) s[i] = 0;
-      for (uint32_t g = 0; g < groups; ++g) {
-        const uint32_t q0 = g * 256;
-        const uint32_t q1 = kMulti ? min(nkeys, q0 + 256) : nkeys;
-        uint32_t a[NW], h[NW];
-#pragma unroll
-        for (int i = 0; i < NW; ++i) a[i] = h[i] = 0;
-#pragma unroll 2
-        for (uint32_t q = q0; q < q1; ++q) {
-          const uint2 key = skeys[q];
-#pragma unroll
-          for (int i = 0; i < NW; ++i) {
-            const uint32_t w = payload_mix(key.x, key.y, ctr[i]);
-            a[i] = mad_add(w, one, a[i]);
-            h[i] = mad_add(__byte_perm(w, 0u, 0x4341), one, h[i]);
-          }
-        }
-        // float kinds carry the -128 offset of the dyadic value; bytes wrap
-        const int32_t bias = K == kU8 ? 0 : 128 * static_cast<int32_t>(q1 - q0);
-#pragma unroll
-        for (int i = 0; i < NW; ++i) {
-          uint32_t t[4];
-          decode_byte_sums(a[i], h[i], t);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) s[i * 4 + e] += static_cast<int32_t>(t[e]) - bias;
-        }
-      }
-      // 3. one rounding per element: local (+) S * 2^-7
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if constexpr (K == kF32) {
-          const int32_t* t = s + u * 4;
-          y[u].x = u32_of(fold_f32(f32_of(x[u].x), t[0]));
-          y[u].y = u32_of(fold_f32(f32_of(x[u].y), t[1]));
-          y[u].z = u32_of(fold_f32(f32_of(x[u].z), t[2]));
-          y[u].w = u32_of(fold_f32(f32_of(x[u].w), t[3]));
-        } else if constexpr (K == kBF16 || K == kF16) {
-          const int32_t* t0 = s + (u * 2) * 4;      // elements 0..3
-          const int32_t* t1 = s + (u * 2 + 1) * 4;  // elements 4..7
-          if constexpr (K == kBF16) {
-            y[u].x = fold_bf16x2(x[u].x, t0[0], t0[1]);
-            y[u].y = fold_bf16x2(x[u].y, t0[2], t0[3]);
-            y[u].z = fold_bf16x2(x[u].z, t1[0], t1[1]);
-            y[u].w = fold_bf16x2(x[u].w, t1[2], t1[3]);
-          } else {
-            y[u].x = fold_f16x2(x[u].x, t0[0], t0[1]);
-            y[u].y = fold_f16x2(x[u].y, t0[2], t0[3]);
-            y[u].z = fold_f16x2(x[u].z, t1[0], t1[1]);
-            y[u].w = fold_f16x2(x[u].w, t1[2], t1[3]);
-          }
-        } else {  // kU8: byte e of word i is S[4i + e] mod 256
-          uint32_t p[4];
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int32_t* t = s + (u * 4 + w) * 4;
-            p[w] = (static_cast<uint32_t>(t[0]) & 0xFFu) | ((static_cast<uint32_t>(t[1]) & 0xFFu) << 8) |
-                   ((static_cast<uint32_t>(t[2]) & 0xFFu) << 16) | (static_cast<uint32_t>(t[3]) << 24);
-          }
-          y[u].x = add_bytes(x[u].x, p[0]);
-          y[u].y = add_bytes(x[u].y, p[1]);
-          y[u].z = add_bytes(x[u].z, p[2]);
-          y[u].w = add_bytes(x[u].w, p[3]);
-        }
-      }
-    }
+    // 2. the emulated peers' sums (registers only), 3. fold + stream out
+    int32_t s[T::kWords ? 1 : NW * 4];
+    uint32_t acc[T::kWords ? NW : 1];
+    peer_sums<K, U, kMulti>(ctr, skeys, nkeys, one, s, acc);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
-      if (v < nvec) st_stream(dst + v, y[u]);
+      if (v < nvec) st_stream(dst + v, fold_vec<K>(x[u], s + u * W * 4, acc + (T::kWords ? u * 4 : 0)));
     }
   }
   // ragged tail (< one vector): the last block's first threads
   if (ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < ntail) {
     elem_reduce<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, skeys, nkeys);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// fused multi-GPU allreduce over peer memory
+// ---------------------------------------------------------------------------
+// With k real GPUs on the box, GPU `me` owns 1/k of the vectors: it pulls
+// that slice from every real GPU's send buffer over NVLink (P2P loads), sums
+// the real contributions in ascending real-rank order, adds the W-k emulated
+// ranks' synthesised payloads in the same pass, and pushes the result into
+// every real GPU's recv buffer (P2P stores).  One launch replaces NCCL
+// reduce-scatter + synthesis + NCCL allgather; every byte crosses NVLink
+// once each way, overlapped with the synthesis.  Cross-GPU ordering uses
+// epoch flags in IPC-mapped memory (release/acquire at system scope):
+//   start: each GPU's first CTA tells every peer "my kernel started" (so its
+//          stream's earlier writes to send are complete); every CTA waits
+//          for all peers' start flags before its first remote load;
+//   done:  the last CTA to finish on each GPU tells every peer "my writes
+//          into your recv are done" and waits for the same from all peers,
+//          so the kernel ends only when its recv buffer is complete.
+// Every wait has a %globaltimer timeout that sets `error` instead of hanging.
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ bool wait_flag(const uint64_t* f, uint64_t epoch, int64_t t0, int64_t timeout) {
+  while (ld_acquire_sys(f) < epoch) {
+    if (globaltimer_ns() - t0 > timeout) return false;
+    __nanosleep(64);
+  }
+  return true;
+}
+
+// real-part fold in the datatype's own arithmetic (the oracle's real_sum)
+template <int K>
+__device__ __forceinline__ uint4 add_real(const uint4& a, const uint4& b) {
+  uint4 r;
+  if constexpr (K == kF32) {
+    r.x = u32_of(__fadd_rn(f32_of(a.x), f32_of(b.x)));
+    r.y = u32_of(__fadd_rn(f32_of(a.y), f32_of(b.y)));
+    r.z = u32_of(__fadd_rn(f32_of(a.z), f32_of(b.z)));
+    r.w = u32_of(__fadd_rn(f32_of(a.w), f32_of(b.w)));
+  } else if constexpr (K == kBF16) {
+    r.x = fold_bf16x2_add(a.x, b.x);
+    r.y = fold_bf16x2_add(a.y, b.y);
+    r.z = fold_bf16x2_add(a.z, b.z);
+    r.w = fold_bf16x2_add(a.w, b.w);
+  } else if constexpr (K == kF16) {
+    r.x = fold_f16x2_add(a.x, b.x);
+    r.y = fold_f16x2_add(a.y, b.y);
+    r.z = fold_f16x2_add(a.z, b.z);
+    r.w = fold_f16x2_add(a.w, b.w);
+  } else if constexpr (K == kU8) {
+    r.x = add_bytes(a.x, b.x);
+    r.y = add_bytes(a.y, b.y);
+    r.z = add_bytes(a.z, b.z);
+    r.w = add_bytes(a.w, b.w);
+  } else {
+    r.x = a.x + b.x;
+    r.y = a.y + b.y;
+    r.z = a.z + b.z;
+    r.w = a.w + b.w;
+  }
+  return r;
+}
+
+// ragged elements after the last full vector: same fold, one element
+template <int DT>
+__device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* skeys) {
+  using S = typename std::conditional<
+      DT == cemuInt8 || DT == cemuUint8, uint8_t,
+      typename std::conditional<DT == cemuFloat16 || DT == cemuBfloat16, uint16_t, uint32_t>::type>::type;
+  S acc = reinterpret_cast<const S*>(a.src[0] + a.v_end)[i];
+  for (int g = 1; g < a.k; ++g) {
+    const S b = reinterpret_cast<const S*>(a.src[g] + a.v_end)[i];
+    if constexpr (DT == cemuFloat32) {
+      acc = u32_of(__fadd_rn(f32_of(acc), f32_of(b)));
+    } else if constexpr (DT == cemuBfloat16) {
+      const uint32_t r = fold_bf16x2_add(static_cast<uint32_t>(acc), static_cast<uint32_t>(b));
+      acc = static_cast<S>(r & 0xFFFFu);
+    } else if constexpr (DT == cemuFloat16) {
+      const uint32_t r = fold_f16x2_add(static_cast<uint32_t>(acc), static_cast<uint32_t>(b));
+      acc = static_cast<S>(r & 0xFFFFu);
+    } else {
+      acc = static_cast<S>(acc + b);
+    }
+  }
+  S out;
+  elem_reduce<DT>(&acc, &out, 0, a.tail_e0 + i, skeys, a.nkeys);
+  for (int g = 0; g < a.k; ++g) reinterpret_cast<S*>(a.dst[g] + a.v_end)[i] = out;
+}
+
+template <int K, int DT, int KMAX, bool kMulti>
+__global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_constant__ FusedArgs a) {
+  using T = VT<K>;
+  constexpr int U = 2, W = T::WPV, NW = U * W;
+  extern __shared__ uint2 skeys[];
+  __shared__ int abort_s;
+  const int64_t t0 = globaltimer_ns();
+  if (a.stamp && blockIdx.x == 0 && threadIdx.x == 0) *a.stamp = t0;
+  // start barrier: announce, then wait for every peer's announcement
+  if (blockIdx.x == 0 && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
+    st_release_sys(a.peer_flags[threadIdx.x] + a.me, a.epoch);
+  }
+  if (threadIdx.x == 0) abort_s = 0;
+  load_keys(skeys, a.keys, a.nkeys);
+  if (threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
+    if (!wait_flag(a.flags + threadIdx.x, a.epoch, t0, a.timeout_ns)) {
+      atomicExch(a.error, 1u);
+      abort_s = 1;
+    }
+  }
+  __syncthreads();
+  if (abort_s) return;
+
+  const uint64_t tile = static_cast<uint64_t>(kThreads) * U;
+  for (uint64_t base = a.v_begin + static_cast<uint64_t>(blockIdx.x) * tile; base < a.v_end;
+       base += static_cast<uint64_t>(gridDim.x) * tile) {
+    // every real GPU's slice first (local HBM + NVLink), then synthesis
+    uint4 x[KMAX][U];
+#pragma unroll
+    for (int g = 0; g < KMAX; ++g) {
+      if (g < a.k) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
+          if (v < a.v_end) x[g][u] = ld_stream(a.src[g] + v);
+        }
+      }
+    }
+    uint32_t ctr[NW];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
+#pragma unroll
+      for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(v * W + w);
+    }
+    int32_t s[T::kWords ? 1 : NW * 4];
+    uint32_t acc[T::kWords ? NW : 1];
+    peer_sums<K, U, kMulti>(ctr, skeys, a.nkeys, 1u, s, acc);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
+      if (v >= a.v_end) continue;
+      uint4 real = x[0][u];
+#pragma unroll
+      for (int g = 1; g < KMAX; ++g) {
+        if (g < a.k) real = add_real<K>(real, x[g][u]);
+      }
+      const uint4 y = fold_vec<K>(real, s + u * W * 4, acc + (T::kWords ? u * 4 : 0));
+#pragma unroll
+      for (int g = 0; g < KMAX; ++g) {
+        if (g < a.k) st_stream(a.dst[g] + v, y);
+      }
+    }
+  }
+  if (a.ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < a.ntail) fused_tail_elem<DT>(a, threadIdx.x, skeys);
+
+  // done barrier: the last CTA on this GPU publishes and waits
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(a.counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *a.counter = 0;
+      __threadfence_system();
+      for (int g = 0; g < a.k; ++g) {
+        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, a.epoch);
+      }
+      for (int g = 0; g < a.k; ++g) {
+        if (g != a.me && !wait_flag(a.flags + 8 + g, a.epoch, globaltimer_ns(), a.timeout_ns)) {
+          atomicExch(a.error, 2u);
+        }
+      }
+    }
   }
 }
 
@@ -726,6 +932,41 @@ cudaError_t launch_synth_fill(int dtype, void* dst, uint64_t block_elems, const 
     case cemuFloat64:
       return fill_scalar<cemuFloat64>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
     default: --*launches; return cudaErrorInvalidValue;
+  }
+}
+
+namespace {
+template <int K, int DT, int KMAX>
+cudaError_t fused_k(const FusedArgs& a, cudaStream_t s) {
+  const bool multi = !VT<K>::kWords && a.nkeys > 256;
+  auto kern = multi ? fused_allreduce_vec<K, DT, KMAX, true> : fused_allreduce_vec<K, DT, KMAX, false>;
+  const uint64_t nvec = a.v_end - a.v_begin;
+  const uint64_t tiles = (nvec + 2ull * kThreads - 1) / (2ull * kThreads);
+  const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * 4));
+  kern<<<static_cast<unsigned>(grid), kThreads, static_cast<size_t>(a.nkeys) * 8, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K, int DT>
+cudaError_t fused_kind(const FusedArgs& a, cudaStream_t s) {
+  if (a.k <= 2) return fused_k<K, DT, 2>(a, s);
+  if (a.k <= 4) return fused_k<K, DT, 4>(a, s);
+  return fused_k<K, DT, 8>(a, s);
+}
+}  // namespace
+
+cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t s, int* launches) {
+  if (a.k < 2 || a.k > kMaxReal || a.nkeys > kMaxKeys) return cudaErrorInvalidValue;
+  ++*launches;
+  switch (dtype) {
+    case cemuFloat32: return fused_kind<kF32, cemuFloat32>(a, s);
+    case cemuBfloat16: return fused_kind<kBF16, cemuBfloat16>(a, s);
+    case cemuFloat16: return fused_kind<kF16, cemuFloat16>(a, s);
+    case cemuUint8: return fused_kind<kU8, cemuUint8>(a, s);
+    case cemuInt8: return fused_kind<kU8, cemuInt8>(a, s);
+    case cemuInt32: return fused_kind<kI32, cemuInt32>(a, s);
+    case cemuUint32: return fused_kind<kI32, cemuUint32>(a, s);
+    default: --*launches; return cudaErrorNotSupported;
   }
 }
 

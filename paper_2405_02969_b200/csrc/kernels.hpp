@@ -46,6 +46,28 @@ cudaError_t launch_synth_fill(int dtype, void* dst, uint64_t block_elems,
                               uint32_t own_index, int64_t* stamp, cudaStream_t stream,
                               int* launches);
 
+// One-kernel multi-GPU allreduce over peer memory (see kernels.cu).
+constexpr int kMaxReal = 8;
+struct FusedArgs {
+  const uint4* src[kMaxReal];  // real GPUs' send buffers, ascending real rank (own = local)
+  uint4* dst[kMaxReal];        // real GPUs' recv buffers
+  int k = 0, me = 0;
+  uint64_t v_begin = 0, v_end = 0;  // 16-byte vectors this GPU reduces
+  uint32_t ntail = 0;               // ragged elements after the last vector (last GPU only)
+  uint64_t tail_e0 = 0;
+  const uint32_t* keys = nullptr;   // emulated ranks' payload keys
+  uint32_t nkeys = 0;
+  uint64_t* flags = nullptr;        // local signals: [0,8) start, [8,16) done
+  uint64_t* peer_flags[kMaxReal];   // every real GPU's signal area (own = local)
+  uint32_t* counter = nullptr;      // local CTA-completion counter
+  uint32_t* error = nullptr;        // set on barrier timeout
+  uint64_t epoch = 0;
+  int64_t* stamp = nullptr;
+  int64_t timeout_ns = 0;
+};
+// Returns cudaErrorNotSupported for datatypes without a vector path.
+cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t stream, int* launches);
+
 cudaError_t launch_stamp(int64_t* slot, cudaStream_t stream, int* launches);
 // chain: device int64 holding the previous spin's absolute deadline (or null)
 cudaError_t launch_spin_ns(int64_t ns, cudaStream_t stream, int* launches, int64_t* chain = nullptr,

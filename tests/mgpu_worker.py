@@ -70,6 +70,36 @@ def main():
                     rs = to_np(sends[real.index(root)]) if root in real else None
                     want = P.broadcast(dt, P.PAYLOAD_HASH, W, real, me, root, 1, rs, count)
                     assert_bit_equal(to_np(b), want, f"broadcast root={root} dt={dt}")
+        # fused path: symmetric buffers -> one kernel over NVLink peer memory,
+        # arbitrary (non-dyadic) floats: the real fold order is the oracle's
+        for dt in (7, 9, 6, 2, 1):
+            for count in (1, 5, 4096 * n + 13, (1 << 22) + 3):
+                g = np.random.default_rng(7 + count)
+                sends = []
+                for i in range(n):
+                    gi = np.random.default_rng(100 * i + count)
+                    if dt in (7, 9, 6):
+                        v = torch.from_numpy(gi.standard_normal(count).astype(np.float32)).to(TORCH[dt])
+                    else:
+                        v = torch.from_numpy(gi.integers(-2**31, 2**31, size=count).astype(np.int64)).to(TORCH[dt])
+                    sends.append(v)
+                off = int(g.integers(0, 64)) * 16 // torch.empty(0, dtype=TORCH[dt]).element_size()
+                x = comm.alloc(count + off, TORCH[dt])[off:]
+                y = comm.alloc(count + off, TORCH[dt])[off:]
+                x.copy_(sends[local].cuda())
+                torch.cuda.synchronize()
+                before = comm.kernel_launches
+                comm.all_reduce(x, y)
+                torch.cuda.synchronize()
+                assert comm.kernel_launches - before == 1, "fused path not taken"
+                assert comm.async_error() is None
+                want = P.allreduce(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(s) for s in sends], count)
+                assert_bit_equal(to_np(y), want, f"fused allreduce real={real} dt={dt} n={count}")
+                comm.all_reduce(x, x)  # in place
+                torch.cuda.synchronize()
+                assert_bit_equal(to_np(x), want, f"fused in-place real={real} dt={dt} n={count}")
+                comm.free(x._base if x._base is not None else x)
+                comm.free(y._base if y._base is not None else y)
         comm.close()
         dist.barrier()
     if local == 0:
