@@ -476,10 +476,10 @@ __device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* ske
   for (int g = 0; g < a.k; ++g) reinterpret_cast<S*>(a.dst[g] + a.v_end)[i] = out;
 }
 
-template <int K, int DT, int KMAX, bool kMulti>
+template <int K, int DT, int KMAX, int U, bool kMulti>
 __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_constant__ FusedArgs a) {
   using T = VT<K>;
-  constexpr int U = 2, W = T::WPV, NW = U * W;
+  constexpr int W = T::WPV, NW = U * W;
   extern __shared__ uint2 skeys[];
   __shared__ int abort_s;
   const int64_t t0 = globaltimer_ns();
@@ -936,15 +936,32 @@ cudaError_t launch_synth_fill(int dtype, void* dst, uint64_t block_elems, const 
 }
 
 namespace {
-template <int K, int DT, int KMAX>
-cudaError_t fused_k(const FusedArgs& a, cudaStream_t s) {
+// Launch shape of the fused kernel: U vectors per thread per tile, blocks
+// per SM (CEMU_FUSED_U / CEMU_FUSED_BPS override, tuning only).
+int fused_env(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+template <int K, int DT, int KMAX, int U>
+cudaError_t fused_ku(const FusedArgs& a, cudaStream_t s) {
+  static const int bps = std::max(1, fused_env("CEMU_FUSED_BPS", 4));
   const bool multi = !VT<K>::kWords && a.nkeys > 256;
-  auto kern = multi ? fused_allreduce_vec<K, DT, KMAX, true> : fused_allreduce_vec<K, DT, KMAX, false>;
+  auto kern = multi ? fused_allreduce_vec<K, DT, KMAX, U, true> : fused_allreduce_vec<K, DT, KMAX, U, false>;
   const uint64_t nvec = a.v_end - a.v_begin;
-  const uint64_t tiles = (nvec + 2ull * kThreads - 1) / (2ull * kThreads);
-  const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * 4));
+  const uint64_t tiles = (nvec + static_cast<uint64_t>(U) * kThreads - 1) / (static_cast<uint64_t>(U) * kThreads);
+  const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * bps));
   kern<<<static_cast<unsigned>(grid), kThreads, static_cast<size_t>(a.nkeys) * 8, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int K, int DT, int KMAX>
+cudaError_t fused_k(const FusedArgs& a, cudaStream_t s) {
+  static const int u = fused_env("CEMU_FUSED_U", 2);
+  if constexpr (KMAX <= 4 && VT<K>::WPV == 1) {
+    if (u == 4) return fused_ku<K, DT, KMAX, 4>(a, s);
+  }
+  return fused_ku<K, DT, KMAX, 2>(a, s);
 }
 
 template <int K, int DT>

@@ -36,8 +36,9 @@ def assert_bit_equal(got: np.ndarray, want: np.ndarray, what: str = ""):
     g, w = bits(got), bits(want)
     if not np.array_equal(g, w):
         es = got.dtype.itemsize
-        diff = np.nonzero(g.reshape(-1, es).any(axis=1) != w.reshape(-1, es).any(axis=1) |
-                          (g.reshape(-1, es) != w.reshape(-1, es)).any(axis=1))[0]
+        if g.size != w.size:
+            raise AssertionError(f"{what}: size {got.size} != {want.size}")
+        diff = np.nonzero((g.reshape(-1, es) != w.reshape(-1, es)).any(axis=1))[0]
         raise AssertionError(f"{what}: {len(diff)} of {len(got)} elements differ; first at {diff[:5]}: "
                              f"got {got[diff[:3]]} want {want[diff[:3]]}")
 

@@ -17,7 +17,26 @@ from gpu_util import TORCH, assert_bit_equal, to_np  # noqa: E402
 from oracle import port as P  # noqa: E402
 
 
+def trace(msg):
+    if os.environ.get("MGPU_TRACE"):
+        print(f"[{os.environ['LOCAL_RANK']}] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
+    import threading
+    # a rank that fails leaves its peers inside collectives: bound the run
+    limit = float(os.environ.get("MGPU_WATCHDOG_S", "240"))
+    threading.Timer(limit, lambda: (print(f"watchdog: {limit}s", file=sys.stderr, flush=True), os._exit(3))).start()
+    try:
+        run()
+    except BaseException as e:  # noqa: BLE001
+        print(f"[{os.environ.get('LOCAL_RANK')}] FAILED: {e!r}", file=sys.stderr, flush=True)
+        os._exit(1)
+    sys.stdout.flush()
+    os._exit(0)
+
+
+def run():
     local = int(os.environ["LOCAL_RANK"])
     n = int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(local)
@@ -32,11 +51,13 @@ def main():
         comm = pb.Communicator(cfg, me, local, obj[0])
         for dt in (7, 9, 2):
             for count in (1, n * 1000 + 3, (1 << 20) + 7):
+                trace(f"real={real} dt={dt} count={count}")
                 sends = []
                 for i in range(n):
                     g = np.random.default_rng(1000 * i + count)
-                    if dt in (7, 9):  # dyadic: the real sum is exact in any order
-                        v = torch.from_numpy((g.integers(-256, 256, size=count) / 64).astype(np.float32)).to(TORCH[dt])
+                    if dt in (7, 9):  # dyadic, <= 5 significant bits: the real sum of <= 8
+                        # values is exact even in bf16, so NCCL's fold order cannot matter
+                        v = torch.from_numpy((g.integers(-16, 16, size=count) / 8).astype(np.float32)).to(TORCH[dt])
                     else:
                         v = torch.from_numpy(g.integers(-2**31, 2**31, size=count).astype(np.int32))
                     sends.append(v)
@@ -46,6 +67,7 @@ def main():
                 torch.cuda.synchronize()
                 want = P.allreduce(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(s) for s in sends], count)
                 assert_bit_equal(to_np(y), want, f"allreduce real={real} dt={dt} n={count}")
+                trace('allgather')
                 # allgather
                 blk = max(count // 8, 1)
                 recv = torch.empty(blk * W, dtype=x.dtype, device="cuda")
@@ -53,14 +75,16 @@ def main():
                 torch.cuda.synchronize()
                 want = P.allgather(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(s[:blk]) for s in sends], blk)
                 assert_bit_equal(to_np(recv), want, f"allgather real={real} dt={dt}")
+                trace('reduce-scatter over a buffer of W chunks')
                 # reduce-scatter over a buffer of W chunks
                 rc = max(count // 16, 1)
-                full = [torch.cat([s] * 16)[: rc * W] for s in sends]
+                full = [torch.cat([s] * -(-rc * W // count))[: rc * W] for s in sends]
                 out = torch.empty(rc, dtype=x.dtype, device="cuda")
                 comm.reduce_scatter(full[local].cuda(), out)
                 torch.cuda.synchronize()
                 want = P.reducescatter(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(f) for f in full], rc)
                 assert_bit_equal(to_np(out), want, f"reducescatter real={real} dt={dt}")
+                trace('broadcast from a real and from an emulated root')
                 # broadcast from a real and from an emulated root
                 for root in (real[-1], (real[-1] + 1) % W):
                     b = torch.empty_like(x)
@@ -84,6 +108,7 @@ def main():
                         v = torch.from_numpy(gi.integers(-2**31, 2**31, size=count).astype(np.int64)).to(TORCH[dt])
                     sends.append(v)
                 off = int(g.integers(0, 64)) * 16 // torch.empty(0, dtype=TORCH[dt]).element_size()
+                trace(f"fused real={real} dt={dt} count={count}")
                 x = comm.alloc(count + off, TORCH[dt])[off:]
                 y = comm.alloc(count + off, TORCH[dt])[off:]
                 x.copy_(sends[local].cuda())
@@ -91,6 +116,7 @@ def main():
                 before = comm.kernel_launches
                 comm.all_reduce(x, y)
                 torch.cuda.synchronize()
+                trace("fused call done")
                 assert comm.kernel_launches - before == 1, "fused path not taken"
                 assert comm.async_error() is None
                 want = P.allreduce(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(s) for s in sends], count)

@@ -31,6 +31,6 @@ def test_multi_gpu_collectives_match_oracle():
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "mgpu_worker.py")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                         "--master-addr", "127.0.0.1", "--master-port", str(_port()), worker],
-                       capture_output=True, text=True, timeout=600)
+                       capture_output=True, text=True, timeout=420)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"MGPU OK {n}" in r.stdout
