@@ -1,0 +1,53 @@
+"""GPU: the paper's interposition route.  tests/apps/nccl_app is an ordinary
+NCCL program; with LD_PRELOAD=libnccl_cemu.so and CEMU_CONFIG set, its
+ncclAllReduce becomes the emulated collective (world 8, 7 emulated ranks),
+bit-exact against the oracle.  Without the preload it is real NCCL."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import port as P
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+APP = os.path.join(ROOT, "tests", "apps", "nccl_app")
+SHIM = os.path.join(ROOT, "paper_2405_02969_b200", "libnccl_cemu.so")
+
+
+def _run(tmp_path, env_extra, nranks, count):
+    out = tmp_path / f"out_{nranks}_{count}.bin"
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([APP, str(nranks), str(count), str(out)], env=env, capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    return np.fromfile(out, dtype=np.float32), r.stdout
+
+
+def test_unmodified_nccl_app_under_ld_preload(cuda, tmp_path):
+    cfg = tmp_path / "job.cfg"
+    cfg.write_text("world_size = 8\nreal_ranks = 0\nbucket_bytes = 65536\n")
+    count = (1 << 20) + 3
+    x = (np.arange(count) % 97).astype(np.float32) * 0.25
+    got, log = _run(tmp_path, {"CEMU_CONFIG": str(cfg), "LD_PRELOAD": SHIM}, 8, count)
+    assert "world 8" in log
+    want = P.allreduce(7, P.PAYLOAD_HASH, 8, [0], 0, 1, [x], count)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_same_app_is_plain_nccl_without_preload(cuda, tmp_path):
+    count = 4099
+    got, log = _run(tmp_path, {}, 1, count)  # a one-rank NCCL world: identity
+    assert np.array_equal(got, (np.arange(count) % 97).astype(np.float32) * 0.25)
+
+
+def test_world_size_mismatch_is_reported(cuda, tmp_path):
+    cfg = tmp_path / "job.cfg"
+    cfg.write_text("world_size = 8\nreal_ranks = 0\nbucket_bytes = 65536\n")
+    r = subprocess.run([APP, "4", "16", str(tmp_path / "x.bin")],
+                       env=dict(os.environ, CEMU_CONFIG=str(cfg), LD_PRELOAD=SHIM),
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and "ncclCommInitRank" in r.stderr

@@ -8,6 +8,7 @@
 """
 from __future__ import annotations
 
+import os
 import random
 import re
 import subprocess
@@ -38,6 +39,16 @@ def test_library_exports_every_header_symbol():
     assert not missing, missing
     for n in names:  # and they resolve through the loader
         getattr(_capi.lib, n)
+
+
+def test_nccl_interposer_exports_ncclapi():
+    shim = os.path.join(os.path.dirname(_capi.LIB_PATH), "libnccl_cemu.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", shim], capture_output=True, text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines()}
+    for name in ("ncclAllReduce", "ncclAllGather", "ncclReduceScatter", "ncclBroadcast", "ncclCommInitRank",
+                 "ncclCommDestroy", "ncclCommCount", "ncclCommUserRank", "ncclGetUniqueId", "ncclGroupStart",
+                 "ncclGroupEnd", "ncclGetErrorString"):
+        assert name in exported, name
 
 
 def test_library_is_sm100a_and_links_no_torch():
