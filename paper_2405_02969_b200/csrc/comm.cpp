@@ -166,6 +166,8 @@ struct cemuComm {
     uint8_t* peer[kMaxReal] = {};  // own = base
   };
   std::vector<Region> regions;
+  void* scratch = nullptr;  // aligned staging for misaligned local outputs
+  size_t scratch_bytes = 0;
 };
 
 namespace {
@@ -276,6 +278,29 @@ cemuResult_t map_peers(cemuComm* c, void* local, size_t bytes, uint8_t** peers) 
     peers[g] = static_cast<uint8_t*>(p);
   }
   return cemuSuccess;
+}
+
+cemuResult_t ensure_scratch(cemuComm* c, size_t bytes) {
+  if (c->scratch_bytes >= bytes) return cemuSuccess;
+  if (c->scratch) cudaFree(c->scratch);
+  c->scratch = nullptr;
+  c->scratch_bytes = 0;
+  const cudaError_t e = cudaMalloc(&c->scratch, bytes);
+  if (e != cudaSuccess) return fail(cemuUnhandledCudaError, std::string("staging buffer: ") + cudaGetErrorString(e));
+  c->scratch_bytes = bytes;
+  return cemuSuccess;
+}
+
+template <typename A>
+void set_barrier(cemuComm* c, A& a) {
+  for (uint32_t g = 0; g < c->k; ++g) a.peer_flags[g] = reinterpret_cast<uint64_t*>(c->peer_sig[g]);
+  a.k = static_cast<int>(c->k);
+  a.me = static_cast<int>(c->li);
+  a.flags = reinterpret_cast<uint64_t*>(c->sig);
+  a.counter = reinterpret_cast<uint32_t*>(c->sig + 256);
+  a.error = reinterpret_cast<uint32_t*>(c->sig + 260);
+  a.epoch = ++c->epoch;
+  a.timeout_ns = c->fused_timeout_ns;
 }
 
 const cemuComm::Region* find_region(const cemuComm* c, const void* p, size_t bytes) {
@@ -442,6 +467,8 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
     const uint64_t per = nvec / c->k;
     a.k = static_cast<int>(c->k);
     a.me = static_cast<int>(c->li);
+    a.ndst = a.k;
+    a.word_base = 0;
     a.v_begin = per * c->li;
     a.v_end = c->li + 1 == c->k ? nvec : per * (c->li + 1);
     const bool last = c->li + 1 == c->k;
@@ -452,22 +479,17 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
     for (uint32_t g = 0; g < c->k; ++g) {
       a.src[g] = reinterpret_cast<const uint4*>(rs->peer[g] + soff);
       a.dst[g] = reinterpret_cast<uint4*>(rr->peer[g] + roff);
-      a.peer_flags[g] = reinterpret_cast<uint64_t*>(c->peer_sig[g]);
     }
     a.keys = c->d_virt_keys;
     a.nkeys = static_cast<uint32_t>(c->virt.size());
-    a.flags = reinterpret_cast<uint64_t*>(c->sig);
-    a.counter = reinterpret_cast<uint32_t*>(c->sig + 256);
-    a.error = reinterpret_cast<uint32_t*>(c->sig + 260);
-    a.epoch = ++c->epoch;
-    a.stamp = call.take_stamp();
-    a.timeout_ns = c->fused_timeout_ns;
     if ((soff | roff) % 16 == 0) {
+      set_barrier(c, a);
+      a.ndst = a.k;
+      a.stamp = call.take_stamp();
       CUDA_OK(launch_fused_allreduce(dt, a, s, &call.launches));
       CUDA_OK(call.finish(kAllReduce));
       return cemuSuccess;
     }
-    --c->epoch;  // misaligned offsets: the NCCL path below
   }
   // k real GPUs: NCCL reduce-scatter of the real part, synthesis on this
   // GPU's 1/k shard only, NCCL allgather.
@@ -512,6 +534,32 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
     CUDA_OK(call.finish(kAllGather));
     return cemuSuccess;
   }
+  if (c->k > 1 && c->fused && es <= 4) {
+    // fused: push the own block to every real GPU over NVLink, synthesise the
+    // emulated blocks locally -- one kernel
+    const cemuComm::Region* rr = find_region(c, recv, sc * es * c->W);
+    const uint64_t roff = rr ? static_cast<uint64_t>(r8 - rr->base) : 1;
+    if (rr && roff % 16 == 0 && (sc * es) % 16 == 0) {  // symmetric conditions only
+      const void* own_src = send;
+      if (reinterpret_cast<uintptr_t>(send) % 16 != 0) {  // local: stage into the own block
+        own_src = r8 + static_cast<uint64_t>(c->rank) * sc * es;
+        if (own_src != send) CUDA_OK(cudaMemcpyAsync(const_cast<void*>(own_src), send, sc * es, cudaMemcpyDeviceToDevice, s));
+      }
+      FusedGatherArgs a;
+      set_barrier(c, a);
+      a.own = static_cast<const uint4*>(own_src);
+      for (uint32_t g = 0; g < c->k; ++g) a.dst[g] = reinterpret_cast<uint4*>(rr->peer[g] + roff);
+      a.own_block = c->rank;
+      a.block_vecs = sc * es / 16;
+      a.vranks = c->d_virt_ranks;
+      a.vkeys = c->d_virt_keys;
+      a.nvirt = nvirt;
+      a.stamp = call.take_stamp();
+      CUDA_OK(launch_fused_allgather(dt, a, s, &call.launches));
+      CUDA_OK(call.finish(kAllGather));
+      return cemuSuccess;
+    }
+  }
   const void* own = (c->k == 1 && !own_in_place) ? send : nullptr;
   CUDA_OK(launch_synth_fill(dt, recv, sc, c->d_virt_ranks, c->d_virt_keys, nvirt, 0, 0, own, c->rank,
                             call.take_stamp(), s, &call.launches));
@@ -551,6 +599,40 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
   if (c->k == 1) {
     CUDA_OK(launch_synth_reduce(dt, s8 + mine * es, recv, rc, mine, c->d_virt_keys, nk,
                                 call.take_stamp(), s, &call.launches));
+    CUDA_OK(call.finish(kReduceScatter));
+    return cemuSuccess;
+  }
+  // fused: pull this rank's chunk from every real GPU's (symmetric) send over
+  // NVLink, add the emulated ranks, write the local recv -- one kernel
+  // The decision must be the same on every real rank (they meet in the
+  // kernel's barriers), so it only looks at symmetric quantities: the send
+  // region offset and the chunk size.  A misaligned local recv is served
+  // through an aligned staging buffer instead of changing the decision.
+  const cemuComm::Region* rs = c->fused ? find_region(c, send, rc * es * c->W) : nullptr;
+  const uint64_t sbase = rs ? static_cast<uint64_t>(s8 - rs->base) : 1;
+  if (rs && es <= 4 && sbase % 16 == 0 && (rc * es) % 16 == 0) {
+    const uint64_t soff = sbase + mine * es;
+    void* out = recv;
+    if (reinterpret_cast<uintptr_t>(recv) % 16 != 0) {
+      if (auto r = ensure_scratch(c, rc * es)) return r;
+      out = c->scratch;
+    }
+    FusedArgs a;
+    set_barrier(c, a);
+    const uint64_t epv = 16 / es;
+    a.ndst = 1;
+    a.word_base = (dt == cemuInt32 || dt == cemuUint32) ? mine : mine / 4;
+    a.v_begin = 0;
+    a.v_end = rc / epv;
+    a.ntail = static_cast<uint32_t>(rc - a.v_end * epv);
+    a.tail_e0 = mine + a.v_end * epv;
+    for (uint32_t g = 0; g < c->k; ++g) a.src[g] = reinterpret_cast<const uint4*>(rs->peer[g] + soff);
+    a.dst[0] = static_cast<uint4*>(out);
+    a.keys = c->d_virt_keys;
+    a.nkeys = nk;
+    a.stamp = call.take_stamp();
+    CUDA_OK(launch_fused_allreduce(dt, a, s, &call.launches));
+    if (out != recv) CUDA_OK(cudaMemcpyAsync(recv, out, rc * es, cudaMemcpyDeviceToDevice, s));
     CUDA_OK(call.finish(kReduceScatter));
     return cemuSuccess;
   }
@@ -697,6 +779,7 @@ cemuResult_t cemuCommDestroy(cemuComm_t c) {
     if (g != c->li && c->peer_sig[g]) cudaIpcCloseMemHandle(c->peer_sig[g]);
   }
   if (c->sig) cudaFree(c->sig);
+  if (c->scratch) cudaFree(c->scratch);
   if (c->inner && nccl()) nccl()->CommDestroy(c->inner);
   cudaFree(c->d_virt_keys);
   cudaFree(c->d_virt_ranks);

@@ -473,7 +473,7 @@ __device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* ske
   }
   S out;
   elem_reduce<DT>(&acc, &out, 0, a.tail_e0 + i, skeys, a.nkeys);
-  for (int g = 0; g < a.k; ++g) reinterpret_cast<S*>(a.dst[g] + a.v_end)[i] = out;
+  for (int g = 0; g < a.ndst; ++g) reinterpret_cast<S*>(a.dst[g] + a.v_end)[i] = out;
 }
 
 template <int K, int DT, int KMAX, int U, bool kMulti>
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
 #pragma unroll
-      for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(v * W + w);
+      for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(a.word_base + v * W + w);
     }
     int32_t s[T::kWords ? 1 : NW * 4];
     uint32_t acc[T::kWords ? NW : 1];
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
       const uint4 y = fold_vec<K>(real, s + u * W * 4, acc + (T::kWords ? u * 4 : 0));
 #pragma unroll
       for (int g = 0; g < KMAX; ++g) {
-        if (g < a.k) st_stream(a.dst[g] + v, y);
+        if (g < a.ndst) st_stream(a.dst[g] + v, y);
       }
     }
   }
@@ -657,6 +657,68 @@ __global__ void __launch_bounds__(kThreads) synth_fill_scalar(void* dst, uint64_
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < block_elems;
        i += stride) {
     elem_fill<DT>(out, i, i, key);
+  }
+}
+
+// Fused allgather.  CTAs [0, push_ctas) copy the own block into every real
+// GPU's recv (local store + NVLink P2P stores) after the start barrier; the
+// remaining CTAs synthesise the emulated blocks into the local recv (HBM
+// writes only: regenerating an emulated block beats moving it).  Real peers'
+// blocks arrive by their own pushes; the done barrier makes them visible.
+template <int K>
+__global__ void __launch_bounds__(kThreads) fused_allgather_vec(const __grid_constant__ FusedGatherArgs a,
+                                                                uint32_t push_ctas) {
+  __shared__ int abort_s;
+  const int64_t t0 = globaltimer_ns();
+  if (a.stamp && blockIdx.x == 0 && threadIdx.x == 0) *a.stamp = t0;
+  if (blockIdx.x == 0 && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
+    st_release_sys(a.peer_flags[threadIdx.x] + a.me, a.epoch);
+  }
+  if (blockIdx.x < push_ctas) {
+    if (threadIdx.x == 0) abort_s = 0;
+    __syncthreads();
+    if (threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
+      if (!wait_flag(a.flags + threadIdx.x, a.epoch, t0, a.timeout_ns)) {
+        atomicExch(a.error, 1u);
+        abort_s = 1;
+      }
+    }
+    __syncthreads();
+    if (!abort_s) {
+      const uint64_t off = static_cast<uint64_t>(a.own_block) * a.block_vecs;
+      for (uint64_t v = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; v < a.block_vecs;
+           v += static_cast<uint64_t>(push_ctas) * kThreads) {
+        const uint4 x = ld_stream(a.own + v);
+        for (int g = 0; g < a.k; ++g) st_stream(a.dst[g] + off + v, x);
+      }
+    }
+  } else {
+    const uint64_t total = static_cast<uint64_t>(a.nvirt) * a.block_vecs;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x - push_ctas) * kThreads;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x - push_ctas) * kThreads + threadIdx.x; i < total;
+         i += stride) {
+      const uint64_t b = i / a.block_vecs, v = i - b * a.block_vecs;
+      const uint2 key = peer_consts(a.vkeys[b]);
+      st_stream(a.dst[a.me] + static_cast<uint64_t>(a.vranks[b]) * a.block_vecs + v,
+                synth_vector<K>(key, v * VT<K>::WPV));
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(a.counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *a.counter = 0;
+      __threadfence_system();
+      for (int g = 0; g < a.k; ++g) {
+        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, a.epoch);
+      }
+      for (int g = 0; g < a.k; ++g) {
+        if (g != a.me && !wait_flag(a.flags + 8 + g, a.epoch, globaltimer_ns(), a.timeout_ns)) {
+          atomicExch(a.error, 2u);
+        }
+      }
+    }
   }
 }
 
@@ -985,6 +1047,31 @@ cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t s
     case cemuUint32: return fused_kind<kI32, cemuUint32>(a, s);
     default: --*launches; return cudaErrorNotSupported;
   }
+}
+
+cudaError_t launch_fused_allgather(int dtype, const FusedGatherArgs& a, cudaStream_t s, int* launches) {
+  if (a.k < 2 || a.k > kMaxReal) return cudaErrorInvalidValue;
+  // NVLink push CTAs vs local synthesis CTAs, split by the bytes each moves
+  const uint64_t push_vecs = a.block_vecs;
+  const uint64_t synth_vecs = static_cast<uint64_t>(a.nvirt) * a.block_vecs;
+  const uint64_t total_ctas = static_cast<uint64_t>(sm_count()) * 4;
+  uint64_t push = std::max<uint64_t>(1, std::min<uint64_t>((push_vecs + kThreads - 1) / kThreads, total_ctas / 2));
+  uint64_t synth = synth_vecs ? std::max<uint64_t>(1, std::min<uint64_t>((synth_vecs + kThreads - 1) / kThreads,
+                                                                          total_ctas - push))
+                              : 0;
+  ++*launches;
+  const unsigned grid = static_cast<unsigned>(push + synth);
+  switch (dtype) {
+    case cemuFloat32: fused_allgather_vec<kF32><<<grid, kThreads, 0, s>>>(a, static_cast<uint32_t>(push)); break;
+    case cemuBfloat16: fused_allgather_vec<kBF16><<<grid, kThreads, 0, s>>>(a, static_cast<uint32_t>(push)); break;
+    case cemuFloat16: fused_allgather_vec<kF16><<<grid, kThreads, 0, s>>>(a, static_cast<uint32_t>(push)); break;
+    case cemuInt8: case cemuUint8: fused_allgather_vec<kU8><<<grid, kThreads, 0, s>>>(a, static_cast<uint32_t>(push)); break;
+    case cemuInt32: case cemuUint32:
+      fused_allgather_vec<kI32><<<grid, kThreads, 0, s>>>(a, static_cast<uint32_t>(push));
+      break;
+    default: --*launches; return cudaErrorNotSupported;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_stamp(int64_t* slot, cudaStream_t s, int* launches) {

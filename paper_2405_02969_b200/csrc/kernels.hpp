@@ -52,6 +52,8 @@ struct FusedArgs {
   const uint4* src[kMaxReal];  // real GPUs' send buffers, ascending real rank (own = local)
   uint4* dst[kMaxReal];        // real GPUs' recv buffers
   int k = 0, me = 0;
+  int ndst = 0;                     // k (allreduce: push to every GPU) or 1 (reduce-scatter)
+  uint64_t word_base = 0;           // payload word of vector 0 (reduce-scatter: own chunk)
   uint64_t v_begin = 0, v_end = 0;  // 16-byte vectors this GPU reduces
   uint32_t ntail = 0;               // ragged elements after the last vector (last GPU only)
   uint64_t tail_e0 = 0;
@@ -67,6 +69,27 @@ struct FusedArgs {
 };
 // Returns cudaErrorNotSupported for datatypes without a vector path.
 cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t stream, int* launches);
+
+// One-kernel multi-GPU allgather: push the own block to every real GPU over
+// NVLink while the same launch synthesises the emulated blocks locally.
+struct FusedGatherArgs {
+  const uint4* own = nullptr;   // local send block
+  uint4* dst[kMaxReal];         // every real GPU's recv buffer (own = local)
+  int k = 0, me = 0;
+  uint32_t own_block = 0;       // world rank of this GPU
+  uint64_t block_vecs = 0;      // 16-byte vectors per block
+  const uint32_t* vranks = nullptr;  // emulated ranks (block indices) and keys
+  const uint32_t* vkeys = nullptr;
+  uint32_t nvirt = 0;
+  uint64_t* flags = nullptr;
+  uint64_t* peer_flags[kMaxReal];
+  uint32_t* counter = nullptr;
+  uint32_t* error = nullptr;
+  uint64_t epoch = 0;
+  int64_t* stamp = nullptr;
+  int64_t timeout_ns = 0;
+};
+cudaError_t launch_fused_allgather(int dtype, const FusedGatherArgs& a, cudaStream_t stream, int* launches);
 
 cudaError_t launch_stamp(int64_t* slot, cudaStream_t stream, int* launches);
 // chain: device int64 holding the previous spin's absolute deadline (or null)

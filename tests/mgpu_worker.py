@@ -126,6 +126,33 @@ def run():
                 assert_bit_equal(to_np(x), want, f"fused in-place real={real} dt={dt} n={count}")
                 comm.free(x._base if x._base is not None else x)
                 comm.free(y._base if y._base is not None else y)
+                # fused reduce-scatter (symmetric send) and allgather (symmetric recv)
+                rc = max(count // 3, 8) // 8 * 8  # 16-byte chunks: the fused path (checked below)
+                full = [torch.cat([v] * -(-rc * W // count))[: rc * W] for v in sends]
+                xs = comm.alloc(rc * W, TORCH[dt])
+                xs.copy_(full[local].cuda())
+                # rank-local misalignment of the output must not change the path
+                out = torch.empty(rc + 1, dtype=TORCH[dt], device="cuda")[local % 2:][:rc]
+                torch.cuda.synchronize()
+                before = comm.kernel_launches
+                comm.reduce_scatter(xs, out)
+                torch.cuda.synchronize()
+                assert comm.kernel_launches - before == 1 and comm.async_error() is None
+                want = P.reducescatter(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(f) for f in full], rc)
+                assert_bit_equal(to_np(out), want, f"fused reducescatter real={real} dt={dt} rc={rc}")
+                blk = rc
+                ag = comm.alloc(blk * W, TORCH[dt])
+                mine = torch.cat([full[local][:1], full[local][:blk]]).cuda()[1:] if local % 2 else \
+                    full[local][:blk].cuda()
+                torch.cuda.synchronize()
+                before = comm.kernel_launches
+                comm.all_gather(mine, ag)
+                torch.cuda.synchronize()
+                assert comm.kernel_launches - before == 1 and comm.async_error() is None
+                want = P.allgather(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(f[:blk]) for f in full], blk)
+                assert_bit_equal(to_np(ag), want, f"fused allgather real={real} dt={dt} blk={blk}")
+                comm.free(xs)
+                comm.free(ag)
         comm.close()
         dist.barrier()
     if local == 0:
