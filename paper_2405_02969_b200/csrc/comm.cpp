@@ -291,6 +291,16 @@ cemuResult_t ensure_scratch(cemuComm* c, size_t bytes) {
   return cemuSuccess;
 }
 
+// 20-bit signature of a fused call; every real rank must compute the same
+uint32_t op_sig(int coll, int dt, uint64_t count) {
+  uint64_t h = 1469598103934665603ull;
+  for (uint64_t v : {static_cast<uint64_t>(coll), static_cast<uint64_t>(dt), count}) {
+    h ^= v;
+    h *= 1099511628211ull;
+  }
+  return static_cast<uint32_t>(h ^ (h >> 32)) & 0xFFFFFu;
+}
+
 template <typename A>
 void set_barrier(cemuComm* c, A& a) {
   for (uint32_t g = 0; g < c->k; ++g) a.peer_flags[g] = reinterpret_cast<uint64_t*>(c->peer_sig[g]);
@@ -484,6 +494,7 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
     a.nkeys = static_cast<uint32_t>(c->virt.size());
     if ((soff | roff) % 16 == 0) {
       set_barrier(c, a);
+      a.sig = op_sig(kAllReduce, dt, count);
       a.ndst = a.k;
       a.stamp = call.take_stamp();
       CUDA_OK(launch_fused_allreduce(dt, a, s, &call.launches));
@@ -547,6 +558,7 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
       }
       FusedGatherArgs a;
       set_barrier(c, a);
+      a.sig = op_sig(kAllGather, dt, sc);
       a.own = static_cast<const uint4*>(own_src);
       for (uint32_t g = 0; g < c->k; ++g) a.dst[g] = reinterpret_cast<uint4*>(rr->peer[g] + roff);
       a.own_block = c->rank;
@@ -619,6 +631,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
     }
     FusedArgs a;
     set_barrier(c, a);
+    a.sig = op_sig(kReduceScatter, dt, rc);
     const uint64_t epv = 16 / es;
     a.ndst = 1;
     a.word_base = (dt == cemuInt32 || dt == cemuUint32) ? mine : mine / 4;
@@ -963,8 +976,9 @@ cemuResult_t cemuCommGetAsyncError(cemuComm_t c, cemuResult_t* err) {
   CUDA_OK(cudaMemcpy(&e, c->sig + 260, 4, cudaMemcpyDeviceToHost));
   if (e) {
     *err = cemuRemoteError;
-    g_last_error = e == 1 ? "fused allreduce: a peer never started (start barrier timed out)"
-                          : "fused allreduce: a peer never finished (done barrier timed out)";
+    g_last_error = e == 1   ? "fused collective: a peer never started (start barrier timed out)"
+                   : e == 2 ? "fused collective: a peer never finished (done barrier timed out)"
+                            : "fused collective: real ranks disagree on the call (collective, dtype or count)";
   }
   return cemuSuccess;
 }

@@ -409,12 +409,25 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   return v;
 }
 
-__device__ __forceinline__ bool wait_flag(const uint64_t* f, uint64_t epoch, int64_t t0, int64_t timeout) {
-  while (ld_acquire_sys(f) < epoch) {
-    if (globaltimer_ns() - t0 > timeout) return false;
+// Flags hold (epoch << 20) | signature.  A start flag of the same epoch with
+// another signature means the ranks disagree on the call (error 3).
+constexpr int kSigBits = 20;
+__device__ __forceinline__ uint64_t flag_word(uint64_t epoch, uint32_t sig) {
+  return (epoch << kSigBits) | (sig & ((1u << kSigBits) - 1));
+}
+
+// 0 = arrived, 1 = timed out, 3 = signature mismatch
+__device__ __forceinline__ int wait_flag(const uint64_t* f, uint64_t epoch, uint32_t sig, bool check_sig,
+                                         int64_t t0, int64_t timeout) {
+  uint64_t v;
+  while (((v = ld_acquire_sys(f)) >> kSigBits) < epoch) {
+    if (globaltimer_ns() - t0 > timeout) return 1;
     __nanosleep(64);
   }
-  return true;
+  if (check_sig && (v >> kSigBits) == epoch && (v & ((1u << kSigBits) - 1)) != (sig & ((1u << kSigBits) - 1))) {
+    return 3;
+  }
+  return 0;
 }
 
 // real-part fold in the datatype's own arithmetic (the oracle's real_sum)
@@ -486,13 +499,14 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
   if (a.stamp && blockIdx.x == 0 && threadIdx.x == 0) *a.stamp = t0;
   // start barrier: announce, then wait for every peer's announcement
   if (blockIdx.x == 0 && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
-    st_release_sys(a.peer_flags[threadIdx.x] + a.me, a.epoch);
+    st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(a.epoch, a.sig));
   }
   if (threadIdx.x == 0) abort_s = 0;
   load_keys(skeys, a.keys, a.nkeys);
   if (threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
-    if (!wait_flag(a.flags + threadIdx.x, a.epoch, t0, a.timeout_ns)) {
-      atomicExch(a.error, 1u);
+    const int w = wait_flag(a.flags + threadIdx.x, a.epoch, a.sig, true, t0, a.timeout_ns);
+    if (w) {
+      atomicExch(a.error, static_cast<uint32_t>(w));
       abort_s = 1;
     }
   }
@@ -551,10 +565,10 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
       *a.counter = 0;
       __threadfence_system();
       for (int g = 0; g < a.k; ++g) {
-        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, a.epoch);
+        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, flag_word(a.epoch, 0));
       }
       for (int g = 0; g < a.k; ++g) {
-        if (g != a.me && !wait_flag(a.flags + 8 + g, a.epoch, globaltimer_ns(), a.timeout_ns)) {
+        if (g != a.me && wait_flag(a.flags + 8 + g, a.epoch, 0, false, globaltimer_ns(), a.timeout_ns)) {
           atomicExch(a.error, 2u);
         }
       }
@@ -672,14 +686,15 @@ __global__ void __launch_bounds__(kThreads) fused_allgather_vec(const __grid_con
   const int64_t t0 = globaltimer_ns();
   if (a.stamp && blockIdx.x == 0 && threadIdx.x == 0) *a.stamp = t0;
   if (blockIdx.x == 0 && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
-    st_release_sys(a.peer_flags[threadIdx.x] + a.me, a.epoch);
+    st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(a.epoch, a.sig));
   }
   if (blockIdx.x < push_ctas) {
     if (threadIdx.x == 0) abort_s = 0;
     __syncthreads();
     if (threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
-      if (!wait_flag(a.flags + threadIdx.x, a.epoch, t0, a.timeout_ns)) {
-        atomicExch(a.error, 1u);
+      const int w = wait_flag(a.flags + threadIdx.x, a.epoch, a.sig, true, t0, a.timeout_ns);
+      if (w) {
+        atomicExch(a.error, static_cast<uint32_t>(w));
         abort_s = 1;
       }
     }
@@ -711,10 +726,10 @@ __global__ void __launch_bounds__(kThreads) fused_allgather_vec(const __grid_con
       *a.counter = 0;
       __threadfence_system();
       for (int g = 0; g < a.k; ++g) {
-        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, a.epoch);
+        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, flag_word(a.epoch, 0));
       }
       for (int g = 0; g < a.k; ++g) {
-        if (g != a.me && !wait_flag(a.flags + 8 + g, a.epoch, globaltimer_ns(), a.timeout_ns)) {
+        if (g != a.me && wait_flag(a.flags + 8 + g, a.epoch, 0, false, globaltimer_ns(), a.timeout_ns)) {
           atomicExch(a.error, 2u);
         }
       }

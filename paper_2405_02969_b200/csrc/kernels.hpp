@@ -64,6 +64,7 @@ struct FusedArgs {
   uint32_t* counter = nullptr;      // local CTA-completion counter
   uint32_t* error = nullptr;        // set on barrier timeout
   uint64_t epoch = 0;
+  uint32_t sig = 0;                 // op signature (coll, dtype, count): must agree across ranks
   int64_t* stamp = nullptr;
   int64_t timeout_ns = 0;
 };
@@ -86,6 +87,7 @@ struct FusedGatherArgs {
   uint32_t* counter = nullptr;
   uint32_t* error = nullptr;
   uint64_t epoch = 0;
+  uint32_t sig = 0;
   int64_t* stamp = nullptr;
   int64_t timeout_ns = 0;
 };

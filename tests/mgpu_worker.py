@@ -153,6 +153,14 @@ def run():
                 assert_bit_equal(to_np(ag), want, f"fused allgather real={real} dt={dt} blk={blk}")
                 comm.free(xs)
                 comm.free(ag)
+        if real == layouts[-1]:
+            # ranks that disagree on a fused call fail loudly (error 3), not silently
+            x, y = comm.alloc(4096, torch.float32), comm.alloc(4096, torch.float32)
+            cnt = 1024 + 16 * local
+            comm.all_reduce(x[:cnt], y[:cnt])
+            torch.cuda.synchronize()
+            err = comm.async_error()
+            assert err is not None and "disagree" in err, err
         comm.close()
         dist.barrier()
     if local == 0:
