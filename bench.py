@@ -306,20 +306,30 @@ def sweep_block(torch, pb, device):
                 reps = 20 if size <= (64 << 20) else 5
                 for _ in range(3):
                     fn()
+                torch.cuda.synchronize(device)
+                # captured in a CUDA graph: small sizes measure the device
+                # work, not the Python launch path
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    for _ in range(reps):
+                        fn()
+                graph.replay()
                 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
                 e0.record()
-                for _ in range(reps):
-                    fn()
+                for _ in range(3):
+                    graph.replay()
                 e1.record()
                 torch.cuda.synchronize(device)
-                us = e0.elapsed_time(e1) * 1e3 / reps
+                us = e0.elapsed_time(e1) * 1e3 / (3 * reps)
+                del graph
                 pts.append([size, round(us, 2), round(algo / (us * 1e-6) / 1e9, 1)])
                 del x
             res[f"{coll}_{dname}"] = pts
     comm.close()
     return {"world": 64, "columns": ["buffer_bytes", "us_per_call", "algorithmic_GB/s"],
             "note": "allgather: in place, (n-1)*block written; reduce-scatter: own chunk read + written; "
-                    "small sizes are launch-latency bound (L2-resident, back-to-back)", **res}
+                    "each point = graph-captured back-to-back calls (device time); small sizes are "
+                    "kernel-launch bound and L2-resident", **res}
 
 
 def run_ours(args, rank, world_size, local_rank):

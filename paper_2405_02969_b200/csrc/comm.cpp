@@ -155,9 +155,8 @@ struct cemuComm {
   ncclComm_t inner = nullptr;
   uint64_t launches = 0;
   // fused multi-GPU path (k > 1): IPC-mapped signal areas and symmetric buffers
-  uint8_t* sig = nullptr;                 // local: flags[16] u64 | counter u32 | error u32
+  uint8_t* sig = nullptr;  // local: flags[16] u64 | counter u32 @256 | error u32 @260 | epoch u64 @264
   uint8_t* peer_sig[kMaxReal] = {};       // every real GPU's area (own = sig)
-  uint64_t epoch = 0;
   bool fused = true;
   int64_t fused_timeout_ns = 30'000'000'000LL;
   struct Region {
@@ -309,7 +308,7 @@ void set_barrier(cemuComm* c, A& a) {
   a.flags = reinterpret_cast<uint64_t*>(c->sig);
   a.counter = reinterpret_cast<uint32_t*>(c->sig + 256);
   a.error = reinterpret_cast<uint32_t*>(c->sig + 260);
-  a.epoch = ++c->epoch;
+  a.epoch = reinterpret_cast<uint64_t*>(c->sig + 264);
   a.timeout_ns = c->fused_timeout_ns;
 }
 

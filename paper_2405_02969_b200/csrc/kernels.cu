@@ -496,22 +496,28 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
   extern __shared__ uint2 skeys[];
   __shared__ int abort_s;
   const int64_t t0 = globaltimer_ns();
+  // every real GPU runs the same fused calls in the same order, so the local
+  // counters agree; the last CTA advances it when the call is complete
+  const uint64_t epoch = *a.epoch + 1;
   if (a.stamp && blockIdx.x == 0 && threadIdx.x == 0) *a.stamp = t0;
   // start barrier: announce, then wait for every peer's announcement
   if (blockIdx.x == 0 && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
-    st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(a.epoch, a.sig));
+    st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(epoch, a.sig));
   }
   if (threadIdx.x == 0) abort_s = 0;
   load_keys(skeys, a.keys, a.nkeys);
   if (threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
-    const int w = wait_flag(a.flags + threadIdx.x, a.epoch, a.sig, true, t0, a.timeout_ns);
+    const int w = wait_flag(a.flags + threadIdx.x, epoch, a.sig, true, t0, a.timeout_ns);
     if (w) {
       atomicExch(a.error, static_cast<uint32_t>(w));
       abort_s = 1;
     }
   }
   __syncthreads();
-  if (abort_s) return;
+  if (abort_s) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.epoch = epoch;
+    return;
+  }
 
   const uint64_t tile = static_cast<uint64_t>(kThreads) * U;
   for (uint64_t base = a.v_begin + static_cast<uint64_t>(blockIdx.x) * tile; base < a.v_end;
@@ -565,13 +571,14 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
       *a.counter = 0;
       __threadfence_system();
       for (int g = 0; g < a.k; ++g) {
-        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, flag_word(a.epoch, 0));
+        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, flag_word(epoch, 0));
       }
       for (int g = 0; g < a.k; ++g) {
-        if (g != a.me && wait_flag(a.flags + 8 + g, a.epoch, 0, false, globaltimer_ns(), a.timeout_ns)) {
+        if (g != a.me && wait_flag(a.flags + 8 + g, epoch, 0, false, globaltimer_ns(), a.timeout_ns)) {
           atomicExch(a.error, 2u);
         }
       }
+      *a.epoch = epoch;
     }
   }
 }
@@ -684,15 +691,16 @@ __global__ void __launch_bounds__(kThreads) fused_allgather_vec(const __grid_con
                                                                 uint32_t push_ctas) {
   __shared__ int abort_s;
   const int64_t t0 = globaltimer_ns();
+  const uint64_t epoch = *a.epoch + 1;
   if (a.stamp && blockIdx.x == 0 && threadIdx.x == 0) *a.stamp = t0;
   if (blockIdx.x == 0 && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
-    st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(a.epoch, a.sig));
+    st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(epoch, a.sig));
   }
   if (blockIdx.x < push_ctas) {
     if (threadIdx.x == 0) abort_s = 0;
     __syncthreads();
     if (threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
-      const int w = wait_flag(a.flags + threadIdx.x, a.epoch, a.sig, true, t0, a.timeout_ns);
+      const int w = wait_flag(a.flags + threadIdx.x, epoch, a.sig, true, t0, a.timeout_ns);
       if (w) {
         atomicExch(a.error, static_cast<uint32_t>(w));
         abort_s = 1;
@@ -726,13 +734,14 @@ __global__ void __launch_bounds__(kThreads) fused_allgather_vec(const __grid_con
       *a.counter = 0;
       __threadfence_system();
       for (int g = 0; g < a.k; ++g) {
-        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, flag_word(a.epoch, 0));
+        if (g != a.me) st_release_sys(a.peer_flags[g] + 8 + a.me, flag_word(epoch, 0));
       }
       for (int g = 0; g < a.k; ++g) {
-        if (g != a.me && wait_flag(a.flags + 8 + g, a.epoch, 0, false, globaltimer_ns(), a.timeout_ns)) {
+        if (g != a.me && wait_flag(a.flags + 8 + g, epoch, 0, false, globaltimer_ns(), a.timeout_ns)) {
           atomicExch(a.error, 2u);
         }
       }
+      *a.epoch = epoch;
     }
   }
 }

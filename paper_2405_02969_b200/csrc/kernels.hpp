@@ -63,7 +63,7 @@ struct FusedArgs {
   uint64_t* peer_flags[kMaxReal];   // every real GPU's signal area (own = local)
   uint32_t* counter = nullptr;      // local CTA-completion counter
   uint32_t* error = nullptr;        // set on barrier timeout
-  uint64_t epoch = 0;
+  uint64_t* epoch = nullptr;       // local device counter: this call is *epoch + 1 (graph-replay safe)
   uint32_t sig = 0;                 // op signature (coll, dtype, count): must agree across ranks
   int64_t* stamp = nullptr;
   int64_t timeout_ns = 0;
@@ -86,7 +86,7 @@ struct FusedGatherArgs {
   uint64_t* peer_flags[kMaxReal];
   uint32_t* counter = nullptr;
   uint32_t* error = nullptr;
-  uint64_t epoch = 0;
+  uint64_t* epoch = nullptr;       // local device counter: this call is *epoch + 1 (graph-replay safe)
   uint32_t sig = 0;
   int64_t* stamp = nullptr;
   int64_t timeout_ns = 0;

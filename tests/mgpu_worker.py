@@ -153,6 +153,29 @@ def run():
                 assert_bit_equal(to_np(ag), want, f"fused allgather real={real} dt={dt} blk={blk}")
                 comm.free(xs)
                 comm.free(ag)
+        # fused calls captured in a CUDA graph and replayed: the barrier epoch
+        # lives in device memory, so every replay synchronises afresh
+        xg, yg = comm.alloc(1 << 16, torch.float32), comm.alloc(1 << 16, torch.float32)
+        src = torch.from_numpy(np.random.default_rng(local).standard_normal(1 << 16).astype(np.float32)).cuda()
+        xg.copy_(src)
+        comm.all_reduce(xg, yg)
+        torch.cuda.synchronize()
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph):
+            for _ in range(3):
+                comm.all_reduce(xg, yg)
+        allsrc = [torch.from_numpy(np.random.default_rng(i).standard_normal(1 << 16).astype(np.float32)) for i in range(n)]
+        want = P.allreduce(7, P.PAYLOAD_HASH, W, real, me, 1, [to_np(v) for v in allsrc], 1 << 16)
+        for _ in range(4):
+            yg.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            gph.replay()
+            torch.cuda.synchronize()
+            assert comm.async_error() is None
+            assert_bit_equal(to_np(yg), want, f"fused graph replay real={real}")
+        comm.free(xg)
+        comm.free(yg)
         if real == layouts[-1]:
             # ranks that disagree on a fused call fail loudly (error 3), not silently
             x, y = comm.alloc(4096, torch.float32), comm.alloc(4096, torch.float32)
