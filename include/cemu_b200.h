@@ -74,6 +74,11 @@ cemuResult_t cemuGetUniqueId(cemuUniqueId* uniqueId);
  * by $CEMU_CONFIG; rank must be a real rank.  Device = the caller's current
  * CUDA device. */
 cemuResult_t cemuCommInitRank(cemuComm_t* comm, int nranks, cemuUniqueId commId, int rank);
+/* ncclCommInitAll shape: one process drives `ndev` GPUs (devlist, or
+ * 0..ndev-1), which serve the config's real ranks in ascending order.  Call
+ * the collectives of all these comms inside cemuGroupStart/End, as with
+ * NCCL.  (The fused peer-memory path needs one process per GPU.) */
+cemuResult_t cemuCommInitAll(cemuComm_t* comms, int ndev, const int* devlist);
 /* Same with the config given as text (reference key=value format). */
 cemuResult_t cemuCommInitRankConfig(cemuComm_t* comm, const char* configText,
                                     cemuUniqueId commId, int rank, int cudaDevice);

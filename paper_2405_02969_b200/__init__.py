@@ -13,7 +13,7 @@ this package without it raises -- there is no CPU fallback.
 from ._capi import CemuError, lib  # noqa: F401  (loads libcemu_b200.so or raises)
 from .comm import (  # noqa: F401
     ALLGATHER, ALLREDUCE, BROADCAST, REDUCESCATTER, CollectivePlanEntry, CollHandle, Communicator,
-    JobConfig, TransportError, WorkerSession, dtype_code, get_unique_id,
+    JobConfig, TransportError, WorkerSession, dtype_code, get_unique_id, group_end, group_start,
 )
 from . import schedule  # noqa: F401
 

@@ -65,6 +65,7 @@ def _load():
         "cemuGetUniqueId": (i32, [C.POINTER(UniqueId)]),
         "cemuCommInitRank": (i32, [C.POINTER(vp), i32, UniqueId, i32]),
         "cemuCommInitRankConfig": (i32, [C.POINTER(vp), cp, UniqueId, i32, i32]),
+        "cemuCommInitAll": (i32, [vp, i32, vp]),
         "cemuCommDestroy": (i32, [vp]),
         "cemuCommCount": (i32, [vp, C.POINTER(i32)]),
         "cemuCommUserRank": (i32, [vp, C.POINTER(i32)]),

@@ -97,6 +97,14 @@ class JobConfig:
             self._h = None
 
 
+def group_start() -> None:
+    check(lib.cemuGroupStart())
+
+
+def group_end() -> None:
+    check(lib.cemuGroupEnd())
+
+
 def get_unique_id() -> bytes:
     uid = UniqueId()
     check(lib.cemuGetUniqueId(C.byref(uid)))
@@ -144,6 +152,26 @@ class Communicator:
         self.config = JobConfig.parse(config_text)
         self.rank = rank
         self.world_size = self.config.world_size
+
+    @classmethod
+    def init_all(cls, config_path: str, devices: list[int]) -> list["Communicator"]:
+        """cemuCommInitAll (ncclCommInitAll shape): one process, one
+        communicator per device, serving the config's real ranks in order.
+        Issue their collectives inside group_start()/group_end()."""
+        import os
+        os.environ["CEMU_CONFIG"] = str(config_path)
+        n = len(devices)
+        handles = (C.c_void_p * n)()
+        devs = (C.c_int * n)(*devices)
+        check(lib.cemuCommInitAll(handles, n, devs))
+        text = open(config_path).read()
+        cfg = JobConfig.parse(text)
+        out = []
+        for i, (h, r) in enumerate(zip(handles, cfg.real_ranks)):
+            c = cls.__new__(cls)
+            c.device, c._h, c.config, c.rank, c.world_size = devices[i], C.c_void_p(h), cfg, r, cfg.world_size
+            out.append(c)
+        return out
 
     # -- collectives (NCCL argument meaning; out-of-place or in-place) -------
     def all_reduce(self, send: torch.Tensor, recv: torch.Tensor | None = None, stream=None):

@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <random>
@@ -54,6 +55,7 @@ struct Nccl {
   void* h = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
@@ -88,6 +90,7 @@ const Nccl* nccl() {
 #define CEMU_SYM(field, name) n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name))
       CEMU_SYM(GetUniqueId, "ncclGetUniqueId");
       CEMU_SYM(CommInitRank, "ncclCommInitRank");
+      CEMU_SYM(CommInitAll, "ncclCommInitAll");
       CEMU_SYM(CommDestroy, "ncclCommDestroy");
       CEMU_SYM(AllReduce, "ncclAllReduce");
       CEMU_SYM(AllGather, "ncclAllGather");
@@ -120,8 +123,13 @@ size_t dtype_size(int dt) {
 // Deferred calls between cemuGroupStart/End (NCCL group semantics: nothing
 // needs to start before ncclGroupEnd).  The composite ops chain NCCL calls
 // with our kernels, so they are replayed in order at GroupEnd.
+using Phases = std::vector<std::function<cemuResult_t()>>;
+struct GroupOp {
+  cemuComm* c;
+  Phases phases;
+};
 thread_local int g_group_depth = 0;
-thread_local std::vector<std::function<cemuResult_t()>> g_group_ops;
+thread_local std::vector<GroupOp> g_group_ops;
 
 }  // namespace
 
@@ -178,9 +186,11 @@ struct Call {
   int launches = 0;
   cudaStream_t s;
 
+  uint32_t i = 0;  // record slot of this call
+
   Call(cemuComm* comm, int coll, uint64_t model_bytes, cudaStream_t stream) : c(comm), s(stream) {
     const uint64_t id = c->calls++;
-    const uint32_t i = static_cast<uint32_t>(id % cemuComm::kSlots);
+    i = static_cast<uint32_t>(id % cemuComm::kSlots);
     auto& m = c->meta[i];
     m.call_id = id;
     m.coll = coll;
@@ -204,7 +214,7 @@ struct Call {
   cudaError_t finish(int coll) {
     c->launches += launches;
     if (!slot) return cudaSuccess;
-    const auto& m = c->meta[static_cast<uint32_t>((c->calls - 1) % cemuComm::kSlots)];
+    const auto& m = c->meta[i];
     DelayLaunch d;
     d.model = c->delay;
     d.coll = coll;
@@ -357,7 +367,10 @@ cemuResult_t check_op(int op, const char* what) {
   return cemuSuccess;
 }
 
-cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, int rank, int device) {
+// `preinit` (cemuCommInitAll): an inner NCCL comm made by ncclCommInitAll in
+// this process; the fused path needs one process per GPU (IPC) and is off.
+cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, int rank, int device,
+                       ncclComm_t preinit = nullptr) {
   if (!out) return fail(cemuInvalidArgument, "cemuCommInitRank: comm pointer is null");
   if (rank < 0 || static_cast<uint32_t>(rank) >= cfg.world_size) {
     return fail(cemuInvalidArgument, "rank " + std::to_string(rank) + " out of range [0," +
@@ -416,12 +429,16 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
                   "job places " + std::to_string(c->k) +
                       " real ranks on this box but libnccl.so.2 could not be loaded");
     }
-    ncclUniqueId nid;
-    static_assert(sizeof(nid) == sizeof(id), "unique id size");
-    std::memcpy(&nid, &id, sizeof nid);
-    NCCL_OK(n->CommInitRank(&c->inner, static_cast<int>(c->k), nid, static_cast<int>(c->li)));
+    if (preinit) {
+      c->inner = preinit;
+    } else {
+      ncclUniqueId nid;
+      static_assert(sizeof(nid) == sizeof(id), "unique id size");
+      std::memcpy(&nid, &id, sizeof nid);
+      NCCL_OK(n->CommInitRank(&c->inner, static_cast<int>(c->k), nid, static_cast<int>(c->li)));
+    }
     const char* fe = std::getenv("CEMU_FUSED");
-    c->fused = c->k <= static_cast<uint32_t>(kMaxReal) && !(fe && std::string(fe) == "0");
+    c->fused = !preinit && c->k <= static_cast<uint32_t>(kMaxReal) && !(fe && std::string(fe) == "0");
     if (const char* t = std::getenv("CEMU_FUSED_TIMEOUT_S")) c->fused_timeout_ns = std::atoll(t) * 1'000'000'000LL;
     if (c->fused) {
       CUDA_OK(cudaMalloc(&c->sig, 4096));
@@ -437,16 +454,16 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
 // collective bodies
 // ----------------------------------------------------------------------------
 cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, cemuComm* c,
-                          cudaStream_t s) {
+                          cudaStream_t s, Phases& ph) {
   const size_t es = dtype_size(dt);
   if (count == 0) return cemuSuccess;
-  Call call(c, kAllReduce, count * es, s);
+  auto call = std::make_shared<Call>(c, kAllReduce, count * es, s);
   const auto* nv = c->d_virt_keys;
   const uint32_t nk = static_cast<uint32_t>(c->virt.size());
-  if (c->mode == PayloadMode::kZero) {
+  if (c->mode == PayloadMode::kZero) ph.push_back([=]() -> cemuResult_t {
     // A10: zero replies; the real rank keeps chunk (rank+1) mod W
     // (test_transport.cpp:129-167), every other chunk is gathered zeros.
-    CUDA_OK(call.stamp_now());
+    CUDA_OK(call->stamp_now());
     const uint64_t total = count * es;
     const uint32_t keep = (c->rank + 1) % c->W;
     const uint64_t off = chunk_offset_bytes(c->W, total, static_cast<uint32_t>(es), keep);
@@ -458,12 +475,16 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
                               cudaMemcpyDeviceToDevice, s));
     }
     if (total - off - len) CUDA_OK(cudaMemsetAsync(r8 + off + len, 0, total - off - len, s));
-    CUDA_OK(call.finish(kAllReduce));
+    CUDA_OK(call->finish(kAllReduce));
     return cemuSuccess;
-  }
+  });
+  if (c->mode == PayloadMode::kZero) return cemuSuccess;
   if (c->k == 1) {
-    CUDA_OK(launch_synth_reduce(dt, send, recv, count, 0, nv, nk, call.take_stamp(), s, &call.launches));
-    CUDA_OK(call.finish(kAllReduce));
+    ph.push_back([=]() -> cemuResult_t {
+      CUDA_OK(launch_synth_reduce(dt, send, recv, count, 0, nv, nk, call->take_stamp(), s, &call->launches));
+      CUDA_OK(call->finish(kAllReduce));
+      return cemuSuccess;
+    });
     return cemuSuccess;
   }
   // k real GPUs, buffers from cemuMemAlloc: one fused kernel over peer memory
@@ -491,20 +512,20 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
     }
     a.keys = c->d_virt_keys;
     a.nkeys = static_cast<uint32_t>(c->virt.size());
-    if ((soff | roff) % 16 == 0) {
+    if ((soff | roff) % 16 == 0) ph.push_back([=]() mutable -> cemuResult_t {
       set_barrier(c, a);
       a.sig = op_sig(kAllReduce, dt, count);
       a.ndst = a.k;
-      a.stamp = call.take_stamp();
-      CUDA_OK(launch_fused_allreduce(dt, a, s, &call.launches));
-      CUDA_OK(call.finish(kAllReduce));
+      a.stamp = call->take_stamp();
+      CUDA_OK(launch_fused_allreduce(dt, a, s, &call->launches));
+      CUDA_OK(call->finish(kAllReduce));
       return cemuSuccess;
-    }
+    });
+    if ((soff | roff) % 16 == 0) return cemuSuccess;
   }
   // k real GPUs: NCCL reduce-scatter of the real part, synthesis on this
   // GPU's 1/k shard only, NCCL allgather.
   const Nccl* n = nccl();
-  CUDA_OK(call.stamp_now());
   cemuShardPlan plan;
   cemuPlanShards(count, c->k, c->li, &plan);
   const size_t shard = plan.shardCount;
@@ -512,36 +533,50 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   auto* r8 = static_cast<uint8_t*>(recv);
   const auto* s8 = static_cast<const uint8_t*>(send);
   const auto ndt = static_cast<ncclDataType_t>(dt);
-  if (shard) NCCL_OK(n->ReduceScatter(send, r8 + c->li * shard * es, shard, ndt, ncclSum, c->inner, s));
-  if (rem) NCCL_OK(n->AllReduce(s8 + c->k * shard * es, r8 + c->k * shard * es, rem, ndt, ncclSum, c->inner, s));
-  if (shard) {
-    CUDA_OK(launch_synth_reduce(dt, r8 + c->li * shard * es, r8 + c->li * shard * es, shard,
-                                c->li * shard, nv, nk, nullptr, s, &call.launches));
-  }
-  if (rem) {
-    CUDA_OK(launch_synth_reduce(dt, r8 + c->k * shard * es, r8 + c->k * shard * es, rem,
-                                c->k * shard, nv, nk, nullptr, s, &call.launches));
-  }
-  if (shard) NCCL_OK(n->AllGather(r8 + c->li * shard * es, r8, shard, ndt, c->inner, s));
-  CUDA_OK(call.finish(kAllReduce));
+  ph.push_back([=]() -> cemuResult_t {  // phase 0: the real part over NCCL
+    CUDA_OK(call->stamp_now());
+    if (shard) NCCL_OK(n->ReduceScatter(send, r8 + c->li * shard * es, shard, ndt, ncclSum, c->inner, s));
+    if (rem) NCCL_OK(n->AllReduce(s8 + c->k * shard * es, r8 + c->k * shard * es, rem, ndt, ncclSum, c->inner, s));
+    return cemuSuccess;
+  });
+  ph.push_back([=]() -> cemuResult_t {  // phase 1: the emulated part on the own shard
+    if (shard) {
+      CUDA_OK(launch_synth_reduce(dt, r8 + c->li * shard * es, r8 + c->li * shard * es, shard,
+                                  c->li * shard, nv, nk, nullptr, s, &call->launches));
+    }
+    if (rem) {
+      CUDA_OK(launch_synth_reduce(dt, r8 + c->k * shard * es, r8 + c->k * shard * es, rem,
+                                  c->k * shard, nv, nk, nullptr, s, &call->launches));
+    }
+    return cemuSuccess;
+  });
+  ph.push_back([=]() -> cemuResult_t {  // phase 2: everyone's shards
+    if (shard) NCCL_OK(n->AllGather(r8 + c->li * shard * es, r8, shard, ndt, c->inner, s));
+    CUDA_OK(call->finish(kAllReduce));
+    return cemuSuccess;
+  });
   return cemuSuccess;
 }
 
-cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuComm* c, cudaStream_t s) {
+cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuComm* c, cudaStream_t s,
+                          Phases& ph) {
   const size_t es = dtype_size(dt);
   if (sc == 0) return cemuSuccess;
-  Call call(c, kAllGather, sc * es, s);
+  auto call = std::make_shared<Call>(c, kAllGather, sc * es, s);
   auto* r8 = static_cast<uint8_t*>(recv);
   const uint32_t nvirt = static_cast<uint32_t>(c->virt.size());
   const bool own_in_place = send == r8 + static_cast<uint64_t>(c->rank) * sc * es;
   if (c->mode == PayloadMode::kZero) {
+    ph.push_back([=]() -> cemuResult_t {
     // test_transport.cpp:169-182: own block kept, every other block zeros
-    CUDA_OK(call.stamp_now());
+    CUDA_OK(call->stamp_now());
     const uint64_t blk = sc * es;
     if (c->rank) CUDA_OK(cudaMemsetAsync(r8, 0, c->rank * blk, s));
     if (c->rank + 1 < c->W) CUDA_OK(cudaMemsetAsync(r8 + (c->rank + 1) * blk, 0, (c->W - c->rank - 1) * blk, s));
     if (!own_in_place) CUDA_OK(cudaMemcpyAsync(r8 + c->rank * blk, send, blk, cudaMemcpyDeviceToDevice, s));
-    CUDA_OK(call.finish(kAllGather));
+    CUDA_OK(call->finish(kAllGather));
+    return cemuSuccess;
+    });
     return cemuSuccess;
   }
   if (c->k > 1 && c->fused && es <= 4) {
@@ -550,6 +585,7 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
     const cemuComm::Region* rr = find_region(c, recv, sc * es * c->W);
     const uint64_t roff = rr ? static_cast<uint64_t>(r8 - rr->base) : 1;
     if (rr && roff % 16 == 0 && (sc * es) % 16 == 0) {  // symmetric conditions only
+      ph.push_back([=]() -> cemuResult_t {
       const void* own_src = send;
       if (reinterpret_cast<uintptr_t>(send) % 16 != 0) {  // local: stage into the own block
         own_src = r8 + static_cast<uint64_t>(c->rank) * sc * es;
@@ -565,16 +601,22 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
       a.vranks = c->d_virt_ranks;
       a.vkeys = c->d_virt_keys;
       a.nvirt = nvirt;
-      a.stamp = call.take_stamp();
-      CUDA_OK(launch_fused_allgather(dt, a, s, &call.launches));
-      CUDA_OK(call.finish(kAllGather));
+      a.stamp = call->take_stamp();
+      CUDA_OK(launch_fused_allgather(dt, a, s, &call->launches));
+      CUDA_OK(call->finish(kAllGather));
+      return cemuSuccess;
+      });
       return cemuSuccess;
     }
   }
   const void* own = (c->k == 1 && !own_in_place) ? send : nullptr;
-  CUDA_OK(launch_synth_fill(dt, recv, sc, c->d_virt_ranks, c->d_virt_keys, nvirt, 0, 0, own, c->rank,
-                            call.take_stamp(), s, &call.launches));
-  if (c->k > 1) {
+  ph.push_back([=]() -> cemuResult_t {  // emulated blocks, written locally
+    CUDA_OK(launch_synth_fill(dt, recv, sc, c->d_virt_ranks, c->d_virt_keys, nvirt, 0, 0, own, c->rank,
+                              call->take_stamp(), s, &call->launches));
+    if (c->k == 1) CUDA_OK(call->finish(kAllGather));
+    return cemuSuccess;
+  });
+  if (c->k > 1) ph.push_back([=]() -> cemuResult_t {  // real blocks over NCCL
     const Nccl* n = nccl();
     const auto ndt = static_cast<ncclDataType_t>(dt);
     if (c->contiguous) {
@@ -587,30 +629,36 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
       }
       NCCL_OK(n->GroupEnd());
     }
-  }
-  CUDA_OK(call.finish(kAllGather));
+    CUDA_OK(call->finish(kAllGather));
+    return cemuSuccess;
+  });
   return cemuSuccess;
 }
 
 cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, cemuComm* c,
-                              cudaStream_t s) {
+                              cudaStream_t s, Phases& ph) {
   const size_t es = dtype_size(dt);
   if (rc == 0) return cemuSuccess;
-  Call call(c, kReduceScatter, rc * es * c->W, s);
+  auto call = std::make_shared<Call>(c, kReduceScatter, rc * es * c->W, s);
   const auto* s8 = static_cast<const uint8_t*>(send);
   const uint64_t mine = static_cast<uint64_t>(c->rank) * rc;
   if (c->mode == PayloadMode::kZero) {
-    // own contribution to chunk `rank` plus zero replies
-    CUDA_OK(launch_synth_fill(dt, recv, rc, nullptr, nullptr, 0, 0, 0, s8 + mine * es, 0,
-                              call.take_stamp(), s, &call.launches));
-    CUDA_OK(call.finish(kReduceScatter));
+    ph.push_back([=]() -> cemuResult_t {  // own contribution to chunk `rank` plus zero replies
+      CUDA_OK(launch_synth_fill(dt, recv, rc, nullptr, nullptr, 0, 0, 0, s8 + mine * es, 0,
+                                call->take_stamp(), s, &call->launches));
+      CUDA_OK(call->finish(kReduceScatter));
+      return cemuSuccess;
+    });
     return cemuSuccess;
   }
   const uint32_t nk = static_cast<uint32_t>(c->virt.size());
   if (c->k == 1) {
-    CUDA_OK(launch_synth_reduce(dt, s8 + mine * es, recv, rc, mine, c->d_virt_keys, nk,
-                                call.take_stamp(), s, &call.launches));
-    CUDA_OK(call.finish(kReduceScatter));
+    ph.push_back([=]() -> cemuResult_t {
+      CUDA_OK(launch_synth_reduce(dt, s8 + mine * es, recv, rc, mine, c->d_virt_keys, nk,
+                                  call->take_stamp(), s, &call->launches));
+      CUDA_OK(call->finish(kReduceScatter));
+      return cemuSuccess;
+    });
     return cemuSuccess;
   }
   // fused: pull this rank's chunk from every real GPU's (symmetric) send over
@@ -622,6 +670,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
   const cemuComm::Region* rs = c->fused ? find_region(c, send, rc * es * c->W) : nullptr;
   const uint64_t sbase = rs ? static_cast<uint64_t>(s8 - rs->base) : 1;
   if (rs && es <= 4 && sbase % 16 == 0 && (rc * es) % 16 == 0) {
+    ph.push_back([=]() -> cemuResult_t {
     const uint64_t soff = sbase + mine * es;
     void* out = recv;
     if (reinterpret_cast<uintptr_t>(recv) % 16 != 0) {
@@ -642,15 +691,18 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
     a.dst[0] = static_cast<uint4*>(out);
     a.keys = c->d_virt_keys;
     a.nkeys = nk;
-    a.stamp = call.take_stamp();
-    CUDA_OK(launch_fused_allreduce(dt, a, s, &call.launches));
+    a.stamp = call->take_stamp();
+    CUDA_OK(launch_fused_allreduce(dt, a, s, &call->launches));
     if (out != recv) CUDA_OK(cudaMemcpyAsync(recv, out, rc * es, cudaMemcpyDeviceToDevice, s));
-    CUDA_OK(call.finish(kReduceScatter));
+    CUDA_OK(call->finish(kReduceScatter));
+    return cemuSuccess;
+    });
     return cemuSuccess;
   }
   const Nccl* n = nccl();
   const auto ndt = static_cast<ncclDataType_t>(dt);
-  CUDA_OK(call.stamp_now());
+  ph.push_back([=]() -> cemuResult_t {  // phase 0: the real part over NCCL
+  CUDA_OK(call->stamp_now());
   if (c->contiguous) {
     NCCL_OK(n->ReduceScatter(s8 + static_cast<uint64_t>(c->real[0]) * rc * es, recv, rc, ndt, ncclSum,
                              c->inner, s));
@@ -662,50 +714,77 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
     }
     NCCL_OK(n->GroupEnd());
   }
-  CUDA_OK(launch_synth_reduce(dt, recv, recv, rc, mine, c->d_virt_keys, nk, nullptr, s, &call.launches));
-  CUDA_OK(call.finish(kReduceScatter));
+  return cemuSuccess;
+  });
+  ph.push_back([=]() -> cemuResult_t {  // phase 1: the emulated part
+    CUDA_OK(launch_synth_reduce(dt, recv, recv, rc, mine, c->d_virt_keys, nk, nullptr, s, &call->launches));
+    CUDA_OK(call->finish(kReduceScatter));
+    return cemuSuccess;
+  });
   return cemuSuccess;
 }
 
 cemuResult_t do_broadcast(const void* send, void* recv, size_t count, int dt, int root, cemuComm* c,
-                          cudaStream_t s) {
+                          cudaStream_t s, Phases& ph) {
   const size_t es = dtype_size(dt);
   if (root < 0 || static_cast<uint32_t>(root) >= c->W) {
     return fail(cemuInvalidArgument, "cemuBroadcast: root " + std::to_string(root) + " out of range [0," +
                                          std::to_string(c->W - 1) + "]");
   }
   if (count == 0) return cemuSuccess;
-  Call call(c, kBroadcast, count * es, s);
+  auto call = std::make_shared<Call>(c, kBroadcast, count * es, s);
   const uint32_t r = static_cast<uint32_t>(root);
+  ph.push_back([=]() -> cemuResult_t {
   if (c->cfg.is_real(r)) {
     if (c->k == 1) {
       if (send != recv) {
-        CUDA_OK(launch_synth_fill(dt, recv, count, nullptr, nullptr, 0, 0, 0, send, 0, call.take_stamp(), s,
-                                  &call.launches));
+        CUDA_OK(launch_synth_fill(dt, recv, count, nullptr, nullptr, 0, 0, 0, send, 0, call->take_stamp(), s,
+                                  &call->launches));
       }
     } else {
-      CUDA_OK(call.stamp_now());
+      CUDA_OK(call->stamp_now());
       const int lroot = static_cast<int>(std::find(c->real.begin(), c->real.end(), r) - c->real.begin());
       NCCL_OK(nccl()->Broadcast(send, recv, count, static_cast<ncclDataType_t>(dt), lroot, c->inner, s));
     }
   } else if (c->mode == PayloadMode::kZero) {
-    CUDA_OK(call.stamp_now());
+    CUDA_OK(call->stamp_now());
     CUDA_OK(cudaMemsetAsync(recv, 0, count * es, s));
   } else {
     CUDA_OK(launch_synth_fill(dt, recv, count, nullptr, nullptr, 1, 0, payload_key(c->seed, r), nullptr, 0,
-                              call.take_stamp(), s, &call.launches));
+                              call->take_stamp(), s, &call->launches));
   }
-  CUDA_OK(call.finish(kBroadcast));
+  CUDA_OK(call->finish(kBroadcast));
+  return cemuSuccess;
+  });
   return cemuSuccess;
 }
 
+// A collective is planned into phases (closures); nothing runs at planning
+// time.  Alone, its phases run back to back.  In a group, cemuGroupEnd runs
+// "rounds" -- the i-th call of every communicator -- phase by phase, each
+// phase inside one NCCL group, so a single thread driving several devices
+// (cemuCommInitAll) never blocks in a device's NCCL call while another
+// device's matching call has not been issued.  Every phase re-selects its
+// communicator's device.
 template <typename F>
-cemuResult_t run_or_defer(F&& f) {
+cemuResult_t run_or_defer(cemuComm* c, F&& plan) {
+  auto ops = std::make_shared<Phases>();
+  if (auto r = plan(*ops)) return r;
+  Phases wrapped;
+  for (auto& f : *ops) {
+    wrapped.push_back([c, f]() -> cemuResult_t {
+      if (cudaSetDevice(c->device) != cudaSuccess) return fail(cemuUnhandledCudaError, "cannot select device");
+      return f();
+    });
+  }
   if (g_group_depth > 0) {
-    g_group_ops.emplace_back(std::forward<F>(f));
+    g_group_ops.push_back(GroupOp{c, std::move(wrapped)});
     return cemuSuccess;
   }
-  return f();
+  for (auto& f : wrapped) {
+    if (auto r = f()) return r;
+  }
+  return cemuSuccess;
 }
 
 }  // namespace
@@ -778,6 +857,65 @@ cemuResult_t cemuCommInitRank(cemuComm_t* comm, int nranks, cemuUniqueId id, int
   }
 }
 
+cemuResult_t cemuCommInitAll(cemuComm_t* comms, int ndev, const int* devlist) {
+  const char* path = std::getenv("CEMU_CONFIG");
+  if (!comms || ndev < 1) return fail(cemuInvalidArgument, "cemuCommInitAll: bad argument");
+  if (!path || !*path) return fail(cemuInvalidUsage, "CEMU_CONFIG: must name the job config file");
+  try {
+    const JobConfig cfg = load_job_config(path);
+    if (cfg.real_ranks.size() != static_cast<size_t>(ndev)) {
+      return fail(cemuInvalidArgument, "cemuCommInitAll: " + std::to_string(ndev) + " devices but the job has " +
+                                           std::to_string(cfg.real_ranks.size()) + " real ranks");
+    }
+    std::vector<ncclComm_t> inner(ndev, nullptr);
+    if (ndev > 1) {
+      const Nccl* n = nccl();
+      if (!n || !n->CommInitAll) return fail(cemuSystemError, "cemuCommInitAll: libnccl.so.2 not loadable");
+      NCCL_OK(n->CommInitAll(inner.data(), ndev, devlist));
+    }
+    cemuUniqueId id{};
+    int i = 0;
+    for (uint32_t r : cfg.real_ranks) {  // device i serves the i-th real rank
+      const int dev = devlist ? devlist[i] : i;
+      if (auto e = init_comm(&comms[i], cfg, id, static_cast<int>(r), dev, inner[i])) return e;
+      ++i;
+    }
+    if (ndev > 1) {
+      // Establish NCCL's connections now, inside one group: a single thread
+      // later issuing each device's call in turn must never block in a
+      // lazy connection handshake waiting for a device it has not reached.
+      const Nccl* n = nccl();
+      std::vector<float*> scratch(ndev, nullptr);
+      for (int d = 0; d < ndev; ++d) {
+        CUDA_OK(cudaSetDevice(comms[d]->device));
+        CUDA_OK(cudaMalloc(&scratch[d], 64 * sizeof(float) * ndev));
+      }
+      for (int op = 0; op < 4; ++op) {
+        NCCL_OK(n->GroupStart());
+        for (int d = 0; d < ndev; ++d) {
+          cudaSetDevice(comms[d]->device);
+          float* b = scratch[d];
+          switch (op) {
+            case 0: NCCL_OK(n->AllReduce(b, b, 64, ncclFloat32, ncclSum, comms[d]->inner, nullptr)); break;
+            case 1: NCCL_OK(n->ReduceScatter(b, b, 64, ncclFloat32, ncclSum, comms[d]->inner, nullptr)); break;
+            case 2: NCCL_OK(n->AllGather(b, b, 64, ncclFloat32, comms[d]->inner, nullptr)); break;
+            default: NCCL_OK(n->Broadcast(b, b, 64, ncclFloat32, 0, comms[d]->inner, nullptr)); break;
+          }
+        }
+        NCCL_OK(n->GroupEnd());
+      }
+      for (int d = 0; d < ndev; ++d) {
+        CUDA_OK(cudaSetDevice(comms[d]->device));
+        CUDA_OK(cudaDeviceSynchronize());
+        cudaFree(scratch[d]);
+      }
+    }
+    return cemuSuccess;
+  } catch (const ConfigError& e) {
+    return fail(cemuInvalidArgument, e.what());
+  }
+}
+
 cemuResult_t cemuCommDestroy(cemuComm_t c) {
   if (!c) return cemuSuccess;
   cudaSetDevice(c->device);
@@ -840,7 +978,7 @@ cemuResult_t cemuAllReduce(const void* send, void* recv, size_t count, cemuDataT
   if (auto r = check_op(op, "cemuAllReduce")) return r;
   if (count && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllReduce: null buffer");
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  return run_or_defer([=] { return do_allreduce(send, recv, count, dt, c, s); });
+  return run_or_defer(c, [=](Phases& ph) { return do_allreduce(send, recv, count, dt, c, s, ph); });
 }
 
 cemuResult_t cemuAllGather(const void* send, void* recv, size_t sc, cemuDataType_t dt, cemuComm_t c,
@@ -848,7 +986,7 @@ cemuResult_t cemuAllGather(const void* send, void* recv, size_t sc, cemuDataType
   if (auto r = check_common(c, dt, "cemuAllGather")) return r;
   if (sc && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllGather: null buffer");
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  return run_or_defer([=] { return do_allgather(send, recv, sc, dt, c, s); });
+  return run_or_defer(c, [=](Phases& ph) { return do_allgather(send, recv, sc, dt, c, s, ph); });
 }
 
 cemuResult_t cemuReduceScatter(const void* send, void* recv, size_t rc, cemuDataType_t dt, cemuRedOp_t op,
@@ -857,7 +995,7 @@ cemuResult_t cemuReduceScatter(const void* send, void* recv, size_t rc, cemuData
   if (auto r = check_op(op, "cemuReduceScatter")) return r;
   if (rc && (!send || !recv)) return fail(cemuInvalidArgument, "cemuReduceScatter: null buffer");
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  return run_or_defer([=] { return do_reducescatter(send, recv, rc, dt, c, s); });
+  return run_or_defer(c, [=](Phases& ph) { return do_reducescatter(send, recv, rc, dt, c, s, ph); });
 }
 
 cemuResult_t cemuBroadcast(const void* send, void* recv, size_t count, cemuDataType_t dt, int root,
@@ -865,7 +1003,7 @@ cemuResult_t cemuBroadcast(const void* send, void* recv, size_t count, cemuDataT
   if (auto r = check_common(c, dt, "cemuBroadcast")) return r;
   if (count && !recv) return fail(cemuInvalidArgument, "cemuBroadcast: null recvbuff");
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  return run_or_defer([=] { return do_broadcast(send, recv, count, dt, root, c, s); });
+  return run_or_defer(c, [=](Phases& ph) { return do_broadcast(send, recv, count, dt, root, c, s, ph); });
 }
 
 cemuResult_t cemuGroupStart(void) {
@@ -876,10 +1014,29 @@ cemuResult_t cemuGroupStart(void) {
 cemuResult_t cemuGroupEnd(void) {
   if (g_group_depth == 0) return fail(cemuInvalidUsage, "cemuGroupEnd: not in a group");
   if (--g_group_depth > 0) return cemuSuccess;
-  std::vector<std::function<cemuResult_t()>> ops;
+  std::vector<GroupOp> ops;
   ops.swap(g_group_ops);
-  for (auto& f : ops) {
-    if (auto r = f()) return r;
+  // round r = the r-th call of every communicator, in issue order
+  std::vector<std::vector<GroupOp*>> rounds;
+  std::map<cemuComm*, size_t> calls_of;
+  for (auto& op : ops) {
+    const size_t r = calls_of[op.c]++;
+    if (rounds.size() <= r) rounds.resize(r + 1);
+    rounds[r].push_back(&op);
+  }
+  const Nccl* n = nccl();
+  for (auto& round : rounds) {
+    size_t nph = 0;
+    for (auto* op : round) nph = std::max(nph, op->phases.size());
+    for (size_t p = 0; p < nph; ++p) {
+      if (n) n->GroupStart();
+      cemuResult_t err = cemuSuccess;
+      for (auto* op : round) {
+        if (p < op->phases.size() && !err) err = op->phases[p]();
+      }
+      if (n && n->GroupEnd() != ncclSuccess && !err) err = fail(cemuInternalError, "ncclGroupEnd failed");
+      if (err) return err;
+    }
   }
   return cemuSuccess;
 }

@@ -34,3 +34,32 @@ def test_multi_gpu_collectives_match_oracle():
                        capture_output=True, text=True, timeout=420)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"MGPU OK {n}" in r.stdout
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_single_process_init_all(tmp_path):
+    """ncclCommInitAll shape: one process drives every GPU (grouped calls)."""
+    import numpy as np
+
+    import paper_2405_02969_b200 as pb
+    from gpu_util import assert_bit_equal, to_np
+    from oracle import port as P
+    n = min(torch.cuda.device_count(), 4)
+    cfg = tmp_path / "job.cfg"
+    cfg.write_text(f"world_size = {8 * n}\nreal_ranks = {','.join(map(str, range(n)))}\nbucket_bytes = 1\n")
+    comms = pb.Communicator.init_all(str(cfg), list(range(n)))
+    count = 100003
+    sends = [np.random.default_rng(i).integers(-64, 64, size=count).astype(np.float32) / 8 for i in range(n)]
+    xs = [torch.from_numpy(sends[i]).to(f"cuda:{i}") for i in range(n)]
+    pb.group_start()
+    for i, c in enumerate(comms):
+        with torch.cuda.device(i):
+            c.all_reduce(xs[i], xs[i])
+    pb.group_end()
+    for i in range(n):
+        torch.cuda.synchronize(i)
+    for i, c in enumerate(comms):
+        want = P.allreduce(7, P.PAYLOAD_HASH, 8 * n, list(range(n)), i, 1, sends, count)
+        assert_bit_equal(to_np(xs[i]), want, f"init_all device {i}")
+        c.close()
