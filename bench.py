@@ -279,12 +279,60 @@ def whatif_block(device, with_reference):
     return out
 
 
+def config3_block(torch, pb, comm_args):
+    """BASELINE config 3 shape on the GPUs this box has: world 128 = 16 nodes
+    x 8 GPUs, the real GPUs are ranks 0..N-1 of node 0, hierarchical ring,
+    bf16 gradients (256 MiB per GPU).  Throughput with the delay off, and the
+    injected-delay error with the hierarchical model on."""
+    rank, device, n, uid, dist = comm_args
+    out = {}
+    base = (f"world_size = 128\nreal_ranks = {','.join(str(r) for r in range(n))}\nbucket_bytes = 1\n"
+            "collective_algo = hierarchical\ntopology.gpus_per_node = 8\n")
+    delay = ("delay.kind = alpha_beta\nlink.alpha_us = 5\nlink.beta_us_per_byte = 0.00002\n"
+             "link.gamma_us_per_byte = 0.0000003\nlink.intra.alpha_us = 2\nlink.intra.beta_us_per_byte = 0.0000013\n")
+    count = (256 << 20) // 2
+    for tag, text in (("throughput", base), ("delay", base + delay)):
+        obj = [pb.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = pb.Communicator(text, rank, device, obj[0])
+        x, y = comm.alloc(count, torch.bfloat16), comm.alloc(count, torch.bfloat16)
+        for _ in range(3):
+            comm.all_reduce(x, y)
+        torch.cuda.synchronize(device)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        reps = 10 if tag == "throughput" else 3
+        for _ in range(reps):
+            comm.all_reduce(x, y)
+        e1.record()
+        torch.cuda.synchronize(device)
+        ms = e0.elapsed_time(e1) / reps
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if tag == "throughput":
+            out["ms_per_call"] = round(float(t.item()), 4)
+            out["algbw_GBps_per_gpu"] = round(count * 2 / (float(t.item()) * 1e-3) / 1e9, 1)
+        else:
+            rec = comm.call_record()
+            meas = (rec["t_end_ns"] - rec["t_start_ns"]) / 1e3
+            out["modelled_latency_us"] = rec["model_latency_us"]
+            out["measured_latency_us"] = round(meas, 3)
+            out["delay_err_us"] = round(abs(meas - rec["model_latency_us"]), 3)
+        comm.free(x)
+        comm.free(y)
+        comm.close()
+    out["note"] = ("world 128 (16 nodes x 8), real = ranks 0..N-1, hierarchical ring, bf16, 256 MiB per GPU, "
+                   "fused kernel over NVLink; 8 real GPUs is design-only (gpurun allows 1, 2, 4)")
+    return out
+
+
 def sweep_block(torch, pb, device):
     """Config 2 shape (single B200 emulating a 64-rank ring): algorithmic HBM
     GB/s per collective, fp32 and bf16, 4 KiB .. 1 GiB (powers of 4)."""
     comm = pb.Communicator("world_size = 64\nreal_ranks = 0\nbucket_bytes = 1\n", 0, device)
     res = {}
-    sizes = [4 << 10 << (2 * i) for i in range(10)]  # 4 KiB .. 1 GiB
+    sizes = [4 << 10 << i for i in range(19)]  # 4 KiB .. 1 GiB (SURVEY 8d: 2^12 .. 2^30)
     for dname, dt in (("fp32", torch.float32), ("bf16", torch.bfloat16)):
         es = torch.empty(0, dtype=dt).element_size()
         for coll in ("allreduce", "allgather", "reducescatter"):
@@ -326,7 +374,23 @@ def sweep_block(torch, pb, device):
                 del x
             res[f"{coll}_{dname}"] = pts
     comm.close()
+    ref_pts = {}
+    try:  # the reference CPU emulator at the same world (allreduce / allgather only)
+        import numpy as np
+        from oracle import ref
+        if ref.available():
+            for coll, name in ((0, "allreduce_fp32"), (1, "allgather_fp32")):
+                pts = []
+                for size in (4 << 10, 64 << 10, 1 << 20, 16 << 20):
+                    per_rank = size if coll == 0 else size // 64
+                    buf = np.zeros((per_rank * (64 if coll else 1)) // 4, dtype=np.int32)
+                    t = ref.emulated_collective(64, coll, buf, per_rank, 4, warmup=1, reps=3)
+                    pts.append([size, round(float(np.mean(t)), 1)])
+                ref_pts[name] = pts
+    except Exception as e:  # noqa: BLE001 - reported, never fatal
+        ref_pts["error"] = str(e)
     return {"world": 64, "columns": ["buffer_bytes", "us_per_call", "algorithmic_GB/s"],
+            "reference_cpu_emulator_us_per_call": ref_pts,
             "note": "allgather: in place, (n-1)*block written; reduce-scatter: own chunk read + written; "
                     "each point = graph-captured back-to-back calls (device time); small sizes are "
                     "kernel-launch bound and L2-resident", **res}
@@ -443,7 +507,12 @@ def run_ours(args, rank, world_size, local_rank):
            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(e2e_ms, 3),
            "path": "pinned host -> cudaMemcpyAsync -> cemuAllReduce (C-ABI) -> cudaMemcpyAsync -> pinned host"}
 
-    extra = {}
+    extra = {"effective": {"algbw_GBps": round(n * nbytes / (ms_per_step * 1e-3) / 1e9, 2),
+                           "busbw_GBps": round(n * nbytes / (ms_per_step * 1e-3) / 1e9
+                                               * 2 * (RANKS_PER_GPU * n - 1) / (RANKS_PER_GPU * n), 2),
+                           "note": "NCCL-style: algbw = S/t per GPU summed over GPUs, busbw = algbw*2(W-1)/W"}}
+    if n > 1:
+        extra["config3_shape"] = config3_block(torch, pb, comm_args=(rank, device, n, uid, dist))
     if rank == 0 and n == 1:
         extra["delay_error"] = delay_error_block(torch, pb, device)
         if not args.no_sweep:

@@ -843,7 +843,7 @@ struct Shape {
   int bps;
 };
 
-Shape pick_shape(int words_per_vec, uint32_t nkeys) {
+Shape pick_shape(int words_per_vec, uint32_t nkeys, uint64_t nvec) {
   static const int env_u = [] {
     const char* e = std::getenv("CEMU_SYNTH_U");
     return e ? std::atoi(e) : 0;
@@ -854,7 +854,12 @@ Shape pick_shape(int words_per_vec, uint32_t nkeys) {
   }();
   const int u_max = 8 / words_per_vec;  // <= 8 payload words per thread per tile
   Shape sh{nkeys * static_cast<uint32_t>(words_per_vec) <= 8 ? 2 : std::max(2, u_max), 0};
-  if ((env_u == 2 || env_u == 4 || env_u == 8) && env_u <= std::max(2, u_max)) sh.u = env_u;
+  // small buffers: spread the synthesis over the machine before amortising
+  // it over more words per thread (a 4 KiB call at 63 peers is otherwise
+  // one block doing all 63 x 8 hashes per thread serially)
+  const uint64_t fill = static_cast<uint64_t>(sm_count()) * 4 * kThreads;
+  while (sh.u > 1 && nvec < fill * static_cast<uint64_t>(sh.u)) sh.u /= 2;
+  if ((env_u == 1 || env_u == 2 || env_u == 4 || env_u == 8) && env_u <= std::max(2, u_max)) sh.u = env_u;
   if (env_bps > 0) sh.bps = env_bps;
   return sh;
 }
@@ -887,13 +892,14 @@ template <int K, int DT>
 cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_base,
                     const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
   constexpr int W = VT<K>::WPV;
-  const Shape sh = pick_shape(W, nkeys);
+  const Shape sh = pick_shape(W, nkeys, count / VT<K>::EPV);
   if constexpr (8 / W >= 8) {
     if (sh.u == 8) return run_vec_u<K, DT, 8>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
   }
   if constexpr (8 / W >= 4) {
     if (sh.u == 4) return run_vec_u<K, DT, 4>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
   }
+  if (sh.u == 1) return run_vec_u<K, DT, 1>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
   return run_vec_u<K, DT, 2>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
 }
 
