@@ -70,26 +70,6 @@ __device__ __forceinline__ float fold_f32(float x, int32_t s) {
   return __fadd_rn(x, __int2float_rn(s) * kDyadicScale);
 }
 
-__device__ __forceinline__ uint32_t fold_bf16x2(uint32_t packed, int32_t s_lo, int32_t s_hi) {
-  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&packed);
-  const float a = fold_f32(__bfloat162float(v.x), s_lo);
-  const float b = fold_f32(__bfloat162float(v.y), s_hi);
-  __nv_bfloat162 r;
-  r.x = __float2bfloat16_rn(a);
-  r.y = __float2bfloat16_rn(b);
-  return *reinterpret_cast<uint32_t*>(&r);
-}
-
-__device__ __forceinline__ uint32_t fold_f16x2(uint32_t packed, int32_t s_lo, int32_t s_hi) {
-  __half2 v = *reinterpret_cast<__half2*>(&packed);
-  const float a = fold_f32(__half2float(v.x), s_lo);
-  const float b = fold_f32(__half2float(v.y), s_hi);
-  __half2 r;
-  r.x = __float2half_rn(a);
-  r.y = __float2half_rn(b);
-  return *reinterpret_cast<uint32_t*>(&r);
-}
-
 // a + b per element of packed 16-bit pairs: fp32 add, one rounding to T
 __device__ __forceinline__ uint32_t fold_bf16x2_add(uint32_t a, uint32_t b) {
   __nv_bfloat162 va = *reinterpret_cast<__nv_bfloat162*>(&a);
@@ -233,38 +213,77 @@ __device__ __forceinline__ uint32_t mad_add(uint32_t a, uint32_t one, uint32_t a
 // Per-word byte sums from the two accumulators of one peer group (<= 257
 // peers): A = sum of whole words (mod 2^32), H = sum of odd bytes in 16-bit
 // lanes (S1, S3).  The even-byte lanes follow exactly:
-//   S0 + S2 * 2^16 = A - S1 * 2^8 - S3 * 2^24  (mod 2^32)
+//   S0 + S2 * 2^16 = A - S1 * 2^8 - S3 * 2^24 = A - H * 2^8  (mod 2^32)
 // so the mask of the even bytes is never computed per peer.
+__device__ __forceinline__ uint32_t even_lanes(uint32_t a, uint32_t h) { return a - (h << 8); }
+
 __device__ __forceinline__ void decode_byte_sums(uint32_t a, uint32_t h, uint32_t s[4]) {
-  const uint32_t s1 = h & 0xFFFFu, s3 = h >> 16;
-  const uint32_t even = a - (s1 << 8) - (s3 << 24);
+  const uint32_t even = even_lanes(a, h);
   s[0] = even & 0xFFFFu;
-  s[1] = s1;
+  s[1] = h & 0xFFFFu;
   s[2] = even >> 16;
-  s[3] = s3;
+  s[3] = h >> 16;
 }
 
-// Emulated-peer sums for the U vectors of one thread-tile.  Byte kinds:
-// s[4i + e] = sum over peers of (byte e of word i) - bias, in int32; word
-// kinds: acc[i] = wrapping sum of word i.  ctr[] holds the hoisted c1 values.
+// A 16-bit lane t dropped into the mantissa of 1.5 * 2^16 (one PRMT) is the
+// float 98304 + t * 2^-7 exactly (ulp 2^-7 in [2^16, 2^17)); subtracting
+// 98304 + n (n peers, each biased by 128) is exact too (same binade), so
+//   lane_delta = (t - 128 n) * 2^-7
+// costs PRMT + FADD instead of IADD + I2F + FMUL.
+constexpr uint32_t kLaneMagic = 0x47C00000u;  // 98304.0f
+// (the magic is materialised opaquely so ptxas keeps it in a register and
+// the selector as the PRMT immediate, not the other way round)
+__device__ __forceinline__ uint32_t lane_magic() {
+  uint32_t m;
+  asm("mov.b32 %0, %1;" : "=r"(m) : "n"(kLaneMagic));
+  return m;
+}
+__device__ __forceinline__ float lane_float(uint32_t w, uint32_t sel) {
+  return __uint_as_float(__byte_perm(w, lane_magic(), sel));
+}
+
+// sm_100 packed fp32 pair add (FADD2): two lanes per instruction
+__device__ __forceinline__ uint64_t pack_f32x2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 add_f32x2(float a0, float a1, float b0, float b1) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pack_f32x2(a0, a1)), "l"(pack_f32x2(b0, b1)));
+  float2 f;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(r));
+  return f;
+}
+
+// Emulated-peer contribution of the U vectors of one thread-tile, as lanes
+// r[] ready for fold_vec:
+//   float kinds  r[4i + e] = float bits of (sum over peers of byte e of
+//                word i, each minus 128) * 2^-7   (exact)
+//   u8           r[4i]     = the four byte sums of word i, mod 256, packed
+//   word kinds   r[i]      = wrapping sum of word i
+// ctr[] holds the hoisted c1 values.
 template <int K, int U, bool kMulti>
 __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skeys, uint32_t nkeys,
-                                          uint32_t one, int32_t* s, uint32_t* acc) {
+                                          uint32_t one, uint32_t* r) {
   using T = VT<K>;
   constexpr int NW = U * T::WPV;
   if constexpr (T::kWords) {
 #pragma unroll
-    for (int i = 0; i < NW; ++i) acc[i] = 0;
+    for (int i = 0; i < NW; ++i) r[i] = 0;
 #pragma unroll 2
     for (uint32_t q = 0; q < nkeys; ++q) {
       const uint2 key = skeys[q];
 #pragma unroll
-      for (int i = 0; i < NW; ++i) acc[i] = mad_add(payload_mix(key.x, key.y, ctr[i]), one, acc[i]);
+      for (int i = 0; i < NW; ++i) r[i] = mad_add(payload_mix(key.x, key.y, ctr[i]), one, r[i]);
     }
   } else {
     const uint32_t groups = kMulti ? (nkeys + 255) / 256 : 1;
+    int32_t s[kMulti ? NW * 4 : 1];
+    if constexpr (kMulti) {
 #pragma unroll
-    for (int i = 0; i < NW * 4; ++i) s[i] = 0;
+      for (int i = 0; i < NW * 4; ++i) s[i] = 0;
+    }
     for (uint32_t g = 0; g < groups; ++g) {
       const uint32_t q0 = g * 256;
       const uint32_t q1 = kMulti ? min(nkeys, q0 + 256) : nkeys;
@@ -281,56 +300,103 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
           h[i] = mad_add(__byte_perm(w, 0u, 0x4341), one, h[i]);
         }
       }
-      // float kinds carry the -128 offset of the dyadic value; bytes wrap
-      const int32_t bias = K == kU8 ? 0 : 128 * static_cast<int32_t>(q1 - q0);
+      if constexpr (!kMulti) {
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          const uint32_t even = even_lanes(a[i], h[i]);
+          if constexpr (K == kU8) {  // bytes wrap: low byte of each lane
+            r[4 * i] = __byte_perm(even, h[i], 0x6240);
+          } else {
+            const float c = -(98304.0f + static_cast<float>(nkeys));
+            const float2 d01 = add_f32x2(lane_float(even, 0x7610), lane_float(h[i], 0x7610), c, c);
+            const float2 d23 = add_f32x2(lane_float(even, 0x7632), lane_float(h[i], 0x7632), c, c);
+            r[4 * i + 0] = __float_as_uint(d01.x);
+            r[4 * i + 1] = __float_as_uint(d01.y);
+            r[4 * i + 2] = __float_as_uint(d23.x);
+            r[4 * i + 3] = __float_as_uint(d23.y);
+          }
+        }
+      } else {
+        // float kinds carry the -128 offset of the dyadic value; bytes wrap
+        const int32_t bias = K == kU8 ? 0 : 128 * static_cast<int32_t>(q1 - q0);
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          uint32_t t[4];
+          decode_byte_sums(a[i], h[i], t);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s[i * 4 + e] += static_cast<int32_t>(t[e]) - bias;
+        }
+      }
+    }
+    if constexpr (kMulti) {
 #pragma unroll
       for (int i = 0; i < NW; ++i) {
-        uint32_t t[4];
-        decode_byte_sums(a[i], h[i], t);
+        const int32_t* t = s + 4 * i;
+        if constexpr (K == kU8) {
+          r[4 * i] = (static_cast<uint32_t>(t[0]) & 0xFFu) | ((static_cast<uint32_t>(t[1]) & 0xFFu) << 8) |
+                     ((static_cast<uint32_t>(t[2]) & 0xFFu) << 16) | (static_cast<uint32_t>(t[3]) << 24);
+        } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) s[i * 4 + e] += static_cast<int32_t>(t[e]) - bias;
+          for (int e = 0; e < 4; ++e) r[4 * i + e] = __float_as_uint(__int2float_rn(t[e]) * kDyadicScale);
+        }
       }
     }
   }
 }
 
-// One rounding per element: x (+) S * 2^-7 (floats), x + sum (integers).
-// `s`/`acc` point at the sums of this vector's words.
+// x + d in fp32 (one rounding) with x a 16-bit half of a packed pair: the
+// sm_100 mixed-precision add reads the half in place (FHADD.BF16 .H0/.H1),
+// so there is no unpack.
+__device__ __forceinline__ uint32_t bf16x2_fold(uint32_t p, uint32_t dlo, uint32_t dhi) {
+  float lo, hi;
+  asm("{ .reg .b16 l, h; mov.b32 {l, h}, %2;\n"
+      "  add.rn.f32.bf16 %0, l, %3;\n  add.rn.f32.bf16 %1, h, %4; }"
+      : "=f"(lo), "=f"(hi) : "r"(p), "f"(__uint_as_float(dlo)), "f"(__uint_as_float(dhi)));
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ uint32_t f16x2_fold(uint32_t p, uint32_t dlo, uint32_t dhi) {
+  float lo, hi;
+  asm("{ .reg .b16 l, h; mov.b32 {l, h}, %2;\n"
+      "  add.rn.f32.f16 %0, l, %3;\n  add.rn.f32.f16 %1, h, %4; }"
+      : "=f"(lo), "=f"(hi) : "r"(p), "f"(__uint_as_float(dlo)), "f"(__uint_as_float(dhi)));
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// One rounding per element: x (+) delta in fp32, then to the element type
+// (floats); x + sum (integers).  `r` points at this vector's lanes.
 template <int K>
-__device__ __forceinline__ uint4 fold_vec(const uint4& x, const int32_t* s, const uint32_t* acc) {
+__device__ __forceinline__ uint4 fold_vec(const uint4& x, const uint32_t* r) {
   uint4 y;
   if constexpr (VT<K>::kWords) {
-    y.x = x.x + acc[0];
-    y.y = x.y + acc[1];
-    y.z = x.z + acc[2];
-    y.w = x.w + acc[3];
+    y.x = x.x + r[0];
+    y.y = x.y + r[1];
+    y.z = x.z + r[2];
+    y.w = x.w + r[3];
   } else if constexpr (K == kF32) {
-    y.x = u32_of(fold_f32(f32_of(x.x), s[0]));
-    y.y = u32_of(fold_f32(f32_of(x.y), s[1]));
-    y.z = u32_of(fold_f32(f32_of(x.z), s[2]));
-    y.w = u32_of(fold_f32(f32_of(x.w), s[3]));
+    const float2 a = add_f32x2(f32_of(x.x), f32_of(x.y), f32_of(r[0]), f32_of(r[1]));
+    const float2 b = add_f32x2(f32_of(x.z), f32_of(x.w), f32_of(r[2]), f32_of(r[3]));
+    y.x = u32_of(a.x);
+    y.y = u32_of(a.y);
+    y.z = u32_of(b.x);
+    y.w = u32_of(b.y);
   } else if constexpr (K == kBF16) {  // words 0 (elements 0..3) and 1 (4..7)
-    y.x = fold_bf16x2(x.x, s[0], s[1]);
-    y.y = fold_bf16x2(x.y, s[2], s[3]);
-    y.z = fold_bf16x2(x.z, s[4], s[5]);
-    y.w = fold_bf16x2(x.w, s[6], s[7]);
+    y.x = bf16x2_fold(x.x, r[0], r[1]);
+    y.y = bf16x2_fold(x.y, r[2], r[3]);
+    y.z = bf16x2_fold(x.z, r[4], r[5]);
+    y.w = bf16x2_fold(x.w, r[6], r[7]);
   } else if constexpr (K == kF16) {
-    y.x = fold_f16x2(x.x, s[0], s[1]);
-    y.y = fold_f16x2(x.y, s[2], s[3]);
-    y.z = fold_f16x2(x.z, s[4], s[5]);
-    y.w = fold_f16x2(x.w, s[6], s[7]);
-  } else {  // kU8: byte e of word i is S[4i + e] mod 256
-    uint32_t p[4];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const int32_t* t = s + w * 4;
-      p[w] = (static_cast<uint32_t>(t[0]) & 0xFFu) | ((static_cast<uint32_t>(t[1]) & 0xFFu) << 8) |
-             ((static_cast<uint32_t>(t[2]) & 0xFFu) << 16) | (static_cast<uint32_t>(t[3]) << 24);
-    }
-    y.x = add_bytes(x.x, p[0]);
-    y.y = add_bytes(x.y, p[1]);
-    y.z = add_bytes(x.z, p[2]);
-    y.w = add_bytes(x.w, p[3]);
+    y.x = f16x2_fold(x.x, r[0], r[1]);
+    y.y = f16x2_fold(x.y, r[2], r[3]);
+    y.z = f16x2_fold(x.z, r[4], r[5]);
+    y.w = f16x2_fold(x.w, r[6], r[7]);
+  } else {  // kU8: packed byte sums of word i at r[4i]
+    y.x = add_bytes(x.x, r[0]);
+    y.y = add_bytes(x.y, r[4]);
+    y.z = add_bytes(x.z, r[8]);
+    y.w = add_bytes(x.w, r[12]);
   }
   return y;
 }
@@ -365,13 +431,12 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
       for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(word_base + v * W + w);
     }
     // 2. the emulated peers' sums (registers only), 3. fold + stream out
-    int32_t s[T::kWords ? 1 : NW * 4];
-    uint32_t acc[T::kWords ? NW : 1];
-    peer_sums<K, U, kMulti>(ctr, skeys, nkeys, one, s, acc);
+    uint32_t r[T::kWords ? NW : NW * 4];
+    peer_sums<K, U, kMulti>(ctr, skeys, nkeys, one, r);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
-      if (v < nvec) st_stream(dst + v, fold_vec<K>(x[u], s + u * W * 4, acc + (T::kWords ? u * 4 : 0)));
+      if (v < nvec) st_stream(dst + v, fold_vec<K>(x[u], r + u * W * (T::kWords ? 1 : 4)));
     }
   }
   // ragged tail (< one vector): the last block's first threads
@@ -541,9 +606,8 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
 #pragma unroll
       for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(a.word_base + v * W + w);
     }
-    int32_t s[T::kWords ? 1 : NW * 4];
-    uint32_t acc[T::kWords ? NW : 1];
-    peer_sums<K, U, kMulti>(ctr, skeys, a.nkeys, 1u, s, acc);
+    uint32_t r[T::kWords ? NW : NW * 4];
+    peer_sums<K, U, kMulti>(ctr, skeys, a.nkeys, 1u, r);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
@@ -553,7 +617,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
       for (int g = 1; g < KMAX; ++g) {
         if (g < a.k) real = add_real<K>(real, x[g][u]);
       }
-      const uint4 y = fold_vec<K>(real, s + u * W * 4, acc + (T::kWords ? u * 4 : 0));
+      const uint4 y = fold_vec<K>(real, r + u * W * (T::kWords ? 1 : 4));
 #pragma unroll
       for (int g = 0; g < KMAX; ++g) {
         if (g < a.ndst) st_stream(a.dst[g] + v, y);
@@ -852,14 +916,17 @@ Shape pick_shape(int words_per_vec, uint32_t nkeys, uint64_t nvec) {
     const char* e = std::getenv("CEMU_SYNTH_BPS");
     return e ? std::atoi(e) : 0;
   }();
-  const int u_max = 8 / words_per_vec;  // <= 8 payload words per thread per tile
+  // <= 8 payload words and <= 4 vectors per thread per tile (8 resident
+  // 16-byte loads push ptxas into a register-starved serial schedule of
+  // the peer loop: measured 8% slower at 63 peers)
+  const int u_max = std::min(4, 8 / words_per_vec);
   Shape sh{nkeys * static_cast<uint32_t>(words_per_vec) <= 8 ? 2 : std::max(2, u_max), 0};
   // small buffers: spread the synthesis over the machine before amortising
   // it over more words per thread (a 4 KiB call at 63 peers is otherwise
   // one block doing all 63 x 8 hashes per thread serially)
   const uint64_t fill = static_cast<uint64_t>(sm_count()) * 4 * kThreads;
   while (sh.u > 1 && nvec < fill * static_cast<uint64_t>(sh.u)) sh.u /= 2;
-  if ((env_u == 1 || env_u == 2 || env_u == 4 || env_u == 8) && env_u <= std::max(2, u_max)) sh.u = env_u;
+  if ((env_u == 1 || env_u == 2 || env_u == 4 || env_u == 8) && env_u <= std::max(2, 8 / words_per_vec)) sh.u = env_u;
   if (env_bps > 0) sh.bps = env_bps;
   return sh;
 }

@@ -67,6 +67,51 @@ def test_allreduce_many_peers_grouped_lanes(comms, W):
         assert_bit_equal(_allreduce(comm, h, inplace=False), want, f"W={W} dt={dt}")
 
 
+def _special_values(dt: int, count: int, seed: int, W: int) -> torch.Tensor:
+    """IEEE edge cases scattered over a random buffer: signed zeros, infs,
+    NaN, subnormals at both ends, the largest finite values (the fold may
+    overflow to inf) and halfway cases for the final rounding."""
+    h = host_input(dt, count, seed=seed)
+    fi = torch.finfo(TORCH[dt])
+    sub = fi.smallest_normal * fi.eps  # smallest subnormal
+    specials = [0.0, -0.0, float("inf"), float("-inf"), float("nan"), sub, -sub, fi.smallest_normal - sub,
+                -(fi.smallest_normal - sub), fi.smallest_normal, fi.max, -fi.max, fi.max * 0.999, 1.0 + fi.eps / 2,
+                0.5 * fi.eps, 2.0 ** -7, -(2.0 ** -8), 3.0 * 2 ** -9]
+    g = torch.Generator().manual_seed(seed)
+    pos = torch.randperm(count, generator=g)[: 40 * len(specials)]
+    vals = torch.tensor(specials * 40, dtype=torch.float64).to(TORCH[dt])
+    h[pos] = vals
+    # where the emulated sum is exactly 0 the fold must return x itself:
+    # put subnormals there (a flush-to-zero add would show up)
+    zeros = torch.zeros(count, dtype=TORCH[dt])
+    d = P.allreduce(dt, P.PAYLOAD_HASH, W, [0], 0, 1, [to_np(zeros)], count)
+    s0 = np.nonzero(np.ascontiguousarray(d).view(np.uint8).reshape(count, -1).max(axis=1) == 0)[0]
+    tiny = torch.tensor([sub, -sub, fi.smallest_normal - sub, 3 * sub, -0.0], dtype=torch.float64).to(TORCH[dt])
+    h[torch.from_numpy(s0)] = tiny[torch.arange(len(s0)) % len(tiny)]
+    return h
+
+
+@pytest.mark.parametrize("W", [2, 8, 300])
+@pytest.mark.parametrize("dt", [7, 9, 6])
+def test_float_fold_ieee_edge_cases(comms, W, dt):
+    """The fold is one fp32 rounding of x + S * 2^-7 then one rounding to the
+    element type; the vector kernel computes S * 2^-7 by a magic-number
+    conversion and the add with sm_100 packed / mixed-precision adds, so the
+    edge cases are checked bit for bit (NaN positions by mask: NaN payload
+    bits are not part of the contract)."""
+    comm = comms(W)
+    count = 16384 + 8
+    h = _special_values(dt, count, seed=W * 10 + dt, W=W)
+    want = P.allreduce(dt, P.PAYLOAD_HASH, W, [0], 0, 1, [to_np(h)], count)
+    got = _allreduce(comm, h, inplace=False)
+    tdt = TORCH[dt]
+    gt = torch.from_numpy(got.view(np.int16) if dt in (6, 9) else got).view(tdt).double().numpy()
+    wt = torch.from_numpy(want.view(np.int16) if dt in (6, 9) else want).view(tdt).double().numpy()
+    assert np.array_equal(np.isnan(gt), np.isnan(wt)), "NaN positions differ"
+    keep = ~np.isnan(wt)
+    assert_bit_equal(got[keep], want[keep], f"edge cases W={W} dt={dt}")
+
+
 def test_real_rank_not_zero_and_other_seed(comms):
     comm = comms(16, seed=0xBEEF, real=(5,), rank=5)
     for dt in (7, 2):
