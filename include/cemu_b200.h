@@ -111,6 +111,22 @@ cemuResult_t cemuBroadcast(const void* sendbuff, void* recvbuff, size_t count,
 cemuResult_t cemuGroupStart(void);
 cemuResult_t cemuGroupEnd(void);
 
+/* Host-buffer forms of allreduce / allgather: `sendbuff`/`recvbuff` are HOST
+ * memory, as WorkerSession's spans are (collective.hpp:66-75:
+ * allreduce_async(span<uint8_t>, elem_size), allgather_async(span, ...)).
+ * Stream-ordered like cudaMemcpyAsync: recvbuff is complete when `stream`
+ * reaches the end of the call (cudaStreamSynchronize = WorkerSession::wait).
+ * With one real GPU the buffer is pipelined through the device in chunks
+ * (H2D, synthesis, D2H overlap; $CEMU_HOST_CHUNK_MIB, default 32); page-
+ * locked host memory is needed for the copies to overlap.  Not groupable.
+ * Allgather: recvbuff holds world_size blocks of sendcount elements; in
+ * place when sendbuff == recvbuff + rank * sendcount. */
+cemuResult_t cemuAllReduceHost(const void* sendbuff, void* recvbuff, size_t count,
+                               cemuDataType_t datatype, cemuRedOp_t op, cemuComm_t comm,
+                               cemuStream_t stream);
+cemuResult_t cemuAllGatherHost(const void* sendbuff, void* recvbuff, size_t sendcount,
+                               cemuDataType_t datatype, cemuComm_t comm, cemuStream_t stream);
+
 /* Symmetric device memory (ncclMemAlloc / window-registration analogue).
  * Collective over the job's real ranks on this box: each allocates `bytes`
  * and maps every peer's allocation (CUDA IPC).  An allreduce whose send and

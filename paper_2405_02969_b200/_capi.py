@@ -74,6 +74,8 @@ def _load():
         "cemuGetLastError": (cp, [vp]),
         "cemuAllReduce": (i32, [vp, vp, sz, i32, i32, vp, vp]),
         "cemuAllGather": (i32, [vp, vp, sz, i32, vp, vp]),
+        "cemuAllReduceHost": (i32, [vp, vp, sz, i32, i32, vp, vp]),
+        "cemuAllGatherHost": (i32, [vp, vp, sz, i32, vp, vp]),
         "cemuReduceScatter": (i32, [vp, vp, sz, i32, i32, vp, vp]),
         "cemuBroadcast": (i32, [vp, vp, sz, i32, i32, vp, vp]),
         "cemuMemAlloc": (i32, [vp, sz, C.POINTER(vp)]),

@@ -187,6 +187,31 @@ class Communicator:
                                 self._h, _stream_ptr(stream)), self._h)
         return recv
 
+    # -- host buffers (WorkerSession's span shape, collective.hpp:66-75) ------
+    def all_reduce_host(self, send: torch.Tensor, recv: torch.Tensor | None = None, stream=None):
+        """Allreduce of a HOST tensor (pin it for overlapped copies).  Stream-
+        ordered: synchronize `stream` before reading `recv`."""
+        recv = send if recv is None else recv
+        self._check_host(send, recv, send.numel())
+        check(lib.cemuAllReduceHost(_ptr(send), _ptr(recv), send.numel(), dtype_code(send.dtype), 0,
+                                    self._h, _stream_ptr(stream)), self._h)
+        return recv
+
+    def all_gather_host(self, send: torch.Tensor, recv: torch.Tensor, stream=None):
+        self._check_host(send, recv, send.numel() * self.world_size)
+        check(lib.cemuAllGatherHost(_ptr(send), _ptr(recv), send.numel(), dtype_code(send.dtype),
+                                    self._h, _stream_ptr(stream)), self._h)
+        return recv
+
+    def _check_host(self, send, recv, recv_numel):
+        if send.dtype != recv.dtype:
+            raise CemuError(_capi.INVALID_ARGUMENT, "send/recv dtypes differ")
+        if recv.numel() != recv_numel:
+            raise CemuError(_capi.INVALID_ARGUMENT, f"recv has {recv.numel()} elements, expected {recv_numel}")
+        for t in (send, recv):
+            if t.is_cuda or not t.is_contiguous():
+                raise CemuError(_capi.INVALID_ARGUMENT, "host collectives take contiguous CPU tensors")
+
     def reduce_scatter(self, send: torch.Tensor, recv: torch.Tensor, stream=None):
         if send.numel() != recv.numel() * self.world_size:
             raise CemuError(_capi.INVALID_ARGUMENT,

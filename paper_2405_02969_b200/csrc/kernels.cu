@@ -699,7 +699,8 @@ __global__ void __launch_bounds__(kThreads) synth_fill_vec(uint4* dst, uint64_t 
                                                            const uint32_t* __restrict__ keys,
                                                            uint32_t nblocks, uint32_t index0,
                                                            uint32_t key0, const uint4* own_src,
-                                                           uint32_t own_index, int64_t* stamp) {
+                                                           uint32_t own_index, int64_t* stamp,
+                                                           uint64_t word_base) {
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
   const uint32_t b = blockIdx.y;
   const bool copy = b == nblocks;
@@ -712,7 +713,7 @@ __global__ void __launch_bounds__(kThreads) synth_fill_vec(uint4* dst, uint64_t 
     if (copy) {
       st_stream(out + v, ld_stream(own_src + v));
     } else {
-      st_stream(out + v, synth_vector<K>(key, v * VT<K>::WPV));
+      st_stream(out + v, synth_vector<K>(key, word_base + v * VT<K>::WPV));
     }
   }
 }
@@ -723,7 +724,8 @@ __global__ void __launch_bounds__(kThreads) synth_fill_scalar(void* dst, uint64_
                                                               const uint32_t* keys, uint32_t nblocks,
                                                               uint32_t index0, uint32_t key0,
                                                               const void* own_src, uint32_t own_index,
-                                                              int64_t* stamp, int elem_size) {
+                                                              int64_t* stamp, int elem_size,
+                                                              uint64_t elem_base) {
   if (stamp && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
   const uint32_t b = blockIdx.y;
   const bool copy = b == nblocks;
@@ -741,7 +743,7 @@ __global__ void __launch_bounds__(kThreads) synth_fill_scalar(void* dst, uint64_
   }
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < block_elems;
        i += stride) {
-    elem_fill<DT>(out, i, i, key);
+    elem_fill<DT>(out, i, elem_base + i, key);
   }
 }
 
@@ -1026,7 +1028,7 @@ namespace {
 template <int K>
 cudaError_t fill_vec(void* dst, uint64_t block_elems, const uint32_t* idx, const uint32_t* keys,
                      uint32_t nblocks, uint32_t index0, uint32_t key0, const void* own,
-                     uint32_t own_index, int64_t* stamp, cudaStream_t s) {
+                     uint32_t own_index, int64_t* stamp, cudaStream_t s, uint64_t elem_base) {
   const uint64_t nvec = block_elems / VT<K>::EPV;
   const uint32_t ny = nblocks + (own ? 1 : 0);
   const uint64_t want = (nvec + kThreads - 1) / kThreads;
@@ -1034,20 +1036,21 @@ cudaError_t fill_vec(void* dst, uint64_t block_elems, const uint32_t* idx, const
   const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(1, std::min(want, cap)));
   synth_fill_vec<K><<<dim3(gx, ny), kThreads, 0, s>>>(static_cast<uint4*>(dst), nvec, idx, keys, nblocks,
                                                       index0, key0, static_cast<const uint4*>(own),
-                                                      own_index, stamp);
+                                                      own_index, stamp,
+                                                      VT<K>::kWords ? elem_base : elem_base / 4);
   return cudaGetLastError();
 }
 
 template <int DT>
 cudaError_t fill_scalar(void* dst, uint64_t block_elems, const uint32_t* idx, const uint32_t* keys,
                         uint32_t nblocks, uint32_t index0, uint32_t key0, const void* own,
-                        uint32_t own_index, int64_t* stamp, cudaStream_t s, int es) {
+                        uint32_t own_index, int64_t* stamp, cudaStream_t s, int es, uint64_t elem_base) {
   const uint32_t ny = nblocks + (own ? 1 : 0);
   const uint64_t want = (block_elems * es + kThreads - 1) / kThreads;
   const uint64_t cap = std::max<uint64_t>(1, static_cast<uint64_t>(sm_count()) * 8 / std::max<uint32_t>(ny, 1));
   const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(1, std::min(want, cap)));
   synth_fill_scalar<DT><<<dim3(gx, ny), kThreads, 0, s>>>(dst, block_elems, idx, keys, nblocks, index0,
-                                                          key0, own, own_index, stamp, es);
+                                                          key0, own, own_index, stamp, es, elem_base);
   return cudaGetLastError();
 }
 
@@ -1064,32 +1067,34 @@ int dsize(int dt) {
 cudaError_t launch_synth_fill(int dtype, void* dst, uint64_t block_elems, const uint32_t* d_index,
                               const uint32_t* d_keys, uint32_t nblocks, uint32_t index0,
                               uint32_t key0, const void* own_src, uint32_t own_index,
-                              int64_t* stamp, cudaStream_t s, int* launches) {
+                              int64_t* stamp, cudaStream_t s, int* launches, uint64_t elem_base) {
   if (block_elems == 0 || (nblocks == 0 && !own_src)) return cudaSuccess;
   if (nblocks + 1 > 65535) return cudaErrorInvalidValue;
   ++*launches;
   const int es = dsize(dtype);
-  const bool al = aligned16(dst) && (!own_src || aligned16(own_src)) && (block_elems * es) % 16 == 0;
+  const bool word_kind = dtype == cemuInt32 || dtype == cemuUint32;
+  const bool al = aligned16(dst) && (!own_src || aligned16(own_src)) && (block_elems * es) % 16 == 0 &&
+                  (word_kind || elem_base % 4 == 0);
   switch (dtype) {
     case cemuFloat32:
-      if (al) return fill_vec<kF32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
-      return fill_scalar<cemuFloat32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+      if (al) return fill_vec<kF32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, elem_base);
+      return fill_scalar<cemuFloat32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es, elem_base);
     case cemuBfloat16:
-      if (al) return fill_vec<kBF16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
-      return fill_scalar<cemuBfloat16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+      if (al) return fill_vec<kBF16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, elem_base);
+      return fill_scalar<cemuBfloat16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es, elem_base);
     case cemuFloat16:
-      if (al) return fill_vec<kF16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
-      return fill_scalar<cemuFloat16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+      if (al) return fill_vec<kF16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, elem_base);
+      return fill_scalar<cemuFloat16>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es, elem_base);
     case cemuInt8: case cemuUint8:
-      if (al) return fill_vec<kU8>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
-      return fill_scalar<cemuUint8>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+      if (al) return fill_vec<kU8>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, elem_base);
+      return fill_scalar<cemuUint8>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es, elem_base);
     case cemuInt32: case cemuUint32:
-      if (al) return fill_vec<kI32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s);
-      return fill_scalar<cemuUint32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+      if (al) return fill_vec<kI32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, elem_base);
+      return fill_scalar<cemuUint32>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es, elem_base);
     case cemuInt64: case cemuUint64:
-      return fill_scalar<cemuUint64>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+      return fill_scalar<cemuUint64>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es, elem_base);
     case cemuFloat64:
-      return fill_scalar<cemuFloat64>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es);
+      return fill_scalar<cemuFloat64>(dst, block_elems, d_index, d_keys, nblocks, index0, key0, own_src, own_index, stamp, s, es, elem_base);
     default: --*launches; return cudaErrorInvalidValue;
   }
 }

@@ -39,12 +39,14 @@ cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t 
 // (elements [dst_index[b]*block_elems, +block_elems) of dst) is filled with
 // the payload of key[b]; if own_src != nullptr, block own_index is copied
 // from own_src.  d_index/d_keys may be null when nblocks == 1, then
-// index0/key0 are used.
+// index0/key0 are used.  Payload element indices start at elem_base (the
+// block holds elements [elem_base, elem_base + block_elems) of the rank's
+// payload; one block per launch then).
 cudaError_t launch_synth_fill(int dtype, void* dst, uint64_t block_elems,
                               const uint32_t* d_index, const uint32_t* d_keys, uint32_t nblocks,
                               uint32_t index0, uint32_t key0, const void* own_src,
                               uint32_t own_index, int64_t* stamp, cudaStream_t stream,
-                              int* launches);
+                              int* launches, uint64_t elem_base = 0);
 
 // One-kernel multi-GPU allreduce over peer memory (see kernels.cu).
 constexpr int kMaxReal = 8;
