@@ -112,7 +112,7 @@ cemuResult_t cemuGroupStart(void);
 cemuResult_t cemuGroupEnd(void);
 
 /* Host-buffer forms of allreduce / allgather: `sendbuff`/`recvbuff` are HOST
- * memory, as WorkerSession's spans are (collective.hpp:66-75:
+ * memory, as WorkerSession's spans are (collective.hpp:68-78:
  * allreduce_async(span<uint8_t>, elem_size), allgather_async(span, ...)).
  * Stream-ordered like cudaMemcpyAsync: recvbuff is complete when `stream`
  * reaches the end of the call (cudaStreamSynchronize = WorkerSession::wait).

@@ -187,7 +187,7 @@ class Communicator:
                                 self._h, _stream_ptr(stream)), self._h)
         return recv
 
-    # -- host buffers (WorkerSession's span shape, collective.hpp:66-75) ------
+    # -- host buffers (WorkerSession's span shape, collective.hpp:68-78) ------
     def all_reduce_host(self, send: torch.Tensor, recv: torch.Tensor | None = None, stream=None):
         """Allreduce of a HOST tensor (pin it for overlapped copies).  Stream-
         ordered: synchronize `stream` before reading `recv`."""
@@ -405,7 +405,10 @@ class WorkerSession:
         issue = _now_us()
         self._submit("allreduce", buffer, elem_size)
         t = self._typed(buffer, elem_size)
-        self.comm.all_reduce(t, t, stream=self.stream)
+        if t.is_cuda:
+            self.comm.all_reduce(t, t, stream=self.stream)
+        else:  # a host span, as the reference's (cemuAllReduceHost)
+            self.comm.all_reduce_host(t, t, stream=self.stream)
         return self._handle(issue)
 
     def allgather_async(self, full: torch.Tensor, elem_size: int) -> CollHandle:
@@ -416,7 +419,10 @@ class WorkerSession:
         if block * self.comm.world_size != t.numel():
             raise TransportError("allgather buffer is not world_size blocks")
         own = t[self._rank * block:(self._rank + 1) * block]
-        self.comm.all_gather(own, t, stream=self.stream)
+        if t.is_cuda:
+            self.comm.all_gather(own, t, stream=self.stream)
+        else:
+            self.comm.all_gather_host(own, t, stream=self.stream)
         return self._handle(issue)
 
     def wait(self, h: CollHandle) -> None:

@@ -773,7 +773,7 @@ cemuResult_t do_broadcast(const void* send, void* recv, size_t count, int dt, in
 }
 
 // ---- host-buffer collectives -------------------------------------------------
-// The reference's WorkerSession takes host spans (collective.hpp:66-75);
+// The reference's WorkerSession takes host spans (collective.hpp:68-78);
 // these entry points keep that shape.  One real GPU, hash payload: the
 // buffer streams through the pipe in chunks, chunk i's H2D overlapping chunk
 // i-1's synthesis and chunk i-2's D2H (PCIe is full duplex; the kernel takes

@@ -1,7 +1,7 @@
 """Host-buffer collectives (cemuAllReduceHost / cemuAllGatherHost).
 
 The reference's boundary, WorkerSession, takes host spans
-(proj/include/cemu/collective.hpp:66-75) and returns when `wait` does; the
+(proj/include/cemu/collective.hpp:68-78) and returns when `wait` does; the
 host forms keep that shape, stream-ordered.  With one real GPU the buffer is
 pipelined through the device in chunks (H2D / synthesis / D2H on three
 streams over four rotating device buffers): the tests force 1 MiB chunks so
@@ -163,3 +163,23 @@ def test_host_usage_errors(cuda):
     assert lib.cemuGroupEnd() == 0
     assert r == 5 and b"cannot be grouped" in lib.cemuGetLastError(None)
     comm.close()
+
+
+def test_worker_session_mirror_takes_host_spans(small_chunks):
+    """pb.WorkerSession with CPU tensors = the reference's host-span calls
+    (allreduce_async(span, elem_size) + wait), through the host C-ABI."""
+    W = 4
+    plan = [pb.CollectivePlanEntry("allreduce", 4 * 4099, 4), pb.CollectivePlanEntry("allgather", 1000, 1)]
+    s = pb.WorkerSession(config(W), 0, plan)
+    h = host_input(2, 4099, seed=11)
+    buf = h.clone().view(torch.uint8)
+    s.wait(s.allreduce_async(buf, 4))
+    want = P.allreduce(2, P.PAYLOAD_HASH, W, [0], 0, 1, [to_np(h)], 4099)
+    assert_bit_equal(buf.view(torch.int32).numpy(), want, "session allreduce (host span)")
+    full = torch.zeros(1000 * W, dtype=torch.uint8)
+    own = host_input(1, 1000, seed=12)
+    full[:1000] = own
+    s.allgather(full, 1)
+    want = P.allgather(1, P.PAYLOAD_HASH, W, [0], 0, 1, [to_np(own)], 1000)
+    assert_bit_equal(full.numpy(), want, "session allgather (host span)")
+    s.close()
