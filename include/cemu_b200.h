@@ -127,6 +127,28 @@ cemuResult_t cemuAllReduceHost(const void* sendbuff, void* recvbuff, size_t coun
 cemuResult_t cemuAllGatherHost(const void* sendbuff, void* recvbuff, size_t sendcount,
                                cemuDataType_t datatype, cemuComm_t comm, cemuStream_t stream);
 
+/* Wire mode (interop with a reference `cemu-emulator`).
+ * Dials endpoint[successor(rank)] of the comm's config (which must carry
+ * endpoint.R keys and the reference's own keys only, so both sides compute
+ * the same config digest), performs the HELLO/TOPO handshake with `plan`
+ * (transport.hpp:25-40; allgather bytes = per-rank block) and from then on
+ * runs cemuAllReduce / cemuAllGather over the CEMU frame protocol exactly
+ * as WorkerSession::run_op does (collective.cpp:268-355): outgoing chunks
+ * are read from the device buffer, incoming DATA payloads folded on the GPU
+ * (int32 lanes when the element size is 4, bytes otherwise).  Calls become
+ * host-synchronous; their call record holds the device model's floors and
+ * the reference engine's observed release (arrival) times.  Replaces the
+ * WorkerSession constructor's dial + handshake (collective.cpp:28-77);
+ * detach (or cemuCommDestroy) sends BYE (collective.cpp:406-442). */
+typedef struct {
+  int32_t coll;     /* 0 allreduce, 1 allgather */
+  uint64_t bytes;   /* allreduce: buffer bytes; allgather: per-rank block */
+  uint32_t elemSize;
+} cemuPlanEntry;
+cemuResult_t cemuCommAttachEmulator(cemuComm_t comm, const cemuPlanEntry* plan, size_t nplan,
+                                    int timeoutMs);
+cemuResult_t cemuCommDetachEmulator(cemuComm_t comm);
+
 /* Symmetric device memory (ncclMemAlloc / window-registration analogue).
  * Collective over the job's real ranks on this box: each allocates `bytes`
  * and maps every peer's allocation (CUDA IPC).  An allreduce whose send and

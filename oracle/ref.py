@@ -68,6 +68,14 @@ def lib():
         L.ref_run_training_loop.argtypes = [cp, u32, u64, C.c_int, dbl, dbl, dbl, dbl, dbl, vp, sz, cp, sz]
         L.ref_real_ring.restype = C.c_int
         L.ref_real_ring.argtypes = [u32, C.c_int, vp, u64, u32, cp, sz]
+        L.ref_emulator_start.restype = vp
+        L.ref_emulator_start.argtypes = [cp, cp, sz]
+        L.ref_emulator_sessions.restype = u64
+        L.ref_emulator_sessions.argtypes = [vp]
+        L.ref_emulator_stop.restype = None
+        L.ref_emulator_stop.argtypes = [vp]
+        L.ref_config_digest.restype = u64
+        L.ref_config_digest.argtypes = [cp]
         _LIB = L
     return _LIB
 
@@ -228,3 +236,34 @@ def bucketize(text: str, bucket_bytes: int):
 def trace_open(path: str) -> None:
     """Opens the reference's process-wide EventLog (trace.cpp:9-19)."""
     lib().ref_trace_open(path.encode())
+
+
+class Emulator:
+    """A reference EmulatorServer (emulator.cpp) serving in a thread of this
+    process, on the config's emulated endpoint -- the `cemu-emulator` the
+    B200 wire mode talks to in the interop tests."""
+
+    def __init__(self, cfg_text: str):
+        err = C.create_string_buffer(1024)
+        self._h = lib().ref_emulator_start(cfg_text.encode(), err, 1024)
+        if not self._h:
+            raise RefError(err.value.decode())
+
+    @property
+    def sessions(self) -> int:
+        return lib().ref_emulator_sessions(self._h)
+
+    def stop(self):
+        if self._h:
+            lib().ref_emulator_stop(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.stop()
+
+
+def config_digest(text: str) -> int:
+    return lib().ref_config_digest(text.encode())

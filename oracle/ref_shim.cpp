@@ -19,6 +19,9 @@
 //                                  proj/tests/test_transport.cpp:38-54
 //   all-real ring ................ n WorkerSessions in threads
 //                                  (proj/tests/test_transport.cpp:218-237)
+//   emulator server .............. EmulatorServer serving in a thread, for
+//                                  the B200 wire-mode interop tests
+//                                  (proj/tools/cemu_emulator.cpp's role)
 #include <netinet/in.h>
 #include <sys/socket.h>
 #include <unistd.h>
@@ -464,6 +467,51 @@ int ref_run_training_loop(const char* model_text, uint32_t n, uint64_t bucket_by
   } catch (const std::exception& e) {
     put_err(err, errcap, e.what());
     return -1;
+  }
+}
+
+
+
+// ---- a reference emulator process, in a thread ------------------------------
+// Parses `cfg_text` with the reference parser, binds the emulator endpoint
+// (emulator.cpp:14-39) and serves sessions until ref_emulator_stop.  Returns
+// a handle, or null with the ConfigError/NetError text in `err`.
+struct RefEmulator {
+  std::unique_ptr<EmulatorServer> server;
+  std::thread th;
+};
+
+void* ref_emulator_start(const char* cfg_text, char* err, size_t errcap) {
+  try {
+    const JobConfig cfg = parse_job_config(cfg_text);
+    auto* h = new RefEmulator;
+    h->server = std::make_unique<EmulatorServer>(cfg);
+    h->th = std::thread([h] { h->server->serve(); });
+    return h;
+  } catch (const std::exception& e) {
+    put_err(err, errcap, e.what());
+    return nullptr;
+  }
+}
+
+uint64_t ref_emulator_sessions(void* h) {
+  return h ? static_cast<RefEmulator*>(h)->server->sessions_served() : 0;
+}
+
+void ref_emulator_stop(void* hv) {
+  auto* h = static_cast<RefEmulator*>(hv);
+  if (!h) return;
+  h->server->request_stop();  // serve() polls the flag every 200 ms
+  if (h->th.joinable()) h->th.join();
+  delete h;
+}
+
+// config_digest of the reference parser (for the interop tests)
+uint64_t ref_config_digest(const char* cfg_text) {
+  try {
+    return config_digest(parse_job_config(cfg_text));
+  } catch (const std::exception&) {
+    return 0;
   }
 }
 

@@ -43,6 +43,10 @@ class ShardPlan(C.Structure):
                 ("tailOffset", C.c_uint64), ("tailCount", C.c_uint64)]
 
 
+class PlanEntry(C.Structure):
+    _fields_ = [("coll", C.c_int32), ("bytes", C.c_uint64), ("elemSize", C.c_uint32)]
+
+
 class CallRecord(C.Structure):
     _fields_ = [
         ("call_id", C.c_uint64), ("coll", C.c_int32), ("delay_active", C.c_int32),
@@ -75,6 +79,8 @@ def _load():
         "cemuAllReduce": (i32, [vp, vp, sz, i32, i32, vp, vp]),
         "cemuAllGather": (i32, [vp, vp, sz, i32, vp, vp]),
         "cemuAllReduceHost": (i32, [vp, vp, sz, i32, i32, vp, vp]),
+        "cemuCommAttachEmulator": (i32, [vp, vp, sz, i32]),
+        "cemuCommDetachEmulator": (i32, [vp]),
         "cemuAllGatherHost": (i32, [vp, vp, sz, i32, vp, vp]),
         "cemuReduceScatter": (i32, [vp, vp, sz, i32, i32, vp, vp]),
         "cemuBroadcast": (i32, [vp, vp, sz, i32, i32, vp, vp]),

@@ -203,6 +203,21 @@ class Communicator:
                                     self._h, _stream_ptr(stream)), self._h)
         return recv
 
+    # -- wire mode (interop with a reference cemu-emulator) -------------------
+    def attach_emulator(self, plan: list, timeout_ms: int = 10000) -> None:
+        """cemuCommAttachEmulator: dial the config's emulator endpoint and
+        handshake with `plan` (CollectivePlanEntry list); all_reduce /
+        all_gather then run the CEMU wire protocol, host-synchronously."""
+        arr = (_capi.PlanEntry * max(len(plan), 1))()
+        for i, e in enumerate(plan):
+            arr[i].coll = {"allreduce": 0, "allgather": 1}[e.kind]
+            arr[i].bytes = e.bytes
+            arr[i].elemSize = e.elem_size
+        check(lib.cemuCommAttachEmulator(self._h, arr, len(plan), timeout_ms), self._h)
+
+    def detach_emulator(self) -> None:
+        check(lib.cemuCommDetachEmulator(self._h), self._h)
+
     def _check_host(self, send, recv, recv_numel):
         if send.dtype != recv.dtype:
             raise CemuError(_capi.INVALID_ARGUMENT, "send/recv dtypes differ")

@@ -38,6 +38,7 @@
 #include "kernels.hpp"
 #include "payload.cuh"
 #include "schedule.hpp"
+#include "wire.hpp"
 
 using namespace cemu_b200;
 
@@ -188,6 +189,11 @@ struct cemuComm {
     cudaEvent_t loaded[kPipeBufs] = {}, done[kPipeBufs] = {}, drained[kPipeBufs] = {};
     void* buf[kPipeBufs] = {};
   } pipe;
+  // wire mode (cemuCommAttachEmulator): collectives travel the CEMU protocol
+  // to a reference emulator instead of being synthesised
+  std::unique_ptr<WireSession> wire;
+  void* wire_buf = nullptr;  // device staging of one received DATA payload
+  size_t wire_buf_bytes = 0;
 };
 
 namespace {
@@ -932,6 +938,87 @@ cemuResult_t host_allgather(const void* send, void* recv, size_t sc, int dt, cem
   return cemuSuccess;
 }
 
+// ---- wire mode -------------------------------------------------------------
+// The call runs the reference worker's op (collective.cpp:268-355) with the
+// buffer on the GPU: each outgoing chunk is read back from HBM, each incoming
+// DATA payload is copied up and folded by launch_wire_fold.  Host-synchronous
+// (the protocol is a conversation); results and the per-step arrival times
+// land in the call record, next to the device model's floors for the same
+// call, so the reference engine's releases can be checked against them.
+cemuResult_t wire_call(cemuComm* c, int coll, const void* send, void* recv, uint64_t buf_bytes, uint64_t model_bytes,
+                       uint32_t es, cudaStream_t s) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_OK(cudaStreamIsCapturing(s, &cap));
+  if (cap != cudaStreamCaptureStatusNone) {
+    return fail(cemuInvalidUsage, "wire mode: collectives are host-synchronous and cannot be captured");
+  }
+  auto* r8 = static_cast<uint8_t*>(recv);
+  if (coll == kAllReduce && send != recv) CUDA_OK(cudaMemcpyAsync(recv, send, buf_bytes, cudaMemcpyDeviceToDevice, s));
+  if (coll == kAllGather) {
+    uint8_t* own = r8 + static_cast<uint64_t>(c->rank) * model_bytes;
+    if (send != own) CUDA_OK(cudaMemcpyAsync(own, send, model_bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  CUDA_OK(cudaStreamSynchronize(s));
+  const uint64_t id = c->calls++;
+  const uint32_t i = static_cast<uint32_t>(id % cemuComm::kSlots);
+  auto& m = c->meta[i];
+  m.call_id = id;
+  m.coll = coll;
+  m.delay = true;  // the record holds the wire arrivals
+  m.k = to_real_count(coll, c->W, c->real);
+  m.bytes = model_bytes;
+  m.latency = call_latency_us(c->delay, coll, c->W, model_bytes, m.k);
+  int launches = 0;
+  cudaError_t cerr = cudaSuccess;
+  auto load = [&](uint64_t off, uint64_t len, uint8_t* host) {
+    if (cerr == cudaSuccess) cerr = cudaMemcpy(host, r8 + off, len, cudaMemcpyDeviceToHost);
+  };
+  auto store = [&](uint64_t off, const uint8_t* host, uint64_t len, bool reduce) {
+    if (cerr != cudaSuccess || len == 0) return;
+    if (!reduce) {
+      cerr = cudaMemcpy(r8 + off, host, len, cudaMemcpyHostToDevice);
+      return;
+    }
+    if (c->wire_buf_bytes < len) {
+      if (c->wire_buf) cudaFree(c->wire_buf);
+      c->wire_buf = nullptr;
+      c->wire_buf_bytes = 0;
+      if ((cerr = cudaMalloc(&c->wire_buf, len)) != cudaSuccess) return;
+      c->wire_buf_bytes = len;
+    }
+    if ((cerr = cudaMemcpyAsync(c->wire_buf, host, len, cudaMemcpyHostToDevice, s)) != cudaSuccess) return;
+    if ((cerr = launch_wire_fold(r8 + off, c->wire_buf, len, es == 4, s, &launches)) != cudaSuccess) return;
+    cerr = cudaStreamSynchronize(s);
+  };
+  int64_t t_open = 0;
+  std::vector<int64_t> arrivals;
+  try {
+    c->wire->run(coll, buf_bytes, es, load, store, &t_open, &arrivals);
+  } catch (const WireError& e) {
+    c->launches += launches;
+    return fail(cemuRemoteError, e.what());
+  }
+  c->launches += launches;
+  CUDA_OK(cerr);
+  // call record: model floors beside the reference engine's observed releases
+  const std::vector<double> offs = release_offsets(c->delay, coll, c->W, model_bytes, m.k);
+  std::vector<int64_t> rec(slot_words(c->kmax), 0);
+  rec[0] = t_open;
+  int64_t maxf = 0;
+  for (uint32_t j = 0; j < m.k; ++j) {
+    const int64_t f = std::llround(offs[j]);
+    maxf = std::max(maxf, f);
+    rec[kSlotHeader + j] = f;
+    rec[kSlotHeader + c->kmax + j] = j < arrivals.size() ? arrivals[j] : 0;
+    std::memcpy(&rec[kSlotHeader + 2 * c->kmax + j], &offs[j], 8);
+  }
+  rec[1] = arrivals.empty() ? t_open : arrivals.back();
+  rec[2] = maxf;
+  rec[3] = m.k;
+  CUDA_OK(cudaMemcpy(c->d_slots + i * slot_words(c->kmax), rec.data(), rec.size() * 8, cudaMemcpyHostToDevice));
+  return cemuSuccess;
+}
+
 // A collective is planned into phases (closures); nothing runs at planning
 // time.  Alone, its phases run back to back.  In a group, cemuGroupEnd runs
 // "rounds" -- the i-th call of every communicator -- phase by phase, each
@@ -1117,6 +1204,8 @@ cemuResult_t cemuCommDestroy(cemuComm_t c) {
     cudaStreamDestroy(p.comp);
     cudaStreamDestroy(p.d2h);
   }
+  c->wire.reset();  // BYE
+  if (c->wire_buf) cudaFree(c->wire_buf);
   if (c->inner && nccl()) nccl()->CommDestroy(c->inner);
   cudaFree(c->d_virt_keys);
   cudaFree(c->d_virt_ranks);
@@ -1165,6 +1254,11 @@ cemuResult_t cemuAllReduce(const void* send, void* recv, size_t count, cemuDataT
   if (auto r = check_op(op, "cemuAllReduce")) return r;
   if (count && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllReduce: null buffer");
   auto s = reinterpret_cast<cudaStream_t>(stream);
+  if (c->wire) {
+    if (g_group_depth > 0) return fail(cemuInvalidUsage, "wire mode: collectives cannot be grouped");
+    const uint64_t b = static_cast<uint64_t>(count) * dtype_size(dt);
+    return wire_call(c, kAllReduce, send, recv, b, b, static_cast<uint32_t>(dtype_size(dt)), s);
+  }
   return run_or_defer(c, [=](Phases& ph) { return do_allreduce(send, recv, count, dt, c, s, ph); });
 }
 
@@ -1174,6 +1268,7 @@ cemuResult_t cemuAllReduceHost(const void* send, void* recv, size_t count, cemuD
   if (auto r = check_op(op, "cemuAllReduceHost")) return r;
   if (count && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllReduceHost: null buffer");
   if (g_group_depth > 0) return fail(cemuInvalidUsage, "cemuAllReduceHost: host-buffer collectives cannot be grouped");
+  if (c->wire) return fail(cemuInvalidUsage, "cemuAllReduceHost: not available in wire mode");
   if (count == 0) return cemuSuccess;
   try {
     return host_allreduce(send, recv, count, dt, c, reinterpret_cast<cudaStream_t>(stream));
@@ -1187,6 +1282,7 @@ cemuResult_t cemuAllGatherHost(const void* send, void* recv, size_t sc, cemuData
   if (auto r = check_common(c, dt, "cemuAllGatherHost")) return r;
   if (sc && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllGatherHost: null buffer");
   if (g_group_depth > 0) return fail(cemuInvalidUsage, "cemuAllGatherHost: host-buffer collectives cannot be grouped");
+  if (c->wire) return fail(cemuInvalidUsage, "cemuAllGatherHost: not available in wire mode");
   if (sc == 0) return cemuSuccess;
   try {
     return host_allgather(send, recv, sc, dt, c, reinterpret_cast<cudaStream_t>(stream));
@@ -1200,6 +1296,11 @@ cemuResult_t cemuAllGather(const void* send, void* recv, size_t sc, cemuDataType
   if (auto r = check_common(c, dt, "cemuAllGather")) return r;
   if (sc && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllGather: null buffer");
   auto s = reinterpret_cast<cudaStream_t>(stream);
+  if (c->wire) {
+    if (g_group_depth > 0) return fail(cemuInvalidUsage, "wire mode: collectives cannot be grouped");
+    const uint64_t b = static_cast<uint64_t>(sc) * dtype_size(dt);
+    return wire_call(c, kAllGather, send, recv, b * c->W, b, static_cast<uint32_t>(dtype_size(dt)), s);
+  }
   return run_or_defer(c, [=](Phases& ph) { return do_allgather(send, recv, sc, dt, c, s, ph); });
 }
 
@@ -1208,6 +1309,7 @@ cemuResult_t cemuReduceScatter(const void* send, void* recv, size_t rc, cemuData
   if (auto r = check_common(c, dt, "cemuReduceScatter")) return r;
   if (auto r = check_op(op, "cemuReduceScatter")) return r;
   if (rc && (!send || !recv)) return fail(cemuInvalidArgument, "cemuReduceScatter: null buffer");
+  if (c->wire) return fail(cemuInvalidUsage, "wire mode: the CEMU protocol has allreduce and allgather only");
   auto s = reinterpret_cast<cudaStream_t>(stream);
   return run_or_defer(c, [=](Phases& ph) { return do_reducescatter(send, recv, rc, dt, c, s, ph); });
 }
@@ -1216,6 +1318,7 @@ cemuResult_t cemuBroadcast(const void* send, void* recv, size_t count, cemuDataT
                            cemuComm_t c, cemuStream_t stream) {
   if (auto r = check_common(c, dt, "cemuBroadcast")) return r;
   if (count && !recv) return fail(cemuInvalidArgument, "cemuBroadcast: null recvbuff");
+  if (c->wire) return fail(cemuInvalidUsage, "wire mode: the CEMU protocol has allreduce and allgather only");
   auto s = reinterpret_cast<cudaStream_t>(stream);
   return run_or_defer(c, [=](Phases& ph) { return do_broadcast(send, recv, count, dt, root, c, s, ph); });
 }
@@ -1404,4 +1507,34 @@ int cemuCommEventLog(cemuComm_t c, uint64_t id, char* out, size_t cap) {
 }  // extern "C"
 
 // launch counter for bench.py's gpu_launches (not part of the public header)
+extern "C" cemuResult_t cemuCommAttachEmulator(cemuComm_t c, const cemuPlanEntry* plan, size_t nplan,
+                                               int timeoutMs) {
+  if (!c) return fail(cemuInvalidArgument, "cemuCommAttachEmulator: comm is null");
+  if (nplan && !plan) return fail(cemuInvalidArgument, "cemuCommAttachEmulator: plan is null");
+  if (c->wire) return fail(cemuInvalidUsage, "cemuCommAttachEmulator: already attached");
+  if (c->k != 1) return fail(cemuInvalidUsage, "cemuCommAttachEmulator: wire mode serves one real rank per box");
+  std::vector<WirePlanEntry> p;
+  for (size_t j = 0; j < nplan; ++j) {
+    if (plan[j].coll != kAllReduce && plan[j].coll != kAllGather) {
+      return fail(cemuInvalidArgument, "cemuCommAttachEmulator: plan entry " + std::to_string(j) +
+                                           " is not allreduce/allgather");
+    }
+    p.push_back(WirePlanEntry{plan[j].coll, plan[j].bytes, plan[j].elemSize});
+  }
+  try {
+    c->wire = std::make_unique<WireSession>(c->cfg, c->rank, std::move(p), timeoutMs > 0 ? timeoutMs : 10000);
+  } catch (const WireError& e) {
+    return fail(cemuRemoteError, e.what());
+  } catch (const std::exception& e) {
+    return fail(cemuSystemError, e.what());
+  }
+  return cemuSuccess;
+}
+
+extern "C" cemuResult_t cemuCommDetachEmulator(cemuComm_t c) {
+  if (!c) return fail(cemuInvalidArgument, "cemuCommDetachEmulator: comm is null");
+  c->wire.reset();
+  return cemuSuccess;
+}
+
 extern "C" uint64_t cemuCommKernelLaunches(cemuComm_t c) { return c ? c->launches : 0; }

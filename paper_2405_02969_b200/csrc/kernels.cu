@@ -1176,6 +1176,32 @@ cudaError_t launch_fused_allgather(int dtype, const FusedGatherArgs& a, cudaStre
   return cudaGetLastError();
 }
 
+// Wire-mode fold of a received DATA payload (collective.cpp:343-350):
+// int32 lanes (wrapping) when the plan's elem_size is 4, bytes otherwise.
+__global__ void wire_fold_kernel(uint8_t* dst, const uint8_t* src, uint64_t bytes, int words) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (words) {
+    auto* d = reinterpret_cast<uint32_t*>(dst);
+    const auto* q = reinterpret_cast<const uint32_t*>(src);
+    for (uint64_t i = t0; i < bytes / 4; i += stride) d[i] += q[i];
+  } else {
+    for (uint64_t i = t0; i < bytes; i += stride) dst[i] = static_cast<uint8_t>(dst[i] + src[i]);
+  }
+}
+
+cudaError_t launch_wire_fold(void* dst, const void* src, uint64_t bytes, bool words, cudaStream_t s,
+                             int* launches) {
+  if (bytes == 0) return cudaSuccess;
+  ++*launches;
+  const uint64_t units = words ? bytes / 4 : bytes;
+  const unsigned grid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>((units + kThreads - 1) / kThreads, sm_count() * 8ull)));
+  wire_fold_kernel<<<grid, kThreads, 0, s>>>(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes,
+                                             words ? 1 : 0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stamp(int64_t* slot, cudaStream_t s, int* launches) {
   ++*launches;
   stamp_kernel<<<1, 1, 0, s>>>(slot);

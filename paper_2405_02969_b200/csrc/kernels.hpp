@@ -95,6 +95,9 @@ struct FusedGatherArgs {
 };
 cudaError_t launch_fused_allgather(int dtype, const FusedGatherArgs& a, cudaStream_t stream, int* launches);
 
+// wire mode: dst += src as int32 lanes (words) or bytes, wrapping
+cudaError_t launch_wire_fold(void* dst, const void* src, uint64_t bytes, bool words, cudaStream_t stream,
+                             int* launches);
 cudaError_t launch_stamp(int64_t* slot, cudaStream_t stream, int* launches);
 // chain: device int64 holding the previous spin's absolute deadline (or null)
 cudaError_t launch_spin_ns(int64_t ns, cudaStream_t stream, int* launches, int64_t* chain = nullptr,
