@@ -516,8 +516,8 @@ def run_ours(args, rank, world_size, local_rank):
            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(e2e_ms, 3),
            "path": ("pinned host -> cemuAllReduceHost (C-ABI; chunked H2D / synthesis / D2H pipeline on "
                     "three streams) -> pinned host" if n == 1 else
-                    "pinned host -> cemuAllReduceHost (C-ABI; staged through device scratch, NCCL real part) "
-                    "-> pinned host"),
+                    "pinned host -> cemuAllReduceHost (C-ABI; chunked H2D / fused NVLink allreduce + synthesis "
+                    "/ D2H pipeline over symmetric buffers) -> pinned host"),
            "unpipelined_reference_point": {
                "value": round(n * 2 * nbytes / (staged_ms * 1e-3) / 1e9, 2), "ms_per_step": round(staged_ms, 3),
                "path": "pinned host -> cudaMemcpyAsync -> cemuAllReduce -> cudaMemcpyAsync -> pinned host"}}

@@ -188,6 +188,8 @@ struct cemuComm {
     cudaEvent_t start = nullptr;
     cudaEvent_t loaded[kPipeBufs] = {}, done[kPipeBufs] = {}, drained[kPipeBufs] = {};
     void* buf[kPipeBufs] = {};
+    bool symmetric = false;            // k > 1: buffers are regions mapped on every real GPU
+    uint8_t* peer[kPipeBufs][kMaxReal] = {};
   } pipe;
   // wire mode (cemuCommAttachEmulator): collectives travel the CEMU protocol
   // to a reference emulator instead of being synthesised
@@ -472,6 +474,33 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
 // ----------------------------------------------------------------------------
 // collective bodies
 // ----------------------------------------------------------------------------
+// Fused allreduce over `count` elements whose payload indices start at e0
+// (a word boundary): this GPU reduces its 1/k of the 16-byte vectors, the
+// last GPU also the ragged tail.  src/dst: every real GPU's buffer.
+FusedArgs fused_allreduce_args(const cemuComm* c, int dt, uint64_t count, uint64_t e0, uint8_t* const* src,
+                               uint8_t* const* dst) {
+  FusedArgs a;
+  const uint64_t es = dtype_size(dt);
+  const uint64_t epv = 16 / es;
+  const uint64_t nvec = count / epv;
+  const uint64_t per = nvec / c->k;
+  a.k = static_cast<int>(c->k);
+  a.me = static_cast<int>(c->li);
+  a.ndst = a.k;
+  a.word_base = (dt == cemuInt32 || dt == cemuUint32) ? e0 : e0 / 4;
+  a.v_begin = per * c->li;
+  a.v_end = c->li + 1 == c->k ? nvec : per * (c->li + 1);
+  a.ntail = c->li + 1 == c->k ? static_cast<uint32_t>(count - nvec * epv) : 0;
+  a.tail_e0 = e0 + nvec * epv;
+  for (uint32_t g = 0; g < c->k; ++g) {
+    a.src[g] = reinterpret_cast<const uint4*>(src[g]);
+    a.dst[g] = reinterpret_cast<uint4*>(dst[g]);
+  }
+  a.keys = c->d_virt_keys;
+  a.nkeys = static_cast<uint32_t>(c->virt.size());
+  return a;
+}
+
 cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, cemuComm* c,
                           cudaStream_t s, Phases& ph) {
   const size_t es = dtype_size(dt);
@@ -510,27 +539,15 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   const cemuComm::Region* rs = c->fused ? find_region(c, send, count * es) : nullptr;
   const cemuComm::Region* rr = c->fused ? find_region(c, recv, count * es) : nullptr;
   if (rs && rr && dtype_size(dt) <= 4 && dt != cemuInt64) {
-    FusedArgs a;
-    const uint64_t epv = 16 / es;
-    const uint64_t nvec = count / epv;
-    const uint64_t per = nvec / c->k;
-    a.k = static_cast<int>(c->k);
-    a.me = static_cast<int>(c->li);
-    a.ndst = a.k;
-    a.word_base = 0;
-    a.v_begin = per * c->li;
-    a.v_end = c->li + 1 == c->k ? nvec : per * (c->li + 1);
-    const bool last = c->li + 1 == c->k;
-    a.ntail = last ? static_cast<uint32_t>(count - nvec * epv) : 0;
-    a.tail_e0 = nvec * epv;
     const uint64_t soff = static_cast<const uint8_t*>(send) - rs->base;
     const uint64_t roff = static_cast<uint8_t*>(recv) - rr->base;
+    uint8_t* sp[kMaxReal];
+    uint8_t* dp[kMaxReal];
     for (uint32_t g = 0; g < c->k; ++g) {
-      a.src[g] = reinterpret_cast<const uint4*>(rs->peer[g] + soff);
-      a.dst[g] = reinterpret_cast<uint4*>(rr->peer[g] + roff);
+      sp[g] = rs->peer[g] + soff;
+      dp[g] = rr->peer[g] + roff;
     }
-    a.keys = c->d_virt_keys;
-    a.nkeys = static_cast<uint32_t>(c->virt.size());
+    FusedArgs a = fused_allreduce_args(c, dt, count, 0, sp, dp);
     if ((soff | roff) % 16 == 0) ph.push_back([=]() mutable -> cemuResult_t {
       set_barrier(c, a);
       a.sig = op_sig(kAllReduce, dt, count);
@@ -796,8 +813,23 @@ cemuResult_t ensure_pipe(cemuComm* c) {
   CUDA_OK(cudaStreamCreateWithFlags(&p.comp, cudaStreamNonBlocking));
   CUDA_OK(cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking));
   CUDA_OK(cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming));
+  // several real GPUs: the buffers are symmetric (mapped on every real GPU,
+  // collective like cemuMemAlloc) so each chunk is one fused kernel
+  p.symmetric = c->k > 1;
   for (int b = 0; b < cemuComm::kPipeBufs; ++b) {
-    CUDA_OK(cudaMalloc(&p.buf[b], p.chunk));
+    if (p.symmetric) {
+      const size_t rounded = (p.chunk + (2u << 20) - 1) & ~static_cast<size_t>((2u << 20) - 1);
+      CUDA_OK(cudaMalloc(&p.buf[b], rounded));
+      cemuComm::Region r;
+      r.base = static_cast<uint8_t*>(p.buf[b]);
+      r.bytes = rounded;
+      r.peer[c->li] = r.base;
+      if (auto e = map_peers(c, p.buf[b], rounded, r.peer)) return e;
+      c->regions.push_back(r);
+      for (uint32_t g = 0; g < c->k; ++g) p.peer[b][g] = r.peer[g];
+    } else {
+      CUDA_OK(cudaMalloc(&p.buf[b], p.chunk));
+    }
     CUDA_OK(cudaEventCreateWithFlags(&p.loaded[b], cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&p.done[b], cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&p.drained[b], cudaEventDisableTiming));
@@ -812,7 +844,7 @@ struct PipeChunk {
   const void* in = nullptr;  // host source (null: nothing to load)
   void* out = nullptr;       // host destination
   size_t bytes = 0;
-  std::function<cudaError_t(void* dbuf, cudaStream_t)> work;
+  std::function<cudaError_t(int b, void* dbuf, cudaStream_t)> work;
 };
 
 cemuResult_t run_pipe(cemuComm* c, cudaStream_t s, const std::vector<PipeChunk>& chunks) {
@@ -836,7 +868,7 @@ cemuResult_t run_pipe(cemuComm* c, cudaStream_t s, const std::vector<PipeChunk>&
     if (ch.in) CUDA_OK(cudaMemcpyAsync(p.buf[b], ch.in, ch.bytes, cudaMemcpyHostToDevice, p.h2d));
     CUDA_OK(cudaEventRecord(p.loaded[b], p.h2d));
     CUDA_OK(cudaStreamWaitEvent(p.comp, p.loaded[b], 0));
-    CUDA_OK(ch.work(p.buf[b], p.comp));
+    CUDA_OK(ch.work(b, p.buf[b], p.comp));
     CUDA_OK(cudaEventRecord(p.done[b], p.comp));
     CUDA_OK(cudaStreamWaitEvent(p.d2h, p.done[b], 0));
     CUDA_OK(cudaMemcpyAsync(ch.out, p.buf[b], ch.bytes, cudaMemcpyDeviceToHost, p.d2h));
@@ -860,7 +892,10 @@ cemuResult_t run_pipe(cemuComm* c, cudaStream_t s, const std::vector<PipeChunk>&
 cemuResult_t host_allreduce(const void* send, void* recv, size_t count, int dt, cemuComm* c, cudaStream_t s) {
   const size_t es = dtype_size(dt);
   const uint64_t bytes = static_cast<uint64_t>(count) * es;
-  if (c->k > 1 || c->mode != PayloadMode::kHash) {  // staged through device scratch
+  // several real GPUs: chunks go through the fused kernel over symmetric
+  // pipe buffers (rank-independent decision: every real rank pipelines)
+  const bool fused = c->k > 1 && c->fused && es <= 4 && c->mode == PayloadMode::kHash;
+  if ((c->k > 1 && !fused) || c->mode != PayloadMode::kHash) {  // staged through device scratch
     if (auto r = ensure_scratch(c, bytes)) return r;
     CUDA_OK(cudaMemcpyAsync(c->scratch, send, bytes, cudaMemcpyHostToDevice, s));
     Phases ph;
@@ -883,9 +918,18 @@ cemuResult_t host_allreduce(const void* send, void* recv, size_t count, int dt, 
     ch.out = static_cast<uint8_t*>(recv) + e0 * es;
     ch.bytes = n * es;
     const uint32_t nk = static_cast<uint32_t>(c->virt.size());
-    ch.work = [c, call, dt, n, e0, nk](void* d, cudaStream_t st) {
-      return launch_synth_reduce(dt, d, d, n, e0, c->d_virt_keys, nk, nullptr, st, &call->launches);
-    };
+    if (fused) {
+      ch.work = [c, call, dt, n, e0](int b, void*, cudaStream_t st) {
+        FusedArgs a = fused_allreduce_args(c, dt, n, e0, c->pipe.peer[b], c->pipe.peer[b]);  // in place
+        set_barrier(c, a);
+        a.sig = op_sig(kAllReduce, dt, n);
+        return launch_fused_allreduce(dt, a, st, &call->launches);
+      };
+    } else {
+      ch.work = [c, call, dt, n, e0, nk](int, void* d, cudaStream_t st) {
+        return launch_synth_reduce(dt, d, d, n, e0, c->d_virt_keys, nk, nullptr, st, &call->launches);
+      };
+    }
     chunks.push_back(std::move(ch));
   }
   if (auto r = run_pipe(c, s, chunks)) return r;
@@ -926,7 +970,7 @@ cemuResult_t host_allgather(const void* send, void* recv, size_t sc, int dt, cem
       PipeChunk ch;
       ch.out = r8 + r * blk + e0 * es;
       ch.bytes = n * es;
-      ch.work = [call, dt, n, e0, key](void* d, cudaStream_t st) {
+      ch.work = [call, dt, n, e0, key](int, void* d, cudaStream_t st) {
         return launch_synth_fill(dt, d, n, nullptr, nullptr, 1, 0, key, nullptr, 0, nullptr, st, &call->launches,
                                  e0);
       };
@@ -1194,7 +1238,7 @@ cemuResult_t cemuCommDestroy(cemuComm_t c) {
     auto& p = c->pipe;
     cudaStreamSynchronize(p.d2h);
     for (int b = 0; b < cemuComm::kPipeBufs; ++b) {
-      cudaFree(p.buf[b]);
+      if (!p.symmetric) cudaFree(p.buf[b]);  // symmetric ones are regions, freed above
       cudaEventDestroy(p.loaded[b]);
       cudaEventDestroy(p.done[b]);
       cudaEventDestroy(p.drained[b]);

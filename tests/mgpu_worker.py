@@ -37,6 +37,7 @@ def main():
 
 
 def run():
+    os.environ["CEMU_HOST_CHUNK_MIB"] = "1"  # host-buffer pipeline: many chunks per call
     local = int(os.environ["LOCAL_RANK"])
     n = int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(local)
@@ -94,6 +95,26 @@ def run():
                     rs = to_np(sends[real.index(root)]) if root in real else None
                     want = P.broadcast(dt, P.PAYLOAD_HASH, W, real, me, root, 1, rs, count)
                     assert_bit_equal(to_np(b), want, f"broadcast root={root} dt={dt}")
+        # host-buffer allreduce: chunks pipelined through symmetric pipe buffers,
+        # one fused kernel per chunk (1 MiB chunks: the buffers rotate)
+        for dt in (7, 9, 2):
+            for count in (5, (5 << 20) // 2 + 7):
+                sends = []
+                for i in range(n):
+                    gi = np.random.default_rng(300 * i + count + dt)
+                    if dt in (7, 9):
+                        v = torch.from_numpy(gi.standard_normal(count).astype(np.float32)).to(TORCH[dt])
+                    else:
+                        v = torch.from_numpy(gi.integers(-2**31, 2**31, size=count).astype(np.int64)).to(TORCH[dt])
+                    sends.append(v)
+                trace(f"host pipeline real={real} dt={dt} count={count}")
+                hin = sends[local].pin_memory()
+                hout = torch.empty_like(hin).pin_memory()
+                comm.all_reduce_host(hin, hout)
+                torch.cuda.synchronize()
+                assert comm.async_error() is None
+                want = P.allreduce(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(s) for s in sends], count)
+                assert_bit_equal(to_np(hout), want, f"host allreduce real={real} dt={dt} n={count}")
         # fused path: symmetric buffers -> one kernel over NVLink peer memory,
         # arbitrary (non-dyadic) floats: the real fold order is the oracle's
         for dt in (7, 9, 6, 2, 1):
