@@ -538,7 +538,7 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   // k real GPUs, buffers from cemuMemAlloc: one fused kernel over peer memory
   const cemuComm::Region* rs = c->fused ? find_region(c, send, count * es) : nullptr;
   const cemuComm::Region* rr = c->fused ? find_region(c, recv, count * es) : nullptr;
-  if (rs && rr && dtype_size(dt) <= 4 && dt != cemuInt64) {
+  if (rs && rr && dtype_size(dt) <= 4 && dt != cemuInt64 && nk > 0) {
     const uint64_t soff = static_cast<const uint8_t*>(send) - rs->base;
     const uint64_t roff = static_cast<uint8_t*>(recv) - rr->base;
     uint8_t* sp[kMaxReal];
@@ -705,7 +705,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
   // through an aligned staging buffer instead of changing the decision.
   const cemuComm::Region* rs = c->fused ? find_region(c, send, rc * es * c->W) : nullptr;
   const uint64_t sbase = rs ? static_cast<uint64_t>(s8 - rs->base) : 1;
-  if (rs && es <= 4 && sbase % 16 == 0 && (rc * es) % 16 == 0) {
+  if (rs && es <= 4 && nk > 0 && sbase % 16 == 0 && (rc * es) % 16 == 0) {
     ph.push_back([=]() -> cemuResult_t {
     const uint64_t soff = sbase + mine * es;
     void* out = recv;
@@ -894,7 +894,7 @@ cemuResult_t host_allreduce(const void* send, void* recv, size_t count, int dt, 
   const uint64_t bytes = static_cast<uint64_t>(count) * es;
   // several real GPUs: chunks go through the fused kernel over symmetric
   // pipe buffers (rank-independent decision: every real rank pipelines)
-  const bool fused = c->k > 1 && c->fused && es <= 4 && c->mode == PayloadMode::kHash;
+  const bool fused = c->k > 1 && c->fused && es <= 4 && c->mode == PayloadMode::kHash && !c->virt.empty();
   if ((c->k > 1 && !fused) || c->mode != PayloadMode::kHash) {  // staged through device scratch
     if (auto r = ensure_scratch(c, bytes)) return r;
     CUDA_OK(cudaMemcpyAsync(c->scratch, send, bytes, cudaMemcpyHostToDevice, s));

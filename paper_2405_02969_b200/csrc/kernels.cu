@@ -177,9 +177,24 @@ __device__ void elem_fill(void* dst, uint64_t i, uint64_t e, uint32_t raw_key) {
   }
 }
 
-__device__ __forceinline__ void load_keys(uint2* skeys, const uint32_t* keys, uint32_t nkeys) {
-  for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x) skeys[i] = peer_consts(keys[i]);
+__device__ __forceinline__ void load_keys(uint2* skeys, const uint32_t* keys, uint32_t nkeys,
+                                          uint32_t shift = 0) {
+  for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x) skeys[i + shift] = peer_consts(keys[i]);
   __syncthreads();
+}
+
+// How the vector kernels walk the emulated peers (a template parameter so
+// every variant keeps 16-byte-aligned LDS.128 loads of key pairs):
+//   kSeed1   odd peer count: peer 0 seeds the sums, the rest go in pairs;
+//            keys sit one slot up in shared memory (key q at skeys[q + 1])
+//            so the pairs start on a 16-byte boundary
+//   kSeed2   even peer count: peers 0 and 1 seed the sums, pairs after
+//   kGroups  > 256 byte-kind peers: 256-peer groups, lanes flushed per group
+enum PeerMode { kSeed1 = 0, kSeed2 = 1, kGroups = 2 };
+__host__ __device__ constexpr uint32_t key_shift(int mode) { return mode == kSeed1 ? 1u : 0u; }
+inline int peer_mode(bool words, uint32_t nkeys) {
+  if (!words && nkeys > 256) return kGroups;  // 16-bit lanes hold <= 257 bytes
+  return (nkeys & 1) ? kSeed1 : kSeed2;
 }
 
 template <int DT>
@@ -256,24 +271,65 @@ __device__ __forceinline__ float2 add_f32x2(float a0, float a1, float b0, float 
   return f;
 }
 
+// c1 of every payload word of one thread-tile: word j = j0 + u*kThreads*W + w
+// with j0 = word_base + (tile base + thread) * W.  Within a tile the high
+// half of j almost never changes, so c1 = ((lo*Weyl) ^ (hi*WeylHi)) * M1 is
+// one add and one xor per word off a per-tile base (the M1 multiply folds
+// into the peer loop's first IMAD); a tile straddling 2^32 words takes the
+// general form.
+template <int W, int U>
+__device__ __forceinline__ void tile_ctrs(uint64_t j0, uint32_t* ctr) {
+  constexpr uint32_t kSpan = (U - 1) * kThreads * W + W - 1;
+  const uint32_t lo = static_cast<uint32_t>(j0);
+  if (lo <= 0xFFFFFFFFu - kSpan) {
+    const uint32_t lw = lo * kWeyl;
+    const uint32_t hx = static_cast<uint32_t>(j0 >> 32) * kWeylHi;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        ctr[u * W + w] = ((lw + static_cast<uint32_t>(u * kThreads * W + w) * kWeyl) ^ hx) * kMul1;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(j0 + static_cast<uint64_t>(u) * kThreads * W + w);
+    }
+  }
+}
+
 // Emulated-peer contribution of the U vectors of one thread-tile, as lanes
 // r[] ready for fold_vec:
 //   float kinds  r[4i + e] = float bits of (sum over peers of byte e of
 //                word i, each minus 128) * 2^-7   (exact)
 //   u8           r[4i]     = the four byte sums of word i, mod 256, packed
 //   word kinds   r[i]      = wrapping sum of word i
-// ctr[] holds the hoisted c1 values.
-template <int K, int U, bool kMulti>
+// ctr[] holds the hoisted c1 values; nkeys >= 1 (launchers route 0 peers
+// elsewhere) and, for kSeed2, even.
+template <int K, int U, int kMode>
 __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skeys, uint32_t nkeys,
                                           uint32_t one, uint32_t* r) {
   using T = VT<K>;
   constexpr int NW = U * T::WPV;
+  constexpr bool kMulti = kMode == kGroups;
+  constexpr uint32_t kShift = key_shift(kMode);
+  constexpr uint32_t kSeed = kMode == kSeed1 ? 1 : 2;  // peers folded in before the pair loop
   if constexpr (T::kWords) {
+    {
+      const uint2 k0 = skeys[kShift];
 #pragma unroll
-    for (int i = 0; i < NW; ++i) r[i] = 0;
+      for (int i = 0; i < NW; ++i) r[i] = payload_mix(k0.x, k0.y, ctr[i]);
+      if constexpr (kSeed == 2) {
+        const uint2 k1 = skeys[1];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) r[i] = mad_add(payload_mix(k1.x, k1.y, ctr[i]), one, r[i]);
+      }
+    }
 #pragma unroll 2
-    for (uint32_t q = 0; q < nkeys; ++q) {
-      const uint2 key = skeys[q];
+    for (uint32_t q = kSeed; q < nkeys; ++q) {
+      const uint2 key = skeys[q + kShift];
 #pragma unroll
       for (int i = 0; i < NW; ++i) r[i] = mad_add(payload_mix(key.x, key.y, ctr[i]), one, r[i]);
     }
@@ -288,11 +344,29 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
       const uint32_t q0 = g * 256;
       const uint32_t q1 = kMulti ? min(nkeys, q0 + 256) : nkeys;
       uint32_t a[NW], h[NW];
+      if constexpr (kMulti) {
 #pragma unroll
-      for (int i = 0; i < NW; ++i) a[i] = h[i] = 0;
+        for (int i = 0; i < NW; ++i) a[i] = h[i] = 0;
+      } else {
+        const uint2 k0 = skeys[kShift];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          a[i] = payload_mix(k0.x, k0.y, ctr[i]);
+          h[i] = __byte_perm(a[i], 0u, 0x4341);
+        }
+        if constexpr (kSeed == 2) {
+          const uint2 k1 = skeys[1];
+#pragma unroll
+          for (int i = 0; i < NW; ++i) {
+            const uint32_t w = payload_mix(k1.x, k1.y, ctr[i]);
+            a[i] = mad_add(w, one, a[i]);
+            h[i] = mad_add(__byte_perm(w, 0u, 0x4341), one, h[i]);
+          }
+        }
+      }
 #pragma unroll 2
-      for (uint32_t q = q0; q < q1; ++q) {
-        const uint2 key = skeys[q];
+      for (uint32_t q = kMulti ? q0 : kSeed; q < q1; ++q) {
+        const uint2 key = skeys[q + kShift];
 #pragma unroll
         for (int i = 0; i < NW; ++i) {
           const uint32_t w = payload_mix(key.x, key.y, ctr[i]);
@@ -401,7 +475,7 @@ __device__ __forceinline__ uint4 fold_vec(const uint4& x, const uint32_t* r) {
   return y;
 }
 
-template <int K, int DT, int U, bool kMulti>
+template <int K, int DT, int U, int kMode>
 __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     const uint4* __restrict__ src, uint4* dst, uint64_t nvec, uint64_t word_base,
     const uint32_t* __restrict__ keys, uint32_t nkeys, int64_t* stamp, const void* tail_src,
@@ -410,7 +484,7 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
   constexpr int W = T::WPV, NW = U * W;
   extern __shared__ uint2 skeys[];
   if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
-  load_keys(skeys, keys, nkeys);
+  load_keys(skeys, keys, nkeys, key_shift(kMode));
 
   const uint64_t tile = static_cast<uint64_t>(kThreads) * U;
   for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * tile; base < nvec;
@@ -424,15 +498,10 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
       if (v < nvec) x[u] = ld_stream(src + v);
     }
     uint32_t ctr[NW];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
-#pragma unroll
-      for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(word_base + v * W + w);
-    }
+    tile_ctrs<W, U>(word_base + (base + threadIdx.x) * W, ctr);
     // 2. the emulated peers' sums (registers only), 3. fold + stream out
     uint32_t r[T::kWords ? NW : NW * 4];
-    peer_sums<K, U, kMulti>(ctr, skeys, nkeys, one, r);
+    peer_sums<K, U, kMode>(ctr, skeys, nkeys, one, r);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
@@ -441,7 +510,7 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
   }
   // ragged tail (< one vector): the last block's first threads
   if (ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < ntail) {
-    elem_reduce<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, skeys, nkeys);
+    elem_reduce<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, skeys + key_shift(kMode), nkeys);
   }
 }
 
@@ -554,7 +623,7 @@ __device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* ske
   for (int g = 0; g < a.ndst; ++g) reinterpret_cast<S*>(a.dst[g] + a.v_end)[i] = out;
 }
 
-template <int K, int DT, int KMAX, int U, bool kMulti>
+template <int K, int DT, int KMAX, int U, int kMode>
 __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_constant__ FusedArgs a) {
   using T = VT<K>;
   constexpr int W = T::WPV, NW = U * W;
@@ -570,7 +639,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
     st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(epoch, a.sig));
   }
   if (threadIdx.x == 0) abort_s = 0;
-  load_keys(skeys, a.keys, a.nkeys);
+  load_keys(skeys, a.keys, a.nkeys, key_shift(kMode));
   if (threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
     const int w = wait_flag(a.flags + threadIdx.x, epoch, a.sig, true, t0, a.timeout_ns);
     if (w) {
@@ -600,14 +669,9 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
       }
     }
     uint32_t ctr[NW];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
-#pragma unroll
-      for (int w = 0; w < W; ++w) ctr[u * W + w] = payload_c1(a.word_base + v * W + w);
-    }
+    tile_ctrs<W, U>(a.word_base + (base + threadIdx.x) * W, ctr);
     uint32_t r[T::kWords ? NW : NW * 4];
-    peer_sums<K, U, kMulti>(ctr, skeys, a.nkeys, 1u, r);
+    peer_sums<K, U, kMode>(ctr, skeys, a.nkeys, 1u, r);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
@@ -624,7 +688,9 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
       }
     }
   }
-  if (a.ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < a.ntail) fused_tail_elem<DT>(a, threadIdx.x, skeys);
+  if (a.ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < a.ntail) {
+    fused_tail_elem<DT>(a, threadIdx.x, skeys + key_shift(kMode));
+  }
 
   // done barrier: the last CTA on this GPU publishes and waits
   __threadfence_system();
@@ -941,12 +1007,13 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
   const uint32_t ntail = static_cast<uint32_t>(count - nvec * T::EPV);
   const size_t es = T::kWords ? 4 : (K == kF32 ? 4 : (K == kU8 ? 1 : 2));
   const uint64_t word_base = T::kWords ? elem_base : elem_base / 4;
-  const size_t smem = static_cast<size_t>(nkeys) * 8;
-  const bool multi = !T::kWords && nkeys > 256;  // 16-bit lanes hold <= 257 bytes
-  auto kern = multi ? synth_reduce_vec<K, DT, U, true> : synth_reduce_vec<K, DT, U, false>;
-  static int per_sm[2] = {0, 0};
-  int& occ = per_sm[multi ? 1 : 0];
-  if (!occ) occ = blocks_per_sm(kern, kMaxKeys * 8);
+  const size_t smem = (static_cast<size_t>(nkeys) + 1) * 8;
+  const int mode = peer_mode(T::kWords, nkeys);
+  auto kern = mode == kGroups ? synth_reduce_vec<K, DT, U, kGroups>
+              : mode == kSeed1 ? synth_reduce_vec<K, DT, U, kSeed1> : synth_reduce_vec<K, DT, U, kSeed2>;
+  static int per_sm[3] = {0, 0, 0};
+  int& occ = per_sm[mode];
+  if (!occ) occ = blocks_per_sm(kern, (kMaxKeys + 1) * 8);
   const int bps = bps_req > 0 ? std::min(bps_req, occ) : std::min(occ, 4);
   const uint64_t tiles = (nvec + static_cast<uint64_t>(kThreads) * U - 1) / (static_cast<uint64_t>(kThreads) * U);
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * bps));
@@ -992,8 +1059,9 @@ cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t 
   if (nkeys > kMaxKeys) return cudaErrorInvalidValue;
   if (count == 0) return cudaSuccess;
   ++*launches;
-  // vector path: 16-byte aligned pointers, payload words aligned to vectors
-  const bool al = aligned16(src) && aligned16(dst);
+  // vector path: 16-byte aligned pointers, payload words aligned to vectors,
+  // at least one emulated peer (the vector kernels seed their sums from it)
+  const bool al = aligned16(src) && aligned16(dst) && nkeys > 0;
   const bool word_al = (elem_base % 4) == 0;
   switch (dtype) {
     case cemuFloat32:
@@ -1110,12 +1178,14 @@ int fused_env(const char* name, int dflt) {
 template <int K, int DT, int KMAX, int U>
 cudaError_t fused_ku(const FusedArgs& a, cudaStream_t s) {
   static const int bps = std::max(1, fused_env("CEMU_FUSED_BPS", 4));
-  const bool multi = !VT<K>::kWords && a.nkeys > 256;
-  auto kern = multi ? fused_allreduce_vec<K, DT, KMAX, U, true> : fused_allreduce_vec<K, DT, KMAX, U, false>;
+  const int mode = peer_mode(VT<K>::kWords, a.nkeys);
+  auto kern = mode == kGroups ? fused_allreduce_vec<K, DT, KMAX, U, kGroups>
+              : mode == kSeed1 ? fused_allreduce_vec<K, DT, KMAX, U, kSeed1>
+                               : fused_allreduce_vec<K, DT, KMAX, U, kSeed2>;
   const uint64_t nvec = a.v_end - a.v_begin;
   const uint64_t tiles = (nvec + static_cast<uint64_t>(U) * kThreads - 1) / (static_cast<uint64_t>(U) * kThreads);
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * bps));
-  kern<<<static_cast<unsigned>(grid), kThreads, static_cast<size_t>(a.nkeys) * 8, s>>>(a);
+  kern<<<static_cast<unsigned>(grid), kThreads, (static_cast<size_t>(a.nkeys) + 1) * 8, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1137,7 +1207,7 @@ cudaError_t fused_kind(const FusedArgs& a, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t s, int* launches) {
-  if (a.k < 2 || a.k > kMaxReal || a.nkeys > kMaxKeys) return cudaErrorInvalidValue;
+  if (a.k < 2 || a.k > kMaxReal || a.nkeys == 0 || a.nkeys > kMaxKeys) return cudaErrorInvalidValue;
   ++*launches;
   switch (dtype) {
     case cemuFloat32: return fused_kind<kF32, cemuFloat32>(a, s);
