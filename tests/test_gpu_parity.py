@@ -291,6 +291,31 @@ def test_full_size_sampled_windows_and_linearity(comms, dt):
         assert torch.equal(y - zero, x)
 
 
+@pytest.mark.parametrize("dt", [1, 2])
+def test_payload_word_index_past_2_32(comms, dt):
+    """Maximum sizes: a 16 GiB buffer whose payload word index crosses 2^32
+    (u8: element 2^34; int32: element 2^32), where the hot kernel's per-tile
+    counters take the general (high-word) form.  Windows at the crossing and
+    at both ends equal the oracle bit for bit."""
+    W = 8
+    comm = comms(W)
+    cross = 1 << 34 if dt == 1 else 1 << 32  # first element of payload word 2^32
+    count = cross + (1 << 20) + 5
+    x = torch.zeros(count, dtype=TORCH[dt], device="cuda")
+    comm.all_reduce(x, x)  # in place: x <- the emulated peers' sum
+    torch.cuda.synchronize()
+    keys = [P.payload_key(1, r) for r in range(1, W)]
+    for s in (0, cross - 5000, cross - 3, count - 4099):
+        n = 8192 if s == cross - 5000 else 4096
+        n = min(n, count - s)
+        vs = sum(P.payload(dt, k, s, n).astype(np.uint64) for k in keys)
+        want = (vs % (256 if dt == 1 else 1 << 32)).astype(np.uint8 if dt == 1 else np.uint32)
+        got = to_np(x[s:s + n])
+        assert_bit_equal(got.view(want.dtype), want, f"window {s} (crossing at {cross})")
+    del x
+    torch.cuda.empty_cache()
+
+
 # ---- the reference-facing WorkerSession mirror -------------------------------
 def test_worker_session_mirror_reference_transport_cases(cuda):
     """test_transport.cpp:129-182 through the WorkerSession mirror (zero mode)."""
