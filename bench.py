@@ -61,7 +61,9 @@ def workload(args, n):
             "buffer_bytes_per_gpu": args.mib << 20, "world": RANKS_PER_GPU * n, "real_gpus": n,
             "emulated_ranks": RANKS_PER_GPU * n - n, "dtype": "fp32",
             "l2_policy": "inputs larger than L2 (1 GiB >> 126 MB)",
-            "parallelism": f"{n} real GPU(s), NCCL RS/AG among them + per-GPU synthesis"}
+            "parallelism": (f"{n} real GPU(s): one fused NVLink allreduce + synthesis kernel per step "
+                            "(CEMU_FUSED=0: NCCL RS/AG + per-GPU synthesis)" if n > 1 else
+                            "1 real GPU: one synthesis kernel per step")}
 
 
 # ---------------------------------------------------------------------------
@@ -484,7 +486,9 @@ def run_ours(args, rank, world_size, local_rank):
                     "kernel": ("fused_allreduce_vec<fp32>: P2P pull of every real GPU's shard + synthesis + "
                                "P2P push of the result, one launch per step") if fused else
                               "NCCL reduce-scatter + synth_reduce_vec<fp32> + NCCL allgather",
-                    "peak_source": peak_src}
+                    "peak_source": peak_src,
+                    "note": ("at N > 1 the step is bound by NVLink (2(N-1)/N x buffer per GPU per direction), "
+                             "not HBM: see the `nvlink` object for its roofline fraction")}
 
     # e2e: pinned host buffers in and out every step, through the C-ABI's
     # host-buffer allreduce (WorkerSession's span shape): the library moves
