@@ -196,6 +196,45 @@ struct cemuComm {
   std::unique_ptr<WireSession> wire;
   void* wire_buf = nullptr;  // device staging of one received DATA payload
   size_t wire_buf_bytes = 0;
+
+  // Releases every resource held, in dependency order; also runs when
+  // initialisation fails half way (init_comm owns the comm in a unique_ptr).
+  ~cemuComm() {
+    cudaSetDevice(device);
+    wire.reset();  // BYE to the emulator
+    auto& p = pipe;
+    for (cudaStream_t st : {p.h2d, p.comp, p.d2h}) {
+      if (st) cudaStreamSynchronize(st);
+    }
+    for (int b = 0; b < kPipeBufs; ++b) {
+      if (!p.symmetric && p.buf[b]) cudaFree(p.buf[b]);  // symmetric buffers are regions (below)
+      for (cudaEvent_t ev : {p.loaded[b], p.done[b], p.drained[b]}) {
+        if (ev) cudaEventDestroy(ev);
+      }
+    }
+    if (p.start) cudaEventDestroy(p.start);
+    for (cudaStream_t st : {p.h2d, p.comp, p.d2h}) {
+      if (st) cudaStreamDestroy(st);
+    }
+    for (auto& r : regions) {
+      for (uint32_t g = 0; g < k; ++g) {
+        if (g != li && r.peer[g]) cudaIpcCloseMemHandle(r.peer[g]);
+      }
+      cudaFree(r.base);
+    }
+    for (uint32_t g = 0; g < k && g < static_cast<uint32_t>(kMaxReal); ++g) {
+      if (g != li && peer_sig[g]) cudaIpcCloseMemHandle(peer_sig[g]);
+    }
+    cudaFree(sig);
+    cudaFree(scratch);
+    cudaFree(wire_buf);
+    if (inner) {
+      if (const Nccl* n = nccl()) n->CommDestroy(inner);
+    }
+    cudaFree(d_virt_keys);
+    cudaFree(d_virt_ranks);
+    cudaFree(d_slots);
+  }
 };
 
 namespace {
@@ -806,33 +845,41 @@ cemuResult_t do_broadcast(const void* send, void* recv, size_t count, int dt, in
 cemuResult_t ensure_pipe(cemuComm* c) {
   auto& p = c->pipe;
   if (p.ready) return cemuSuccess;
-  size_t mib = 32;  // measured: 4 MiB 27.3 ms, 16 MiB 24.8, 32 MiB 22.9 per 1 GiB (full-duplex PCIe floor 22.4)
-  if (const char* e = std::getenv("CEMU_HOST_CHUNK_MIB")) mib = std::max(1, std::atoi(e));
-  p.chunk = mib << 20;
-  CUDA_OK(cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking));
-  CUDA_OK(cudaStreamCreateWithFlags(&p.comp, cudaStreamNonBlocking));
-  CUDA_OK(cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking));
-  CUDA_OK(cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming));
+  if (!p.chunk) {
+    size_t mib = 32;  // measured: 4 MiB 27.3 ms, 16 MiB 24.8, 32 MiB 22.9 per 1 GiB (full-duplex PCIe floor 22.4)
+    if (const char* e = std::getenv("CEMU_HOST_CHUNK_MIB")) mib = std::max(1, std::atoi(e));
+    p.chunk = mib << 20;
+  }
+  // (a retry after a failed attempt creates only what is still missing)
+  if (!p.h2d) CUDA_OK(cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking));
+  if (!p.comp) CUDA_OK(cudaStreamCreateWithFlags(&p.comp, cudaStreamNonBlocking));
+  if (!p.d2h) CUDA_OK(cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking));
+  if (!p.start) CUDA_OK(cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming));
   // several real GPUs: the buffers are symmetric (mapped on every real GPU,
   // collective like cemuMemAlloc) so each chunk is one fused kernel
   p.symmetric = c->k > 1;
   for (int b = 0; b < cemuComm::kPipeBufs; ++b) {
-    if (p.symmetric) {
+    if (!p.buf[b] && p.symmetric) {
       const size_t rounded = (p.chunk + (2u << 20) - 1) & ~static_cast<size_t>((2u << 20) - 1);
-      CUDA_OK(cudaMalloc(&p.buf[b], rounded));
+      void* d = nullptr;
+      CUDA_OK(cudaMalloc(&d, rounded));
       cemuComm::Region r;
-      r.base = static_cast<uint8_t*>(p.buf[b]);
+      r.base = static_cast<uint8_t*>(d);
       r.bytes = rounded;
       r.peer[c->li] = r.base;
-      if (auto e = map_peers(c, p.buf[b], rounded, r.peer)) return e;
-      c->regions.push_back(r);
+      if (auto e = map_peers(c, d, rounded, r.peer)) {
+        cudaFree(d);
+        return e;
+      }
+      c->regions.push_back(r);  // owns the allocation from here on
+      p.buf[b] = d;
       for (uint32_t g = 0; g < c->k; ++g) p.peer[b][g] = r.peer[g];
-    } else {
+    } else if (!p.buf[b]) {
       CUDA_OK(cudaMalloc(&p.buf[b], p.chunk));
     }
-    CUDA_OK(cudaEventCreateWithFlags(&p.loaded[b], cudaEventDisableTiming));
-    CUDA_OK(cudaEventCreateWithFlags(&p.done[b], cudaEventDisableTiming));
-    CUDA_OK(cudaEventCreateWithFlags(&p.drained[b], cudaEventDisableTiming));
+    if (!p.loaded[b]) CUDA_OK(cudaEventCreateWithFlags(&p.loaded[b], cudaEventDisableTiming));
+    if (!p.done[b]) CUDA_OK(cudaEventCreateWithFlags(&p.done[b], cudaEventDisableTiming));
+    if (!p.drained[b]) CUDA_OK(cudaEventCreateWithFlags(&p.drained[b], cudaEventDisableTiming));
   }
   p.ready = true;
   return cemuSuccess;
@@ -1221,40 +1268,7 @@ cemuResult_t cemuCommInitAll(cemuComm_t* comms, int ndev, const int* devlist) {
 }
 
 cemuResult_t cemuCommDestroy(cemuComm_t c) {
-  if (!c) return cemuSuccess;
-  cudaSetDevice(c->device);
-  for (auto& r : c->regions) {
-    for (uint32_t g = 0; g < c->k; ++g) {
-      if (g != c->li && r.peer[g]) cudaIpcCloseMemHandle(r.peer[g]);
-    }
-    cudaFree(r.base);
-  }
-  for (uint32_t g = 0; g < c->k; ++g) {
-    if (g != c->li && c->peer_sig[g]) cudaIpcCloseMemHandle(c->peer_sig[g]);
-  }
-  if (c->sig) cudaFree(c->sig);
-  if (c->scratch) cudaFree(c->scratch);
-  if (c->pipe.ready) {
-    auto& p = c->pipe;
-    cudaStreamSynchronize(p.d2h);
-    for (int b = 0; b < cemuComm::kPipeBufs; ++b) {
-      if (!p.symmetric) cudaFree(p.buf[b]);  // symmetric ones are regions, freed above
-      cudaEventDestroy(p.loaded[b]);
-      cudaEventDestroy(p.done[b]);
-      cudaEventDestroy(p.drained[b]);
-    }
-    cudaEventDestroy(p.start);
-    cudaStreamDestroy(p.h2d);
-    cudaStreamDestroy(p.comp);
-    cudaStreamDestroy(p.d2h);
-  }
-  c->wire.reset();  // BYE
-  if (c->wire_buf) cudaFree(c->wire_buf);
-  if (c->inner && nccl()) nccl()->CommDestroy(c->inner);
-  cudaFree(c->d_virt_keys);
-  cudaFree(c->d_virt_ranks);
-  cudaFree(c->d_slots);
-  delete c;
+  delete c;  // ~cemuComm releases everything (null is a no-op, as ncclCommDestroy(NULL))
   return cemuSuccess;
 }
 
