@@ -359,8 +359,13 @@ WireSession::~WireSession() {
       }
     }
     // the BYE sits ahead of the FIN; the emulator answers BYE and closes,
-    // which ends the reader
+    // which ends the reader -- unless it is gone: then, after a grace
+    // period, shutting the read side down wakes the blocked recv
     ::shutdown(fd_, SHUT_WR);
+    std::unique_lock<std::mutex> lk(mu_);
+    if (!cv_.wait_for(lk, std::chrono::seconds(2), [this] { return reader_done_; })) {
+      ::shutdown(fd_, SHUT_RDWR);
+    }
   }
   if (reader_.joinable()) reader_.join();
   if (fd_ >= 0) ::close(fd_);
@@ -382,6 +387,14 @@ void WireSession::fail(const std::string& why) {
 }
 
 void WireSession::reader_main() {
+  struct Done {  // tells the destructor the reader has left, however it leaves
+    WireSession* w;
+    ~Done() {
+      std::lock_guard<std::mutex> lk(w->mu_);
+      w->reader_done_ = true;
+      w->cv_.notify_all();
+    }
+  } done{this};
   try {
     while (true) {
       WireFrame f;

@@ -109,7 +109,7 @@ class WireSession {
   std::mutex mu_;
   std::condition_variable cv_;
   std::deque<WireFrame> inbox_;
-  bool failed_ = false, closing_ = false, eof_ = false;
+  bool failed_ = false, closing_ = false, eof_ = false, reader_done_ = false;
   std::string fail_reason_;
   std::vector<uint8_t> out_;  // staging for outgoing DATA payloads
 };
