@@ -154,3 +154,104 @@ def test_wire_mode_errors_are_loud(cuda):
         with pytest.raises(pb.CemuError, match="config digest mismatch"):
             c2.attach_emulator([pb.CollectivePlanEntry("allreduce", 64, 4)])
         c2.close()
+
+
+# ---- failure paths, against a scripted fake emulator ------------------------
+import json as _json
+import struct
+import threading
+import time
+
+
+def _frame(t, op=0, seq=0, src=0, dst=0, chunk=0, payload=b""):
+    return struct.pack("<4sBBIIHHHI", b"CEMU", 1, t, op, seq, src, dst, chunk, len(payload)) + payload
+
+
+def _read_frame(conn):
+    def exact(n):
+        b = b""
+        while len(b) < n:
+            c = conn.recv(n - len(b))
+            if not c:
+                raise EOFError
+            b += c
+        return b
+    h = exact(24)
+    magic, ver, t, op, seq, src, dst, chunk, n = struct.unpack("<4sBBIIHHHI", h)
+    return t, op, seq, src, dst, chunk, exact(n) if n else b""
+
+
+class FakeEmulator:
+    """Accepts one session, answers the handshake, then follows `script`:
+    "silent" (never answers), "error" (ERROR on OPEN_OP), "bad_chunk"
+    (DATA for the wrong chunk)."""
+
+    def __init__(self, text: str, script: str):
+        pe = int(text.split("endpoint.1 = 127.0.0.1:")[1].split()[0])
+        self.digest = pb.JobConfig.parse(text).digest
+        self.world = pb.JobConfig.parse(text).world_size
+        self.script = script
+        self.sock = socket.socket()
+        self.sock.setsockopt(socket.SOL_SOCKET, socket.SO_REUSEADDR, 1)
+        self.sock.bind(("127.0.0.1", pe))
+        self.sock.listen(1)
+        self.th = threading.Thread(target=self._serve, daemon=True)
+        self.th.start()
+
+    def _serve(self):
+        conn, _ = self.sock.accept()
+        self.conn = conn
+        t, *_ , payload = _read_frame(conn)
+        assert t == 1  # HELLO
+        hello = _json.loads(payload)
+        topo = _json.dumps({"rank": -1, "world_size": self.world, "config_digest": self.digest,
+                            "plan": hello["plan"]}).encode()
+        conn.sendall(_frame(2, payload=topo))
+        try:
+            t, op, seq, *_ = _read_frame(conn)  # OPEN_OP
+            if self.script == "error":
+                conn.sendall(_frame(5, payload=b"injected failure"))
+            elif self.script == "bad_chunk":
+                _read_frame(conn)  # the worker's DATA for position 0
+                conn.sendall(_frame(4, op=op, seq=0, src=self.world - 1, dst=0, chunk=99, payload=b"\0" * 16))
+            while True:  # "silent": swallow everything, answer nothing
+                _read_frame(conn)
+        except (EOFError, OSError):
+            pass
+
+    def close(self):
+        try:
+            self.conn.close()
+        except Exception:
+            pass
+        self.sock.close()
+
+
+@pytest.mark.parametrize("script,match", [("error", "peer reported error: injected failure"),
+                                          ("bad_chunk", "protocol mismatch")])
+def test_wire_peer_errors_surface(cuda, script, match):
+    W = 4
+    text = wire_config(W)
+    fake = FakeEmulator(text, script)
+    comm = pb.Communicator(text, 0, 0)
+    comm.attach_emulator([pb.CollectivePlanEntry("allreduce", 64, 4)])
+    x = torch.zeros(16, dtype=torch.int32, device="cuda")
+    with pytest.raises(pb.CemuError, match=match):
+        comm.all_reduce(x, x)
+    with pytest.raises(pb.CemuError):  # the session stays failed, as the reference's does
+        comm.all_reduce(x, x)
+    comm.close()
+    fake.close()
+
+
+def test_wire_detach_from_a_silent_emulator_is_bounded(cuda):
+    W = 4
+    text = wire_config(W)
+    fake = FakeEmulator(text, "silent")
+    comm = pb.Communicator(text, 0, 0)
+    comm.attach_emulator([pb.CollectivePlanEntry("allreduce", 64, 4)])
+    t0 = time.perf_counter()
+    comm.detach_emulator()  # BYE goes out, no BYE comes back
+    assert time.perf_counter() - t0 < 10
+    comm.close()
+    fake.close()
