@@ -301,6 +301,25 @@ __device__ __forceinline__ void tile_ctrs(uint64_t j0, uint32_t* ctr) {
   }
 }
 
+// One payload word's byte-kind lanes from its single-group accumulators
+// (A, H over n <= 257 peers): u8 -> the packed byte sums mod 256 in r[0];
+// float kinds -> the four exact dyadic deltas (t - 128 n) * 2^-7 in r[0..3].
+template <int K>
+__device__ __forceinline__ void ah_to_lanes(uint32_t a, uint32_t h, uint32_t n, uint32_t* r) {
+  const uint32_t even = even_lanes(a, h);
+  if constexpr (K == kU8) {  // bytes wrap: low byte of each lane
+    r[0] = __byte_perm(even, h, 0x6240);
+  } else {
+    const float c = -(98304.0f + static_cast<float>(n));
+    const float2 d01 = add_f32x2(lane_float(even, 0x7610), lane_float(h, 0x7610), c, c);
+    const float2 d23 = add_f32x2(lane_float(even, 0x7632), lane_float(h, 0x7632), c, c);
+    r[0] = __float_as_uint(d01.x);
+    r[1] = __float_as_uint(d01.y);
+    r[2] = __float_as_uint(d23.x);
+    r[3] = __float_as_uint(d23.y);
+  }
+}
+
 // Emulated-peer contribution of the U vectors of one thread-tile, as lanes
 // r[] ready for fold_vec:
 //   float kinds  r[4i + e] = float bits of (sum over peers of byte e of
@@ -377,20 +396,7 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
       }
       if constexpr (!kMulti) {
 #pragma unroll
-        for (int i = 0; i < NW; ++i) {
-          const uint32_t even = even_lanes(a[i], h[i]);
-          if constexpr (K == kU8) {  // bytes wrap: low byte of each lane
-            r[4 * i] = __byte_perm(even, h[i], 0x6240);
-          } else {
-            const float c = -(98304.0f + static_cast<float>(nkeys));
-            const float2 d01 = add_f32x2(lane_float(even, 0x7610), lane_float(h[i], 0x7610), c, c);
-            const float2 d23 = add_f32x2(lane_float(even, 0x7632), lane_float(h[i], 0x7632), c, c);
-            r[4 * i + 0] = __float_as_uint(d01.x);
-            r[4 * i + 1] = __float_as_uint(d01.y);
-            r[4 * i + 2] = __float_as_uint(d23.x);
-            r[4 * i + 3] = __float_as_uint(d23.y);
-          }
-        }
+        for (int i = 0; i < NW; ++i) ah_to_lanes<K>(a[i], h[i], nkeys, r + 4 * i);
       } else {
         // float kinds carry the -128 offset of the dyadic value; bytes wrap
         const int32_t bias = K == kU8 ? 0 : 128 * static_cast<int32_t>(q1 - q0);
@@ -515,6 +521,68 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
   }
 }
 
+
+// Small buffers: P threads share one vector's peers (peer q goes to lane
+// q mod P), each accumulating A/H (or word sums) over its share; the P
+// partial sums -- plain wrapping adds, so the lane bounds are those of the
+// whole peer set -- are combined with warp shuffles and the group's first
+// lane folds and stores.  Used when one thread per vector would leave most
+// of the machine idle (a 4 KiB call at 63 peers is 8 blocks instead of 1).
+template <int K, int DT, int P>
+__global__ void __launch_bounds__(kThreads) synth_reduce_split(
+    const uint4* __restrict__ src, uint4* dst, uint64_t nvec, uint64_t word_base,
+    const uint32_t* __restrict__ keys, uint32_t nkeys, int64_t* stamp, const void* tail_src,
+    void* tail_dst, uint32_t ntail, uint64_t tail_e0, uint32_t one) {
+  using T = VT<K>;
+  constexpr int W = T::WPV;
+  static_assert(P >= 2 && P <= 32 && (P & (P - 1)) == 0, "P: power of two within a warp");
+  extern __shared__ uint2 skeys[];
+  if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
+  load_keys(skeys, keys, nkeys);
+  const uint32_t part = threadIdx.x % P;
+  const uint64_t v = static_cast<uint64_t>(blockIdx.x) * (kThreads / P) + threadIdx.x / P;
+  const bool live = v < nvec;
+  uint4 x = make_uint4(0, 0, 0, 0);
+  if (live && part == 0) x = ld_stream(src + v);
+  uint32_t ctr[W], a[W], h[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    ctr[w] = payload_c1(word_base + v * W + w);
+    a[w] = h[w] = 0;
+  }
+  for (uint32_t q = part; q < nkeys; q += P) {
+    const uint2 key = skeys[q];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t wv = payload_mix(key.x, key.y, ctr[w]);
+      a[w] = mad_add(wv, one, a[w]);
+      if constexpr (!T::kWords) h[w] = mad_add(__byte_perm(wv, 0u, 0x4341), one, h[w]);
+    }
+  }
+#pragma unroll
+  for (int o = P / 2; o > 0; o >>= 1) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      a[w] += __shfl_xor_sync(0xffffffffu, a[w], o);
+      if constexpr (!T::kWords) h[w] += __shfl_xor_sync(0xffffffffu, h[w], o);
+    }
+  }
+  if (live && part == 0) {
+    uint32_t r[T::kWords ? W : W * 4];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      if constexpr (T::kWords) {
+        r[w] = a[w];
+      } else {
+        ah_to_lanes<K>(a[w], h[w], nkeys, r + 4 * w);
+      }
+    }
+    st_stream(dst + v, fold_vec<K>(x, r));
+  }
+  if (ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < ntail) {
+    elem_reduce<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, skeys, nkeys);
+  }
+}
 
 // ---------------------------------------------------------------------------
 // fused multi-GPU allreduce over peer memory
@@ -1035,10 +1103,56 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
   return cudaGetLastError();
 }
 
+// Peer-split width for a buffer of nvec vectors: 0 = the per-vector kernels.
+// Otherwise the largest power of two P <= 32 with >= 4 peers per thread and
+// nvec * P within half a wave of resident threads.  Byte kinds need the
+// whole peer set in one lane group (<= 256 peers).
+int split_ways(bool words, uint32_t nkeys, uint64_t nvec) {
+  static const int env = [] {
+    const char* e = std::getenv("CEMU_SYNTH_SPLIT");
+    return e ? std::atoi(e) : -1;  // 0 disables, P forces
+  }();
+  if (env == 0 || nvec == 0 || (!words && nkeys > 256)) return 0;
+  if (env > 1) return env;
+  // measured (world 64, graph replay): 4-64 KiB 2.4-3.0 -> 1.6-1.8 us, a tie
+  // at 256 KiB, slower from 1 MiB -- so only up to 64 vectors per SM
+  const uint64_t wave = static_cast<uint64_t>(sm_count()) * 2048;
+  if (nkeys < 8 || nvec > static_cast<uint64_t>(sm_count()) * 64) return 0;
+  int p = 1;
+  while (p < 32 && static_cast<uint32_t>(p) * 8 <= nkeys && nvec * p * 2 <= wave) p *= 2;
+  return p >= 2 ? p : 0;
+}
+
+template <int K, int DT, int P>
+cudaError_t run_split(const void* src, void* dst, uint64_t count, uint64_t elem_base, const uint32_t* keys,
+                      uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
+  using T = VT<K>;
+  const uint64_t nvec = count / T::EPV;
+  const uint32_t ntail = static_cast<uint32_t>(count - nvec * T::EPV);
+  const size_t es = T::kWords ? 4 : (K == kF32 ? 4 : (K == kU8 ? 1 : 2));
+  const uint64_t word_base = T::kWords ? elem_base : elem_base / 4;
+  const uint64_t per_block = kThreads / P;
+  const uint64_t grid = std::max<uint64_t>(1, (nvec + per_block - 1) / per_block);
+  synth_reduce_split<K, DT, P><<<static_cast<unsigned>(grid), kThreads, static_cast<size_t>(nkeys) * 8, s>>>(
+      static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, keys, nkeys, stamp,
+      static_cast<const uint8_t*>(src) + nvec * T::EPV * es, static_cast<uint8_t*>(dst) + nvec * T::EPV * es,
+      ntail, elem_base + nvec * T::EPV, 1u);
+  return cudaGetLastError();
+}
+
 template <int K, int DT>
 cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_base,
                     const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
   constexpr int W = VT<K>::WPV;
+  if (const int P = split_ways(VT<K>::kWords, nkeys, count / VT<K>::EPV)) {
+    switch (P) {
+      case 2: return run_split<K, DT, 2>(src, dst, count, elem_base, keys, nkeys, stamp, s);
+      case 4: return run_split<K, DT, 4>(src, dst, count, elem_base, keys, nkeys, stamp, s);
+      case 8: return run_split<K, DT, 8>(src, dst, count, elem_base, keys, nkeys, stamp, s);
+      case 16: return run_split<K, DT, 16>(src, dst, count, elem_base, keys, nkeys, stamp, s);
+      default: return run_split<K, DT, 32>(src, dst, count, elem_base, keys, nkeys, stamp, s);
+    }
+  }
   const Shape sh = pick_shape(W, nkeys, count / VT<K>::EPV);
   if constexpr (8 / W >= 8) {
     if (sh.u == 8) return run_vec_u<K, DT, 8>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
