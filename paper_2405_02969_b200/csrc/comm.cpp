@@ -473,6 +473,11 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
       keys.push_back(payload_key(c->seed, r));
     }
   }
+  if (c->virt.size() > kMaxEmulatedPeers) {
+    return fail(cemuInvalidArgument, "world_size: " + std::to_string(c->virt.size()) +
+                                         " emulated ranks exceed the " + std::to_string(kMaxEmulatedPeers) +
+                                         " one GPU can synthesise per call");
+  }
   c->cfg = std::move(cfg);
   if (cudaSetDevice(device) != cudaSuccess) return fail(cemuUnhandledCudaError, "cudaSetDevice failed");
   CUDA_OK(cudaMalloc(&c->d_virt_keys, keys.size() * 4));

@@ -36,7 +36,7 @@ namespace cemu_b200 {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr uint32_t kMaxKeys = 4096;  // smem (k1, km) table (32 KB) upper bound
+constexpr uint32_t kMaxKeys = kMaxEmulatedPeers;  // kernels.hpp
 
 __device__ __forceinline__ int64_t globaltimer_ns() {
   uint64_t t;
@@ -1024,6 +1024,14 @@ int sm_count() {
   return cached[dev];
 }
 
+// Opts a kernel into > 48 KB of dynamic shared memory when a large emulated
+// world needs it (the default limit covers 6143 peers).
+template <typename Kern>
+cudaError_t fit_smem(Kern k, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+}
+
 template <typename Kern>
 int blocks_per_sm(Kern k, size_t smem) {
   int b = 0;
@@ -1080,10 +1088,7 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
   const int mode = peer_mode(T::kWords, nkeys);
   auto kern = mode == kGroups ? synth_reduce_vec<K, DT, U, kGroups>
               : mode == kSeed1 ? synth_reduce_vec<K, DT, U, kSeed1> : synth_reduce_vec<K, DT, U, kSeed2>;
-  static int per_sm[3] = {0, 0, 0};
-  int& occ = per_sm[mode];
-  if (!occ) occ = blocks_per_sm(kern, (kMaxKeys + 1) * 8);
-  const int bps = bps_req > 0 ? std::min(bps_req, occ) : std::min(occ, 4);
+  if (const cudaError_t e = fit_smem(kern, smem)) return e;
   const uint64_t tiles = (nvec + static_cast<uint64_t>(kThreads) * U - 1) / (static_cast<uint64_t>(kThreads) * U);
   // One tile per block over the whole buffer (not a persistent grid-stride
   // loop): the hardware block scheduler then sweeps HBM in address order,
@@ -1094,7 +1099,11 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
     const char* e = std::getenv("CEMU_SYNTH_GRID");
     return (e && std::string(e) == "persistent") || std::getenv("CEMU_SYNTH_BPS");
   }();
-  const uint64_t cap = persistent ? static_cast<uint64_t>(sm_count()) * bps : 0x7FFFFFFFull;
+  uint64_t cap = 0x7FFFFFFFull;
+  if (persistent) {
+    const int occ = blocks_per_sm(kern, smem);
+    cap = static_cast<uint64_t>(sm_count()) * (bps_req > 0 ? std::min(bps_req, occ) : std::min(occ, 4));
+  }
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, cap));
   kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(
       static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, keys, nkeys,
@@ -1133,6 +1142,7 @@ cudaError_t run_split(const void* src, void* dst, uint64_t count, uint64_t elem_
   const uint64_t word_base = T::kWords ? elem_base : elem_base / 4;
   const uint64_t per_block = kThreads / P;
   const uint64_t grid = std::max<uint64_t>(1, (nvec + per_block - 1) / per_block);
+  if (const cudaError_t e = fit_smem(synth_reduce_split<K, DT, P>, static_cast<size_t>(nkeys) * 8)) return e;
   synth_reduce_split<K, DT, P><<<static_cast<unsigned>(grid), kThreads, static_cast<size_t>(nkeys) * 8, s>>>(
       static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, keys, nkeys, stamp,
       static_cast<const uint8_t*>(src) + nvec * T::EPV * es, static_cast<uint8_t*>(dst) + nvec * T::EPV * es,
@@ -1169,6 +1179,7 @@ cudaError_t run_scalar(const void* src, void* dst, uint64_t count, uint64_t elem
                        const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
   const uint64_t blocks = std::max<uint64_t>(
       1, std::min<uint64_t>((count + kThreads - 1) / kThreads, static_cast<uint64_t>(sm_count()) * 8));
+  if (const cudaError_t e = fit_smem(synth_reduce_scalar<DT>, static_cast<size_t>(nkeys) * 8)) return e;
   synth_reduce_scalar<DT><<<static_cast<unsigned>(blocks), kThreads, static_cast<size_t>(nkeys) * 8, s>>>(
       src, dst, count, elem_base, keys, nkeys, stamp);
   return cudaGetLastError();
@@ -1313,6 +1324,7 @@ cudaError_t fused_ku(const FusedArgs& a, cudaStream_t s) {
   // persistent: NVLink-bound, and every CTA passes the start barrier (one
   // tile per block measured 1.64 -> 2.10 ms for the 1 GiB k=2 allreduce)
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * bps));
+  if (const cudaError_t e = fit_smem(kern, (static_cast<size_t>(a.nkeys) + 1) * 8)) return e;
   kern<<<static_cast<unsigned>(grid), kThreads, (static_cast<size_t>(a.nkeys) + 1) * 8, s>>>(a);
   return cudaGetLastError();
 }

@@ -15,6 +15,9 @@ namespace cemu_b200 {
 //   [8 .. 8+kmax)            floors_us[j]
 //   [8+kmax .. 8+2kmax)      release_ns[j]   (%globaltimer at release)
 //   [8+2kmax .. 8+3kmax)     offsets_us[j]   (double bits)
+// Emulated peers one call can synthesise (the kernels' shared-memory key
+// table: 8 B per peer, up to the 227 KB a block can opt into).
+constexpr uint32_t kMaxEmulatedPeers = 28 * 1024;
 constexpr int kSlotHeader = 8;
 inline size_t slot_words(uint32_t kmax) { return kSlotHeader + 3 * static_cast<size_t>(kmax); }
 

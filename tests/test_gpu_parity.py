@@ -112,6 +112,30 @@ def test_float_fold_ieee_edge_cases(comms, W, dt):
     assert_bit_equal(got[keep], want[keep], f"edge cases W={W} dt={dt}")
 
 
+@pytest.mark.parametrize("W", [4097, 20000])
+def test_very_large_emulated_worlds(comms, W):
+    """Beyond 6143 emulated peers the key table needs > 48 KB of shared
+    memory (opted into per kernel); allreduce and allgather stay bit-exact."""
+    comm = comms(W)
+    for dt in (7, 9, 2):
+        count = 1000 + 3
+        h = host_input(dt, count, seed=W + dt)
+        want = P.allreduce(dt, P.PAYLOAD_HASH, W, [0], 0, 1, [to_np(h)], count)
+        assert_bit_equal(_allreduce(comm, h, inplace=False), want, f"W={W} dt={dt}")
+    sc = 40
+    h = host_input(7, sc, seed=1)
+    recv = torch.empty(sc * W, dtype=torch.float32, device="cuda")
+    comm.all_gather(h.cuda(), recv)
+    torch.cuda.synchronize()
+    want = P.allgather(7, P.PAYLOAD_HASH, W, [0], 0, 1, [to_np(h)], sc)
+    assert_bit_equal(to_np(recv), want, f"allgather W={W}")
+
+
+def test_world_beyond_the_key_table_fails_at_init(cuda):
+    with pytest.raises(pb.CemuError, match="emulated ranks exceed"):
+        pb.Communicator(config(30000), 0, 0)
+
+
 def test_real_rank_not_zero_and_other_seed(comms):
     comm = comms(16, seed=0xBEEF, real=(5,), rank=5)
     for dt in (7, 2):
