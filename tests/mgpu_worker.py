@@ -50,15 +50,17 @@ def run():
         dist.broadcast_object_list(obj, src=0)
         cfg = f"world_size = {W}\nreal_ranks = {','.join(map(str, real))}\nbucket_bytes = 1\n"
         comm = pb.Communicator(cfg, me, local, obj[0])
-        for dt in (7, 9, 2):
+        for dt in (7, 9, 2, 4, 8):
             for count in (1, n * 1000 + 3, (1 << 20) + 7):
                 trace(f"real={real} dt={dt} count={count}")
                 sends = []
                 for i in range(n):
                     g = np.random.default_rng(1000 * i + count)
-                    if dt in (7, 9):  # dyadic, <= 5 significant bits: the real sum of <= 8
+                    if dt in (7, 9, 8):  # dyadic, <= 5 significant bits: the real sum of <= 8
                         # values is exact even in bf16, so NCCL's fold order cannot matter
                         v = torch.from_numpy((g.integers(-16, 16, size=count) / 8).astype(np.float32)).to(TORCH[dt])
+                    elif dt == 4:
+                        v = torch.from_numpy(g.integers(-2**62, 2**62, size=count).astype(np.int64))
                     else:
                         v = torch.from_numpy(g.integers(-2**31, 2**31, size=count).astype(np.int32))
                     sends.append(v)
