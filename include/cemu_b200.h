@@ -182,6 +182,23 @@ typedef struct {
   int64_t device_latency_us; /* max_j floor_j as evaluated on the device */
 } cemuCallRecord;
 
+/* Delay-model plugin: replaces DelayModelFn / make_delay_model
+ * (proj/include/cemu/delay.hpp:52-55, src/delay.cpp:49-53).  The reference's
+ * plugin maps (boundary DAG, bytes) to the per-step release offsets; the
+ * boundary is closed-form here, so the function receives the collective
+ * (0 allreduce, 1 allgather, 2 reduce-scatter, 3 broadcast), the world size,
+ * the model bytes and K = the number of to-real steps, and writes K offsets
+ * in microseconds from the call's start into offsetsUs (return 0, or
+ * non-zero to fail the call with cemuInvalidArgument).  It runs on the host
+ * when the call is enqueued; floors = llround(offset) and the head-of-line
+ * release are applied on the device exactly as for the built-in models
+ * (engine.cpp:36-70).  Setting it activates delay injection on every call;
+ * NULL restores the job config's model.  (In a captured CUDA graph the
+ * offsets are those of the capture.) */
+typedef int (*cemuDelayModelFn)(int coll, uint32_t worldSize, uint64_t bytes, uint32_t k,
+                                double* offsetsUs, void* user);
+cemuResult_t cemuCommSetDelayModel(cemuComm_t comm, cemuDelayModelFn fn, void* user);
+
 cemuResult_t cemuCommLastCallId(cemuComm_t comm, uint64_t* callId);
 /* Copies the record (and up to `cap` floors / release times / offsets) of a
  * call still held in the comm's record ring. Synchronous device read. */

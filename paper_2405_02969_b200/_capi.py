@@ -43,6 +43,11 @@ class ShardPlan(C.Structure):
                 ("tailOffset", C.c_uint64), ("tailCount", C.c_uint64)]
 
 
+# int (*)(int coll, uint32 world, uint64 bytes, uint32 k, double* offsets, void* user)
+DELAY_MODEL_FN = C.CFUNCTYPE(C.c_int, C.c_int, C.c_uint32, C.c_uint64, C.c_uint32, C.POINTER(C.c_double),
+                             C.c_void_p)
+
+
 class PlanEntry(C.Structure):
     _fields_ = [("coll", C.c_int32), ("bytes", C.c_uint64), ("elemSize", C.c_uint32)]
 
@@ -113,6 +118,7 @@ def _load():
         "cemuPlanShards": (None, [u64, u32, u32, C.POINTER(ShardPlan)]),
         "cemuPayloadKey": (u32, [u64, u32]),
         "cemuPayloadWord": (u32, [u32, u64]),
+        "cemuCommSetDelayModel": (i32, [vp, DELAY_MODEL_FN, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -203,6 +203,30 @@ class Communicator:
                                     self._h, _stream_ptr(stream)), self._h)
         return recv
 
+    # -- delay-model plugin (DelayModelFn, proj/include/cemu/delay.hpp:52-55) --
+    def set_delay_model(self, fn) -> None:
+        """fn(coll, world_size, bytes, k) -> k release offsets (us from the
+        call's start), evaluated on the host when each call is enqueued; the
+        device applies llround floors and the head-of-line release.  None
+        restores the job config's model."""
+        if fn is None:
+            check(lib.cemuCommSetDelayModel(self._h, _capi.DELAY_MODEL_FN(), None), self._h)
+            self._delay_cb = None
+            return
+
+        def cb(coll, n, nbytes, k, out, _user):
+            try:
+                vals = list(fn(coll, n, nbytes, k))
+                if len(vals) != k:
+                    return 2
+                for j, v in enumerate(vals):
+                    out[j] = float(v)
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a failed plugin call
+                return 1
+        self._delay_cb = _capi.DELAY_MODEL_FN(cb)  # kept alive with the communicator
+        check(lib.cemuCommSetDelayModel(self._h, self._delay_cb, None), self._h)
+
     # -- wire mode (interop with a reference cemu-emulator) -------------------
     def attach_emulator(self, plan: list, timeout_ms: int = 10000) -> None:
         """cemuCommAttachEmulator: dial the config's emulator endpoint and

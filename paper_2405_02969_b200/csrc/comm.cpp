@@ -143,6 +143,13 @@ struct cemuComm {
   bool contiguous = true;      // real ranks form one block [real[0], real[0]+k)
   cemuDelayModel delay{};
   bool delay_active = false;
+  // delay-model plugin (cemuCommSetDelayModel): offsets per call from the
+  // user's function, staged through pinned memory into the record slot
+  cemuDelayModelFn delay_fn = nullptr;
+  void* delay_user = nullptr;
+  bool config_delay_active = false;
+  double* h_offsets = nullptr;            // pinned, kSlots x kmax
+  cudaEvent_t offsets_copied[64] = {};    // per slot: the staging may be rewritten
   uint64_t seed = 1;
   PayloadMode mode = PayloadMode::kHash;
   std::vector<uint32_t> virt;  // emulated ranks, ascending
@@ -231,6 +238,10 @@ struct cemuComm {
     if (inner) {
       if (const Nccl* n = nccl()) n->CommDestroy(inner);
     }
+    for (cudaEvent_t ev : offsets_copied) {
+      if (ev) cudaEventDestroy(ev);
+    }
+    if (h_offsets) cudaFreeHost(h_offsets);
     cudaFree(d_virt_keys);
     cudaFree(d_virt_ranks);
     cudaFree(d_slots);
@@ -247,6 +258,8 @@ struct Call {
   cudaStream_t s;
 
   uint32_t i = 0;  // record slot of this call
+  std::vector<double> plugin;  // a delay-model plugin's offsets for this call
+  std::string error;           // set when the plugin failed: the call must not run
 
   Call(cemuComm* comm, int coll, uint64_t model_bytes, cudaStream_t stream) : c(comm), s(stream) {
     const uint64_t id = c->calls++;
@@ -257,7 +270,20 @@ struct Call {
     m.delay = c->delay_active;
     m.k = to_real_count(coll, c->W, c->real);
     m.bytes = model_bytes;
-    m.latency = c->delay_active ? call_latency_us(c->delay, coll, c->W, model_bytes, m.k) : 0;
+    if (c->delay_fn) {
+      // DelayModelFn(boundary, bytes) -> offsets (delay.hpp:52-55): the
+      // boundary is closed-form here, so the plugin sees (coll, n, bytes, K)
+      plugin.assign(m.k, 0.0);
+      const int rc = c->delay_fn(coll, c->W, model_bytes, m.k, plugin.data(), c->delay_user);
+      if (rc != 0) {
+        error = "delay model plugin returned " + std::to_string(rc) + " for call " + std::to_string(id);
+      }
+      int64_t lat = 0;
+      for (double o : plugin) lat = std::max<int64_t>(lat, std::llround(o));
+      m.latency = lat;
+    } else {
+      m.latency = c->delay_active ? call_latency_us(c->delay, coll, c->W, model_bytes, m.k) : 0;
+    }
     if (c->delay_active) slot = c->d_slots + i * slot_words(c->kmax);
   }
   // pointer the first kernel of the call writes t_start into (or null)
@@ -283,6 +309,26 @@ struct Call {
     d.k = m.k;
     d.kmax = c->kmax;
     d.self_stamp = stamped ? 0 : 1;
+    d.preloaded = 0;
+    if (!plugin.empty()) {
+      // stage the plugin's offsets into the slot's offsets region, in stream
+      // order; the pinned staging of slot i is reused 64 calls later
+      cudaEvent_t& ev = c->offsets_copied[i];
+      if (!ev) {
+        if (const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) return e;
+      } else if (const cudaError_t e = cudaEventSynchronize(ev)) {
+        return e;
+      }
+      double* h = c->h_offsets + static_cast<size_t>(i) * c->kmax;
+      std::memcpy(h, plugin.data(), plugin.size() * sizeof(double));
+      auto* dev_offs = reinterpret_cast<double*>(slot + kSlotHeader + 2 * static_cast<size_t>(c->kmax));
+      if (const cudaError_t e = cudaMemcpyAsync(dev_offs, h, plugin.size() * sizeof(double),
+                                                cudaMemcpyHostToDevice, s)) {
+        return e;
+      }
+      if (const cudaError_t e = cudaEventRecord(ev, s)) return e;
+      d.preloaded = 1;
+    }
     int l = 0;
     const cudaError_t e = launch_delay_spin(d, slot, s, &l);
     c->launches += l;
@@ -461,6 +507,7 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
   c->delay.intra_alpha_us = cfg.intra_alpha_us;
   c->delay.intra_beta_us_per_byte = cfg.intra_beta_us_per_byte;
   c->delay_active = cfg.delay_kind != DelayKind::kNone || cfg.delay_inject_us != 0.0;
+  c->config_delay_active = c->delay_active;
   if (c->mode == PayloadMode::kZero && c->k != 1) {
     return fail(cemuInvalidUsage,
                 "payload.mode: zero reproduces the reference emulator, which serves exactly "
@@ -550,6 +597,7 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   const size_t es = dtype_size(dt);
   if (count == 0) return cemuSuccess;
   auto call = std::make_shared<Call>(c, kAllReduce, count * es, s);
+  if (!call->error.empty()) return fail(cemuInvalidArgument, call->error);
   const auto* nv = c->d_virt_keys;
   const uint32_t nk = static_cast<uint32_t>(c->virt.size());
   if (c->mode == PayloadMode::kZero) ph.push_back([=]() -> cemuResult_t {
@@ -643,6 +691,7 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
   const size_t es = dtype_size(dt);
   if (sc == 0) return cemuSuccess;
   auto call = std::make_shared<Call>(c, kAllGather, sc * es, s);
+  if (!call->error.empty()) return fail(cemuInvalidArgument, call->error);
   auto* r8 = static_cast<uint8_t*>(recv);
   const uint32_t nvirt = static_cast<uint32_t>(c->virt.size());
   const bool own_in_place = send == r8 + static_cast<uint64_t>(c->rank) * sc * es;
@@ -720,6 +769,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
   const size_t es = dtype_size(dt);
   if (rc == 0) return cemuSuccess;
   auto call = std::make_shared<Call>(c, kReduceScatter, rc * es * c->W, s);
+  if (!call->error.empty()) return fail(cemuInvalidArgument, call->error);
   const auto* s8 = static_cast<const uint8_t*>(send);
   const uint64_t mine = static_cast<uint64_t>(c->rank) * rc;
   if (c->mode == PayloadMode::kZero) {
@@ -813,6 +863,7 @@ cemuResult_t do_broadcast(const void* send, void* recv, size_t count, int dt, in
   }
   if (count == 0) return cemuSuccess;
   auto call = std::make_shared<Call>(c, kBroadcast, count * es, s);
+  if (!call->error.empty()) return fail(cemuInvalidArgument, call->error);
   const uint32_t r = static_cast<uint32_t>(root);
   ph.push_back([=]() -> cemuResult_t {
   if (c->cfg.is_real(r)) {
@@ -960,6 +1011,7 @@ cemuResult_t host_allreduce(const void* send, void* recv, size_t count, int dt, 
   }
   if (auto r = ensure_pipe(c)) return r;
   auto call = std::make_shared<Call>(c, kAllReduce, bytes, s);
+  if (!call->error.empty()) return fail(cemuInvalidArgument, call->error);
   CUDA_OK(call->stamp_now());
   const uint64_t per = c->pipe.chunk / es;  // elements per chunk: a multiple of 4 (payload words)
   std::vector<PipeChunk> chunks;
@@ -1007,6 +1059,7 @@ cemuResult_t host_allgather(const void* send, void* recv, size_t sc, int dt, cem
   }
   if (auto r = ensure_pipe(c)) return r;
   auto call = std::make_shared<Call>(c, kAllGather, blk, s);
+  if (!call->error.empty()) return fail(cemuInvalidArgument, call->error);
   CUDA_OK(call->stamp_now());
   // the own block (collective.cpp:289-291: in place it is already there)
   if (send != r8 + c->rank * blk) {
@@ -1521,7 +1574,30 @@ cemuResult_t cemuCommGetAsyncError(cemuComm_t c, cemuResult_t* err) {
 
 cemuResult_t cemuCommModelLatencyUs(cemuComm_t c, int coll, uint64_t bytes, int64_t* out) {
   if (!c || !out || coll < 0 || coll > 3) return fail(cemuInvalidArgument, "cemuCommModelLatencyUs: bad argument");
-  *out = c->delay_active ? call_latency_us(c->delay, coll, c->W, bytes, to_real_count(coll, c->W, c->real)) : 0;
+  const uint32_t k = to_real_count(coll, c->W, c->real);
+  if (c->delay_fn) {
+    std::vector<double> offs(k, 0.0);
+    if (const int rc = c->delay_fn(coll, c->W, bytes, k, offs.data(), c->delay_user)) {
+      return fail(cemuInvalidArgument, "delay model plugin returned " + std::to_string(rc));
+    }
+    int64_t lat = 0;
+    for (double o : offs) lat = std::max<int64_t>(lat, std::llround(o));
+    *out = lat;
+    return cemuSuccess;
+  }
+  *out = c->delay_active ? call_latency_us(c->delay, coll, c->W, bytes, k) : 0;
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommSetDelayModel(cemuComm_t c, cemuDelayModelFn fn, void* user) {
+  if (!c) return fail(cemuInvalidArgument, "cemuCommSetDelayModel: comm is null");
+  if (fn && !c->h_offsets) {
+    if (cudaSetDevice(c->device) != cudaSuccess) return fail(cemuUnhandledCudaError, "cudaSetDevice");
+    CUDA_OK(cudaMallocHost(&c->h_offsets, static_cast<size_t>(cemuComm::kSlots) * c->kmax * sizeof(double)));
+  }
+  c->delay_fn = fn;
+  c->delay_user = user;
+  c->delay_active = fn ? true : c->config_delay_active;
   return cemuSuccess;
 }
 

@@ -980,10 +980,11 @@ __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int
     if (d.self_stamp) slot[0] = t0_s;
   }
   // Evaluate the model on the device: delay.cpp:23-47 offsets and
-  // engine.cpp:41 llround floors, strided over the block.
-  const double total = d.model.kind == 1 ? model_total_us(d.model, d.coll, d.n, d.bytes) : 0.0;
+  // engine.cpp:41 llround floors, strided over the block.  A delay-model
+  // plugin's offsets (DelayModelFn, delay.hpp:52-55) arrive preloaded.
+  const double total = (!d.preloaded && d.model.kind == 1) ? model_total_us(d.model, d.coll, d.n, d.bytes) : 0.0;
   for (uint32_t j = threadIdx.x; j < d.k; j += blockDim.x) {
-    const double o = release_offset_us(d.model, total, j, d.k);
+    const double o = d.preloaded ? offs[j] : release_offset_us(d.model, total, j, d.k);
     offs[j] = o;
     floors[j] = llround(o);
   }

@@ -29,6 +29,7 @@ struct DelayLaunch {
   uint32_t k;
   uint32_t kmax;
   int32_t self_stamp;  // 1: this kernel records t_start itself
+  int32_t preloaded;   // 1: the K offsets are already in the slot (a delay-model plugin's)
 };
 
 // dst[i] = src[i] (+) sum over `nkeys` emulated peers of their payload at

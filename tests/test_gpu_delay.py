@@ -217,3 +217,59 @@ def test_event_log_matches_reference_emulator_trace(cuda):
             t = [int(ln.split()[0]) for ln in lines if ln.split()[3] == d]
             assert t == sorted(t)
         comm.close()
+
+
+# ---- the delay-model plugin (DelayModelFn, delay.hpp:52-55) ------------------
+def test_plugin_reproducing_the_builtin_model_gives_identical_floors(cuda):
+    """A plugin that returns the built-in alpha-beta offsets (the host's
+    release_offsets, bit-identical to delay.cpp) yields the same device
+    floors, latency and release schedule as the built-in model."""
+    W, nbytes = 8, 64 << 10
+    text = delay_config(W, 1, a=10.0, b=0.001, g=0.0001)
+    builtin = pb.Communicator(text, 0, 0)
+    ref = run_coll(builtin, 0, nbytes // 4)
+    builtin.close()
+    m = pb.schedule.delay_model(1, 0, 10.0, 0.001, 0.0001, 0.0, 0.0)
+    comm = pb.Communicator(config(W), 0, 0)  # no delay in the config: the plugin turns it on
+    comm.set_delay_model(lambda coll, n, b, k: pb.schedule.release_offsets(m, coll, n, b, k))
+    rec = run_coll(comm, 0, nbytes // 4)
+    assert rec["delay_active"] and rec["steps"] == ref["steps"]
+    assert rec["floors_us"].tolist() == ref["floors_us"].tolist()
+    assert rec["offsets_us"].view(np.uint64).tolist() == ref["offsets_us"].view(np.uint64).tolist()
+    assert rec["model_latency_us"] == ref["model_latency_us"] == rec["device_latency_us"]
+    comm.close()
+
+
+@pytest.mark.parametrize("coll", [0, 1, 2, 3])
+def test_custom_plugin_schedule_is_released_on_the_device(cuda, coll):
+    W = 4
+    comm = pb.Communicator(config(W), 0, 0)
+    seen = []
+
+    def step_model(c, n, nbytes, k):  # 300 us per step, the last one held to 2 ms
+        seen.append((c, n, nbytes, k))
+        return [300.0 * (j + 1) for j in range(k - 1)] + [2000.0]
+    comm.set_delay_model(step_model)
+    rec = run_coll(comm, coll, 4096)
+    k = rec["steps"]
+    assert seen[-1][0] == coll and seen[-1][1] == W and seen[-1][3] == k
+    want = [300 * (j + 1) for j in range(k - 1)] + [2000]
+    assert rec["floors_us"].tolist() == want
+    assert rec["model_latency_us"] == max(want) == rec["device_latency_us"]
+    rel = (rec["release_ns"] - rec["t_start_ns"]) / 1e3
+    assert np.all(rel >= np.array(want) - 0.05) and np.all(rel <= np.array(want) + 20), rel
+    assert abs((rec["t_end_ns"] - rec["t_start_ns"]) / 1e3 - max(want)) <= max(0.01 * max(want), 2.0)
+    comm.close()
+
+
+def test_plugin_failure_is_loud_and_none_restores_the_config(cuda):
+    comm = pb.Communicator(config(4), 0, 0)
+    comm.set_delay_model(lambda c, n, b, k: [1.0] * (k + 1))  # wrong length
+    x = torch.zeros(64, device="cuda")
+    with pytest.raises(pb.CemuError, match="delay model plugin returned"):
+        comm.all_reduce(x, x)
+    comm.set_delay_model(None)
+    comm.all_reduce(x, x)
+    torch.cuda.synchronize()
+    assert not comm.call_record()["delay_active"]  # the config has no delay
+    comm.close()
