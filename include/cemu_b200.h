@@ -230,6 +230,23 @@ uint32_t cemuConfigWorldSize(cemuJobConfig_t cfg);
 /* Writes up to cap real ranks (ascending); returns how many there are. */
 uint32_t cemuConfigRealRanks(cemuJobConfig_t cfg, uint32_t* out, size_t cap);
 
+/* synthesize_global_topology (config.cpp:314-331): one node per rank (its
+ * node class and whether it is real) and a ring of edges r -> r+1 mod n, each
+ * carrying the job's link; the edge structure depends on the world size
+ * alone.  Writes up to cap nodes and edges; returns world_size. */
+typedef struct {
+  int32_t isReal;
+  char nodeClass[64]; /* NUL-terminated, truncated to 63 bytes */
+} cemuTopoNode;
+typedef struct {
+  uint32_t src, dst;
+  double alphaUs, betaUsPerByte, gammaUsPerByte;
+} cemuTopoEdge;
+uint32_t cemuConfigTopology(cemuJobConfig_t cfg, cemuTopoNode* nodes, cemuTopoEdge* edges, size_t cap);
+/* RingOrder (config.cpp:360-376): ascending ring. */
+uint32_t cemuRingSuccessor(uint32_t n, uint32_t rank);
+uint32_t cemuRingPredecessor(uint32_t n, uint32_t rank);
+
 /* ------------------------------------------------------------------ */
 /* Schedule + delay model (pure host functions, for parity checks)      */
 /* ------------------------------------------------------------------ */

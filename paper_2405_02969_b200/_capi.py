@@ -48,6 +48,15 @@ DELAY_MODEL_FN = C.CFUNCTYPE(C.c_int, C.c_int, C.c_uint32, C.c_uint64, C.c_uint3
                              C.c_void_p)
 
 
+class TopoNode(C.Structure):
+    _fields_ = [("isReal", C.c_int32), ("nodeClass", C.c_char * 64)]
+
+
+class TopoEdge(C.Structure):
+    _fields_ = [("src", C.c_uint32), ("dst", C.c_uint32), ("alphaUs", C.c_double),
+                ("betaUsPerByte", C.c_double), ("gammaUsPerByte", C.c_double)]
+
+
 class PlanEntry(C.Structure):
     _fields_ = [("coll", C.c_int32), ("bytes", C.c_uint64), ("elemSize", C.c_uint32)]
 
@@ -119,6 +128,9 @@ def _load():
         "cemuPayloadKey": (u32, [u64, u32]),
         "cemuPayloadWord": (u32, [u32, u64]),
         "cemuCommSetDelayModel": (i32, [vp, DELAY_MODEL_FN, vp]),
+        "cemuConfigTopology": (u32, [vp, C.POINTER(TopoNode), C.POINTER(TopoEdge), sz]),
+        "cemuRingSuccessor": (u32, [u32, u32]),
+        "cemuRingPredecessor": (u32, [u32, u32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

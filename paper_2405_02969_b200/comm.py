@@ -91,6 +91,16 @@ class JobConfig:
         lib.cemuConfigRealRanks(self._h, arr, n)
         return list(arr[:n])
 
+    def topology(self):
+        """synthesize_global_topology (config.cpp:314-331): (nodes, edges),
+        nodes = [(is_real, node_class)], edges = [(src, dst, alpha, beta, gamma)]."""
+        n = lib.cemuConfigTopology(self._h, None, None, 0)
+        nodes = (_capi.TopoNode * max(n, 1))()
+        edges = (_capi.TopoEdge * max(n, 1))()
+        lib.cemuConfigTopology(self._h, nodes, edges, n)
+        return ([(bool(v.isReal), v.nodeClass.decode()) for v in nodes[:n]],
+                [(e.src, e.dst, e.alphaUs, e.betaUsPerByte, e.gammaUsPerByte) for e in edges[:n]])
+
     def __del__(self):
         if getattr(self, "_h", None):
             lib.cemuConfigFree(self._h)

@@ -83,6 +83,31 @@ uint32_t cemuConfigRealRanks(cemuJobConfig_t cfg, uint32_t* out, size_t cap) {
   return static_cast<uint32_t>(i);
 }
 
+uint32_t cemuConfigTopology(cemuJobConfig_t cfg, cemuTopoNode* nodes, cemuTopoEdge* edges, size_t cap) {
+  if (!cfg) return 0;
+  const JobConfig& c = cfg->cfg;
+  for (uint32_t r = 0; r < c.world_size && r < cap; ++r) {
+    if (nodes) {
+      nodes[r].isReal = c.is_real(r) ? 1 : 0;
+      const std::string& nc = c.node_class[r];
+      const size_t n = std::min<size_t>(nc.size(), sizeof nodes[r].nodeClass - 1);
+      std::memcpy(nodes[r].nodeClass, nc.data(), n);
+      nodes[r].nodeClass[n] = '\0';
+    }
+    if (edges) {
+      edges[r].src = r;
+      edges[r].dst = (r + 1) % c.world_size;
+      edges[r].alphaUs = c.link.alpha_us;
+      edges[r].betaUsPerByte = c.link.beta_us_per_byte;
+      edges[r].gammaUsPerByte = c.link.gamma_us_per_byte;
+    }
+  }
+  return c.world_size;
+}
+
+uint32_t cemuRingSuccessor(uint32_t n, uint32_t rank) { return n ? (rank + 1) % n : 0; }
+uint32_t cemuRingPredecessor(uint32_t n, uint32_t rank) { return n ? (rank + n - 1) % n : 0; }
+
 uint64_t cemuChunkBytes(uint32_t n, uint64_t total, uint32_t elem, uint32_t chunk) {
   return chunk_bytes(n, total, elem, chunk);
 }

@@ -163,3 +163,40 @@ def test_host_payload_equals_oracle():
         assert S.payload_word(key, j) == word
     for seed, rank, key in golden("payload.json")["keys"]:
         assert S.payload_key(seed, rank) == key
+
+
+# ---- topology + ring order (config.cpp:314-376; test_config.cpp:120-165) -------
+def _connected(n, edges):
+    adj = {i: set() for i in range(n)}
+    for s, d, *_ in edges:
+        adj[s].add(d)
+        adj[d].add(s)
+    seen, stack = {0}, [0]
+    while stack:
+        for v in adj[stack.pop()] - seen:
+            seen.add(v)
+            stack.append(v)
+    return len(seen) == n
+
+
+def test_topology_covers_every_rank_and_stays_connected():
+    cfg = pb.JobConfig.parse("world_size = 4\nreal_ranks = 0\nbucket_bytes = 8\nlink.alpha_us = 3\n")
+    nodes, edges = cfg.topology()
+    assert len(nodes) == 4 and [r for r, _ in nodes] == [True, False, False, False]
+    assert all(nc == "default" for _, nc in nodes)
+    assert _connected(4, edges) and all(e[2] == 3.0 for e in edges)
+
+
+def test_topology_edge_structure_ignores_which_ranks_are_real():
+    a = pb.JobConfig.parse("world_size = 8\nreal_ranks = 0\nbucket_bytes = 8\n").topology()[1]
+    b = pb.JobConfig.parse("world_size = 8\nreal_ranks = 0,3,5\nbucket_bytes = 8\n").topology()[1]
+    assert [(s, d) for s, d, *_ in a] == [(s, d) for s, d, *_ in b]
+    assert _connected(8, a)
+
+
+def test_ring_order_is_ascending_and_involutive():
+    L = _capi.lib
+    assert L.cemuRingSuccessor(4, 0) == 1 and L.cemuRingSuccessor(4, 3) == 0 and L.cemuRingPredecessor(4, 0) == 3
+    for r in range(4):
+        assert L.cemuRingSuccessor(4, L.cemuRingPredecessor(4, r)) == r
+    assert L.cemuRingSuccessor(2, 0) == 1 and L.cemuRingSuccessor(2, 1) == 0
