@@ -125,6 +125,48 @@ def run_loop(comm, spec: ModelSpec, bucket_bytes: int):
             "issue_us": issue.reshape(iters, -1)[:, :nb], "complete_us": done.reshape(iters, -1)[:, :nb]}
 
 
+TRACE_COLUMNS = ["iter", "start_us", "end_us", "bucket_id", "issue_us", "complete_us"]
+
+
+def write_iteration_csv(path: str, trace: dict) -> None:
+    """One row per (iteration, bucket) with the reference's columns
+    (harness.cpp:256-271); times are device-event microseconds from the
+    loop's first event, rounded to whole microseconds as the reference's
+    integer clock is."""
+    import csv
+    with open(path, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(TRACE_COLUMNS)
+        for it in range(len(trace["start_us"])):
+            for b in range(trace["issue_us"].shape[1]):
+                w.writerow([it, round(float(trace["start_us"][it])), round(float(trace["end_us"][it])), b,
+                            round(float(trace["issue_us"][it, b])), round(float(trace["complete_us"][it, b]))])
+
+
+def read_iteration_csv(path: str) -> dict:
+    """read_iteration_csv (harness.cpp:273-303): the rows back, by iteration."""
+    import csv
+    rows = {}
+    with open(path) as f:
+        lines = [l for l in f if l.strip() and not l.startswith("#")]
+    r = csv.reader(lines[1:])
+    for cols in r:
+        if len(cols) != 6:
+            raise ValueError(f"bad trace csv row: {','.join(cols)}")
+        it, s, e, b, iu, cu = (int(c) for c in cols)
+        t = rows.setdefault(it, {"start_us": s, "end_us": e, "buckets": []})
+        t["buckets"].append((b, iu, cu))
+    return rows
+
+
+def iteration_stats(trace: dict, warmup: int) -> dict:
+    """iteration_stats (harness.cpp:305-319): count, mean and sample stddev
+    of the iteration times after `warmup` iterations."""
+    xs = np.asarray(trace["iter_us"])[warmup:]
+    return {"count": int(len(xs)), "mean_us": float(np.mean(xs)) if len(xs) else 0.0,
+            "stddev_us": float(np.std(xs, ddof=1)) if len(xs) > 1 else 0.0}
+
+
 def predicted_us(comm, spec: ModelSpec, bucket_bytes: int) -> float:
     lats = []
     for _, _, nbytes in spec.buckets(bucket_bytes):
@@ -149,7 +191,8 @@ def ols_slope(x, y):
 
 
 def sweep(model: str, delays_us, world: int = 2, bucket_bytes: int = 65536, device: int = 0,
-          extra_config: str = "", iterations: int | None = None, reference_fn=None):
+          extra_config: str = "", iterations: int | None = None, reference_fn=None,
+          trace_csv: str | None = None):
     """`reference_fn(model_text, world, bucket_bytes, inject_us) -> per-iteration
     times (us)` optionally times a comparison emulator on the same loop (the
     callers pass the reference CPU emulator; this package never imports it)."""
@@ -171,6 +214,9 @@ def sweep(model: str, delays_us, world: int = 2, bucket_bytes: int = 65536, devi
                f"delay.inject_us = {float(d)!r}\n" + extra_config)
         comm = Communicator(cfg, 0, device)
         r = run_loop(comm, spec, bucket_bytes)
+        if trace_csv:  # one file per injected delay: <stem>_inject<us>.csv
+            stem, ext = os.path.splitext(trace_csv)
+            write_iteration_csv(f"{stem}_inject{int(d)}{ext or '.csv'}", r)
         ideal = predicted_us(comm, spec, bucket_bytes)
         comm.close()
         xs = r["iter_us"][info["warmup"]:]
@@ -208,8 +254,9 @@ def main():
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--bucket-bytes", type=int, default=65536)
     ap.add_argument("--iterations", type=int, default=None)
+    ap.add_argument("--trace-csv", default=None, help="per-(iteration, bucket) trace, reference columns")
     a = ap.parse_args()
-    res = sweep(a.model, a.delays_us, a.world, a.bucket_bytes, iterations=a.iterations)
+    res = sweep(a.model, a.delays_us, a.world, a.bucket_bytes, iterations=a.iterations, trace_csv=a.trace_csv)
     for p in res["points"]:
         ref_txt = (f"   reference {p['reference_mean_us']:9.1f} us (err {100 * p['reference_rel_err']:.2f}%)"
                    if "reference_mean_us" in p else "")

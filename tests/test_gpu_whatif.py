@@ -20,10 +20,13 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_bert_like_whatif_sweep(cuda):
+def test_bert_like_whatif_sweep(cuda, tmp_path):
     # acceptance criterion 7's sweep (acceptance_main.cpp:323-334)
     res = sweep("bert-like", [0, 500, 1000, 4000, 6000, 8000, 10000], world=2, bucket_bytes=65536,
-                iterations=30)
+                iterations=30, trace_csv=str(tmp_path / "trace.csv"))
+    from paper_2405_02969_b200.whatif import read_iteration_csv
+    tr = read_iteration_csv(str(tmp_path / "trace_inject4000.csv"))  # reference columns, 30 x 4 rows
+    assert len(tr) == 30 and all(len(t["buckets"]) == 4 for t in tr.values())
     assert res["buckets"] == 4 and res["knee_us"] == 2000
     assert res["checks_pass"], res
     assert res["max_rel_err"] < 0.01, res

@@ -75,3 +75,22 @@ def test_predicted_timeline_hand_computed():
         assert got == max(t, free)
     assert lib.cemuPredictIterationUs(spec._h, 65536, np.zeros(4).ctypes.data, 4) == 12000.0
     _ = C
+
+
+def test_iteration_csv_round_trip_and_stats(tmp_path):
+    """write_iteration_csv / read_iteration_csv / iteration_stats with the
+    reference's columns and semantics (harness.cpp:256-319)."""
+    import numpy as np
+    from paper_2405_02969_b200 import whatif as W
+    trace = {"start_us": np.array([0.0, 1000.4, 2100.0]), "end_us": np.array([990.0, 2080.0, 3300.6]),
+             "issue_us": np.array([[10.0, 500.0], [1010.0, 1600.0], [2110.0, 2700.0]]),
+             "complete_us": np.array([[400.0, 980.0], [1500.0, 2070.0], [2600.0, 3290.0]])}
+    trace["iter_us"] = trace["end_us"] - trace["start_us"]
+    p = tmp_path / "t.csv"
+    W.write_iteration_csv(str(p), trace)
+    lines = p.read_text().splitlines()
+    assert lines[0] == "iter,start_us,end_us,bucket_id,issue_us,complete_us" and len(lines) == 7
+    back = W.read_iteration_csv(str(p))
+    assert sorted(back) == [0, 1, 2] and back[1]["buckets"] == [(0, 1010, 1500), (1, 1600, 2070)]
+    st = W.iteration_stats(trace, warmup=1)
+    assert st["count"] == 2 and abs(st["mean_us"] - np.mean(trace["iter_us"][1:])) < 1e-9
