@@ -1364,11 +1364,17 @@ cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t s
 
 cudaError_t launch_fused_allgather(int dtype, const FusedGatherArgs& a, cudaStream_t s, int* launches) {
   if (a.k < 2 || a.k > kMaxReal) return cudaErrorInvalidValue;
-  // NVLink push CTAs vs local synthesis CTAs, split by the bytes each moves
+  // NVLink push CTAs vs local synthesis CTAs, split by the bytes each writes
+  // (k destinations of the own block vs the emulated blocks): measured 24-27%
+  // faster than an even split at 1 GiB (k = 2: 0.295 -> 0.225 ms, k = 4:
+  // 0.369 -> 0.270 ms), with 8 CTAs per SM (write streams need many in flight)
   const uint64_t push_vecs = a.block_vecs;
   const uint64_t synth_vecs = static_cast<uint64_t>(a.nvirt) * a.block_vecs;
-  const uint64_t total_ctas = static_cast<uint64_t>(sm_count()) * 4;
-  uint64_t push = std::max<uint64_t>(1, std::min<uint64_t>((push_vecs + kThreads - 1) / kThreads, total_ctas / 2));
+  static const int per_sm = std::max(1, fused_env("CEMU_FUSED_AG_CTAS", 8));
+  const uint64_t total_ctas = static_cast<uint64_t>(sm_count()) * per_sm;
+  const uint64_t share = total_ctas * static_cast<uint64_t>(a.k) / (static_cast<uint64_t>(a.k) + a.nvirt);
+  uint64_t push = std::max<uint64_t>(1, std::min<uint64_t>((push_vecs + kThreads - 1) / kThreads,
+                                                           std::max<uint64_t>(share, 1)));
   uint64_t synth = synth_vecs ? std::max<uint64_t>(1, std::min<uint64_t>((synth_vecs + kThreads - 1) / kThreads,
                                                                           total_ctas - push))
                               : 0;
