@@ -16,33 +16,12 @@
 // errors map to cemuInvalidArgument / cemuInvalidUsage with a message that
 // names the offending argument (cemuGetLastError), as the reference's
 // TransportError/ConfigError texts do (collective.cpp:190-205).
-#include <cuda_runtime.h>
-#include <dlfcn.h>
-#include <nccl.h>
+//
+// Shared declarations: comm_internal.hpp; the host-buffer pipeline lives in
+// host_pipe.cpp, wire mode in comm_wire.cpp.
+#include "comm_internal.hpp"
 
-#include <algorithm>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <functional>
-#include <map>
-#include <memory>
-#include <mutex>
-#include <random>
-#include <string>
-#include <vector>
-
-#include "cemu_b200.h"
-#include "config.hpp"
-#include "delay_math.cuh"
-#include "kernels.hpp"
-#include "payload.cuh"
-#include "schedule.hpp"
-#include "wire.hpp"
-
-using namespace cemu_b200;
-
-namespace {
+namespace cemu_b200 {
 
 thread_local std::string g_last_error;
 
@@ -52,26 +31,7 @@ cemuResult_t fail(cemuResult_t code, const std::string& msg) {
 }
 
 // ---- NCCL, loaded on demand (only jobs with several real GPUs need it) ----
-struct Nccl {
-  void* h = nullptr;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
-                                ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int,
-                         ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*GroupStart)() = nullptr;
-  ncclResult_t (*GroupEnd)() = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-};
+
 
 std::mutex g_nccl_mu;
 Nccl g_nccl;
@@ -121,222 +81,8 @@ size_t dtype_size(int dt) {
   }
 }
 
-// Deferred calls between cemuGroupStart/End (NCCL group semantics: nothing
-// needs to start before ncclGroupEnd).  The composite ops chain NCCL calls
-// with our kernels, so they are replayed in order at GroupEnd.
-using Phases = std::vector<std::function<cemuResult_t()>>;
-struct GroupOp {
-  cemuComm* c;
-  Phases phases;
-};
 thread_local int g_group_depth = 0;
 thread_local std::vector<GroupOp> g_group_ops;
-
-}  // namespace
-
-struct cemuComm {
-  JobConfig cfg;
-  uint32_t W = 0, rank = 0;
-  int device = 0;
-  std::vector<uint32_t> real;  // ascending world ranks of the real GPUs
-  uint32_t k = 1, li = 0;      // number of real ranks, my index among them
-  bool contiguous = true;      // real ranks form one block [real[0], real[0]+k)
-  cemuDelayModel delay{};
-  bool delay_active = false;
-  // delay-model plugin (cemuCommSetDelayModel): offsets per call from the
-  // user's function, staged through pinned memory into the record slot
-  cemuDelayModelFn delay_fn = nullptr;
-  void* delay_user = nullptr;
-  bool config_delay_active = false;
-  double* h_offsets = nullptr;            // pinned, kSlots x kmax
-  cudaEvent_t offsets_copied[64] = {};    // per slot: the staging may be rewritten
-  uint64_t seed = 1;
-  PayloadMode mode = PayloadMode::kHash;
-  std::vector<uint32_t> virt;  // emulated ranks, ascending
-  uint32_t* d_virt_keys = nullptr;
-  uint32_t* d_virt_ranks = nullptr;
-  // per-call record ring
-  static constexpr uint32_t kSlots = 64;
-  uint32_t kmax = 1;
-  int64_t* d_slots = nullptr;
-  struct Meta {
-    uint64_t call_id = ~0ull;
-    int32_t coll = 0;
-    bool delay = false;
-    uint32_t k = 0;
-    uint64_t bytes = 0;
-    int64_t latency = 0;
-  } meta[kSlots];
-  uint64_t calls = 0;
-  ncclComm_t inner = nullptr;
-  uint64_t launches = 0;
-  // fused multi-GPU path (k > 1): IPC-mapped signal areas and symmetric buffers
-  uint8_t* sig = nullptr;  // local: flags[16] u64 | counter u32 @256 | error u32 @260 | epoch u64 @264
-  uint8_t* peer_sig[kMaxReal] = {};       // every real GPU's area (own = sig)
-  bool fused = true;
-  int64_t fused_timeout_ns = 30'000'000'000LL;
-  struct Region {
-    uint8_t* base = nullptr;
-    size_t bytes = 0;
-    uint8_t* peer[kMaxReal] = {};  // own = base
-  };
-  std::vector<Region> regions;
-  void* scratch = nullptr;  // aligned staging for misaligned local outputs
-  size_t scratch_bytes = 0;
-  // host-buffer collectives (cemuAllReduceHost / cemuAllGatherHost): chunks
-  // ride a 3-stage pipeline -- H2D copy engine, synthesis kernel, D2H copy
-  // engine -- over kPipeBufs rotating device buffers, so both PCIe
-  // directions and the SMs work at once
-  static constexpr int kPipeBufs = 4;
-  struct HostPipe {
-    bool ready = false;
-    size_t chunk = 0;                 // bytes per chunk (multiple of 1 MiB)
-    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
-    cudaEvent_t start = nullptr;
-    cudaEvent_t loaded[kPipeBufs] = {}, done[kPipeBufs] = {}, drained[kPipeBufs] = {};
-    void* buf[kPipeBufs] = {};
-    bool symmetric = false;            // k > 1: buffers are regions mapped on every real GPU
-    uint8_t* peer[kPipeBufs][kMaxReal] = {};
-  } pipe;
-  // wire mode (cemuCommAttachEmulator): collectives travel the CEMU protocol
-  // to a reference emulator instead of being synthesised
-  std::unique_ptr<WireSession> wire;
-  void* wire_buf = nullptr;  // device staging of one received DATA payload
-  size_t wire_buf_bytes = 0;
-
-  // Releases every resource held, in dependency order; also runs when
-  // initialisation fails half way (init_comm owns the comm in a unique_ptr).
-  ~cemuComm() {
-    cudaSetDevice(device);
-    wire.reset();  // BYE to the emulator
-    auto& p = pipe;
-    for (cudaStream_t st : {p.h2d, p.comp, p.d2h}) {
-      if (st) cudaStreamSynchronize(st);
-    }
-    for (int b = 0; b < kPipeBufs; ++b) {
-      if (!p.symmetric && p.buf[b]) cudaFree(p.buf[b]);  // symmetric buffers are regions (below)
-      for (cudaEvent_t ev : {p.loaded[b], p.done[b], p.drained[b]}) {
-        if (ev) cudaEventDestroy(ev);
-      }
-    }
-    if (p.start) cudaEventDestroy(p.start);
-    for (cudaStream_t st : {p.h2d, p.comp, p.d2h}) {
-      if (st) cudaStreamDestroy(st);
-    }
-    for (auto& r : regions) {
-      for (uint32_t g = 0; g < k; ++g) {
-        if (g != li && r.peer[g]) cudaIpcCloseMemHandle(r.peer[g]);
-      }
-      cudaFree(r.base);
-    }
-    for (uint32_t g = 0; g < k && g < static_cast<uint32_t>(kMaxReal); ++g) {
-      if (g != li && peer_sig[g]) cudaIpcCloseMemHandle(peer_sig[g]);
-    }
-    cudaFree(sig);
-    cudaFree(scratch);
-    cudaFree(wire_buf);
-    if (inner) {
-      if (const Nccl* n = nccl()) n->CommDestroy(inner);
-    }
-    for (cudaEvent_t ev : offsets_copied) {
-      if (ev) cudaEventDestroy(ev);
-    }
-    if (h_offsets) cudaFreeHost(h_offsets);
-    cudaFree(d_virt_keys);
-    cudaFree(d_virt_ranks);
-    cudaFree(d_slots);
-  }
-};
-
-namespace {
-
-struct Call {
-  cemuComm* c;
-  int64_t* slot = nullptr;
-  bool stamped = false;
-  int launches = 0;
-  cudaStream_t s;
-
-  uint32_t i = 0;  // record slot of this call
-  std::vector<double> plugin;  // a delay-model plugin's offsets for this call
-  std::string error;           // set when the plugin failed: the call must not run
-
-  Call(cemuComm* comm, int coll, uint64_t model_bytes, cudaStream_t stream) : c(comm), s(stream) {
-    const uint64_t id = c->calls++;
-    i = static_cast<uint32_t>(id % cemuComm::kSlots);
-    auto& m = c->meta[i];
-    m.call_id = id;
-    m.coll = coll;
-    m.delay = c->delay_active;
-    m.k = to_real_count(coll, c->W, c->real);
-    m.bytes = model_bytes;
-    if (c->delay_fn) {
-      // DelayModelFn(boundary, bytes) -> offsets (delay.hpp:52-55): the
-      // boundary is closed-form here, so the plugin sees (coll, n, bytes, K)
-      plugin.assign(m.k, 0.0);
-      const int rc = c->delay_fn(coll, c->W, model_bytes, m.k, plugin.data(), c->delay_user);
-      if (rc != 0) {
-        error = "delay model plugin returned " + std::to_string(rc) + " for call " + std::to_string(id);
-      }
-      int64_t lat = 0;
-      for (double o : plugin) lat = std::max<int64_t>(lat, std::llround(o));
-      m.latency = lat;
-    } else {
-      m.latency = c->delay_active ? call_latency_us(c->delay, coll, c->W, model_bytes, m.k) : 0;
-    }
-    if (c->delay_active) slot = c->d_slots + i * slot_words(c->kmax);
-  }
-  // pointer the first kernel of the call writes t_start into (or null)
-  int64_t* take_stamp() {
-    if (!slot || stamped) return nullptr;
-    stamped = true;
-    return slot;
-  }
-  cudaError_t stamp_now() {
-    if (!slot || stamped) return cudaSuccess;
-    stamped = true;
-    return launch_stamp(slot, s, &launches);
-  }
-  cudaError_t finish(int coll) {
-    c->launches += launches;
-    if (!slot) return cudaSuccess;
-    const auto& m = c->meta[i];
-    DelayLaunch d;
-    d.model = c->delay;
-    d.coll = coll;
-    d.n = c->W;
-    d.bytes = m.bytes;
-    d.k = m.k;
-    d.kmax = c->kmax;
-    d.self_stamp = stamped ? 0 : 1;
-    d.preloaded = 0;
-    if (!plugin.empty()) {
-      // stage the plugin's offsets into the slot's offsets region, in stream
-      // order; the pinned staging of slot i is reused 64 calls later
-      cudaEvent_t& ev = c->offsets_copied[i];
-      if (!ev) {
-        if (const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) return e;
-      } else if (const cudaError_t e = cudaEventSynchronize(ev)) {
-        return e;
-      }
-      double* h = c->h_offsets + static_cast<size_t>(i) * c->kmax;
-      std::memcpy(h, plugin.data(), plugin.size() * sizeof(double));
-      auto* dev_offs = reinterpret_cast<double*>(slot + kSlotHeader + 2 * static_cast<size_t>(c->kmax));
-      if (const cudaError_t e = cudaMemcpyAsync(dev_offs, h, plugin.size() * sizeof(double),
-                                                cudaMemcpyHostToDevice, s)) {
-        return e;
-      }
-      if (const cudaError_t e = cudaEventRecord(ev, s)) return e;
-      d.preloaded = 1;
-    }
-    int l = 0;
-    const cudaError_t e = launch_delay_spin(d, slot, s, &l);
-    c->launches += l;
-    return e;
-  }
-};
-
-namespace {
 
 // All-gather `rec` (bytes each) among the k real GPUs through the inner NCCL
 // comm; synchronous (setup / registration only, never on the hot path).
@@ -416,17 +162,6 @@ uint32_t op_sig(int coll, int dt, uint64_t count) {
   return static_cast<uint32_t>(h ^ (h >> 32)) & 0xFFFFFu;
 }
 
-template <typename A>
-void set_barrier(cemuComm* c, A& a) {
-  for (uint32_t g = 0; g < c->k; ++g) a.peer_flags[g] = reinterpret_cast<uint64_t*>(c->peer_sig[g]);
-  a.k = static_cast<int>(c->k);
-  a.me = static_cast<int>(c->li);
-  a.flags = reinterpret_cast<uint64_t*>(c->sig);
-  a.counter = reinterpret_cast<uint32_t*>(c->sig + 256);
-  a.error = reinterpret_cast<uint32_t*>(c->sig + 260);
-  a.epoch = reinterpret_cast<uint64_t*>(c->sig + 264);
-  a.timeout_ns = c->fused_timeout_ns;
-}
 
 const cemuComm::Region* find_region(const cemuComm* c, const void* p, size_t bytes) {
   const auto* b = static_cast<const uint8_t*>(p);
@@ -435,24 +170,6 @@ const cemuComm::Region* find_region(const cemuComm* c, const void* p, size_t byt
   }
   return nullptr;
 }
-
-}  // namespace
-
-#define CUDA_OK(expr)                                                                   \
-  do {                                                                                  \
-    const cudaError_t e_ = (expr);                                                      \
-    if (e_ != cudaSuccess)                                                              \
-      return fail(cemuUnhandledCudaError, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-#define NCCL_OK(expr)                                                                       \
-  do {                                                                                      \
-    const ncclResult_t r_ = (expr);                                                         \
-    if (r_ != ncclSuccess)                                                                  \
-      return fail(static_cast<cemuResult_t>(r_),                                            \
-                  std::string(#expr) + ": " +                                               \
-                      (nccl()->GetErrorString ? nccl()->GetErrorString(r_) : "nccl error")); \
-  } while (0)
 
 cemuResult_t check_common(cemuComm* c, int dt, const char* what) {
   if (!c) return fail(cemuInvalidArgument, std::string(what) + ": comm is null");
@@ -890,284 +607,6 @@ cemuResult_t do_broadcast(const void* send, void* recv, size_t count, int dt, in
   return cemuSuccess;
 }
 
-// ---- host-buffer collectives -------------------------------------------------
-// The reference's WorkerSession takes host spans (collective.hpp:68-78);
-// these entry points keep that shape.  One real GPU, hash payload: the
-// buffer streams through the pipe in chunks, chunk i's H2D overlapping chunk
-// i-1's synthesis and chunk i-2's D2H (PCIe is full duplex; the kernel takes
-// ~1% of a chunk's transfer time).  Anything else (several real GPUs, zero
-// payload) stages the whole buffer through device scratch and runs the
-// device collective.
-cemuResult_t ensure_pipe(cemuComm* c) {
-  auto& p = c->pipe;
-  if (p.ready) return cemuSuccess;
-  if (!p.chunk) {
-    size_t mib = 32;  // measured: 4 MiB 27.3 ms, 16 MiB 24.8, 32 MiB 22.9 per 1 GiB (full-duplex PCIe floor 22.4)
-    if (const char* e = std::getenv("CEMU_HOST_CHUNK_MIB")) mib = std::max(1, std::atoi(e));
-    p.chunk = mib << 20;
-  }
-  // (a retry after a failed attempt creates only what is still missing)
-  if (!p.h2d) CUDA_OK(cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking));
-  if (!p.comp) CUDA_OK(cudaStreamCreateWithFlags(&p.comp, cudaStreamNonBlocking));
-  if (!p.d2h) CUDA_OK(cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking));
-  if (!p.start) CUDA_OK(cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming));
-  // several real GPUs: the buffers are symmetric (mapped on every real GPU,
-  // collective like cemuMemAlloc) so each chunk is one fused kernel
-  p.symmetric = c->k > 1;
-  for (int b = 0; b < cemuComm::kPipeBufs; ++b) {
-    if (!p.buf[b] && p.symmetric) {
-      const size_t rounded = (p.chunk + (2u << 20) - 1) & ~static_cast<size_t>((2u << 20) - 1);
-      void* d = nullptr;
-      CUDA_OK(cudaMalloc(&d, rounded));
-      cemuComm::Region r;
-      r.base = static_cast<uint8_t*>(d);
-      r.bytes = rounded;
-      r.peer[c->li] = r.base;
-      if (auto e = map_peers(c, d, rounded, r.peer)) {
-        cudaFree(d);
-        return e;
-      }
-      c->regions.push_back(r);  // owns the allocation from here on
-      p.buf[b] = d;
-      for (uint32_t g = 0; g < c->k; ++g) p.peer[b][g] = r.peer[g];
-    } else if (!p.buf[b]) {
-      CUDA_OK(cudaMalloc(&p.buf[b], p.chunk));
-    }
-    if (!p.loaded[b]) CUDA_OK(cudaEventCreateWithFlags(&p.loaded[b], cudaEventDisableTiming));
-    if (!p.done[b]) CUDA_OK(cudaEventCreateWithFlags(&p.done[b], cudaEventDisableTiming));
-    if (!p.drained[b]) CUDA_OK(cudaEventCreateWithFlags(&p.drained[b], cudaEventDisableTiming));
-  }
-  p.ready = true;
-  return cemuSuccess;
-}
-
-// One chunk: optional H2D of `in` into the device buffer, `work` on the
-// compute stream, D2H of the buffer into `out`.
-struct PipeChunk {
-  const void* in = nullptr;  // host source (null: nothing to load)
-  void* out = nullptr;       // host destination
-  size_t bytes = 0;
-  std::function<cudaError_t(int b, void* dbuf, cudaStream_t)> work;
-};
-
-cemuResult_t run_pipe(cemuComm* c, cudaStream_t s, const std::vector<PipeChunk>& chunks) {
-  auto& p = c->pipe;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  CUDA_OK(cudaStreamIsCapturing(s, &cap));
-  const bool capturing = cap != cudaStreamCaptureStatusNone;
-  CUDA_OK(cudaEventRecord(p.start, s));  // fork: everything after the caller's prior work
-  CUDA_OK(cudaStreamWaitEvent(p.h2d, p.start, 0));
-  CUDA_OK(cudaStreamWaitEvent(p.comp, p.start, 0));
-  CUDA_OK(cudaStreamWaitEvent(p.d2h, p.start, 0));
-  for (size_t i = 0; i < chunks.size(); ++i) {
-    const int b = static_cast<int>(i % cemuComm::kPipeBufs);
-    const PipeChunk& ch = chunks[i];
-    // buffer b is free once its previous chunk has drained (a previous
-    // call's drain is ordered by the fork unless the caller switched
-    // streams; outside capture wait for it explicitly)
-    if (i >= static_cast<size_t>(cemuComm::kPipeBufs) || !capturing) {
-      CUDA_OK(cudaStreamWaitEvent(p.h2d, p.drained[b], 0));
-    }
-    if (ch.in) CUDA_OK(cudaMemcpyAsync(p.buf[b], ch.in, ch.bytes, cudaMemcpyHostToDevice, p.h2d));
-    CUDA_OK(cudaEventRecord(p.loaded[b], p.h2d));
-    CUDA_OK(cudaStreamWaitEvent(p.comp, p.loaded[b], 0));
-    CUDA_OK(ch.work(b, p.buf[b], p.comp));
-    CUDA_OK(cudaEventRecord(p.done[b], p.comp));
-    CUDA_OK(cudaStreamWaitEvent(p.d2h, p.done[b], 0));
-    CUDA_OK(cudaMemcpyAsync(ch.out, p.buf[b], ch.bytes, cudaMemcpyDeviceToHost, p.d2h));
-    CUDA_OK(cudaEventRecord(p.drained[b], p.d2h));
-  }
-  // join: the d2h stream is in order, its last event covers every chunk
-  if (!chunks.empty()) {
-    const int last = static_cast<int>((chunks.size() - 1) % cemuComm::kPipeBufs);
-    CUDA_OK(cudaStreamWaitEvent(s, p.drained[last], 0));
-  }
-  // capture needs every forked stream joined back
-  if (capturing) {
-    CUDA_OK(cudaEventRecord(p.loaded[0], p.h2d));
-    CUDA_OK(cudaStreamWaitEvent(s, p.loaded[0], 0));
-    CUDA_OK(cudaEventRecord(p.done[0], p.comp));
-    CUDA_OK(cudaStreamWaitEvent(s, p.done[0], 0));
-  }
-  return cemuSuccess;
-}
-
-cemuResult_t host_allreduce(const void* send, void* recv, size_t count, int dt, cemuComm* c, cudaStream_t s) {
-  const size_t es = dtype_size(dt);
-  const uint64_t bytes = static_cast<uint64_t>(count) * es;
-  // several real GPUs: chunks go through the fused kernel over symmetric
-  // pipe buffers (rank-independent decision: every real rank pipelines)
-  const bool fused = c->k > 1 && c->fused && es <= 4 && c->mode == PayloadMode::kHash && !c->virt.empty();
-  if ((c->k > 1 && !fused) || c->mode != PayloadMode::kHash) {  // staged through device scratch
-    if (auto r = ensure_scratch(c, bytes)) return r;
-    CUDA_OK(cudaMemcpyAsync(c->scratch, send, bytes, cudaMemcpyHostToDevice, s));
-    Phases ph;
-    if (auto r = do_allreduce(c->scratch, c->scratch, count, dt, c, s, ph)) return r;
-    for (auto& f : ph) {
-      if (auto r = f()) return r;
-    }
-    CUDA_OK(cudaMemcpyAsync(recv, c->scratch, bytes, cudaMemcpyDeviceToHost, s));
-    return cemuSuccess;
-  }
-  if (auto r = ensure_pipe(c)) return r;
-  auto call = std::make_shared<Call>(c, kAllReduce, bytes, s);
-  if (!call->error.empty()) return fail(cemuInvalidArgument, call->error);
-  CUDA_OK(call->stamp_now());
-  const uint64_t per = c->pipe.chunk / es;  // elements per chunk: a multiple of 4 (payload words)
-  std::vector<PipeChunk> chunks;
-  for (uint64_t e0 = 0; e0 < count; e0 += per) {
-    const uint64_t n = std::min<uint64_t>(per, count - e0);
-    PipeChunk ch;
-    ch.in = static_cast<const uint8_t*>(send) + e0 * es;
-    ch.out = static_cast<uint8_t*>(recv) + e0 * es;
-    ch.bytes = n * es;
-    const uint32_t nk = static_cast<uint32_t>(c->virt.size());
-    if (fused) {
-      ch.work = [c, call, dt, n, e0](int b, void*, cudaStream_t st) {
-        FusedArgs a = fused_allreduce_args(c, dt, n, e0, c->pipe.peer[b], c->pipe.peer[b]);  // in place
-        set_barrier(c, a);
-        a.sig = op_sig(kAllReduce, dt, n);
-        return launch_fused_allreduce(dt, a, st, &call->launches);
-      };
-    } else {
-      ch.work = [c, call, dt, n, e0, nk](int, void* d, cudaStream_t st) {
-        return launch_synth_reduce(dt, d, d, n, e0, c->d_virt_keys, nk, nullptr, st, &call->launches);
-      };
-    }
-    chunks.push_back(std::move(ch));
-  }
-  if (auto r = run_pipe(c, s, chunks)) return r;
-  CUDA_OK(call->finish(kAllReduce));
-  return cemuSuccess;
-}
-
-cemuResult_t host_allgather(const void* send, void* recv, size_t sc, int dt, cemuComm* c, cudaStream_t s) {
-  const size_t es = dtype_size(dt);
-  const uint64_t blk = static_cast<uint64_t>(sc) * es;
-  auto* r8 = static_cast<uint8_t*>(recv);
-  if (c->k > 1 || c->mode != PayloadMode::kHash) {
-    if (auto r = ensure_scratch(c, blk * c->W)) return r;
-    auto* d8 = static_cast<uint8_t*>(c->scratch);
-    CUDA_OK(cudaMemcpyAsync(d8 + c->rank * blk, send, blk, cudaMemcpyHostToDevice, s));
-    Phases ph;
-    if (auto r = do_allgather(d8 + c->rank * blk, d8, sc, dt, c, s, ph)) return r;
-    for (auto& f : ph) {
-      if (auto r = f()) return r;
-    }
-    CUDA_OK(cudaMemcpyAsync(recv, c->scratch, blk * c->W, cudaMemcpyDeviceToHost, s));
-    return cemuSuccess;
-  }
-  if (auto r = ensure_pipe(c)) return r;
-  auto call = std::make_shared<Call>(c, kAllGather, blk, s);
-  if (!call->error.empty()) return fail(cemuInvalidArgument, call->error);
-  CUDA_OK(call->stamp_now());
-  // the own block (collective.cpp:289-291: in place it is already there)
-  if (send != r8 + c->rank * blk) {
-    CUDA_OK(cudaMemcpyAsync(r8 + c->rank * blk, send, blk, cudaMemcpyDefault, s));
-  }
-  const uint64_t per = c->pipe.chunk / es;
-  std::vector<PipeChunk> chunks;
-  for (size_t v = 0; v < c->virt.size(); ++v) {
-    const uint32_t r = c->virt[v];
-    const uint32_t key = payload_key(c->seed, r);
-    for (uint64_t e0 = 0; e0 < sc; e0 += per) {
-      const uint64_t n = std::min<uint64_t>(per, sc - e0);
-      PipeChunk ch;
-      ch.out = r8 + r * blk + e0 * es;
-      ch.bytes = n * es;
-      ch.work = [call, dt, n, e0, key](int, void* d, cudaStream_t st) {
-        return launch_synth_fill(dt, d, n, nullptr, nullptr, 1, 0, key, nullptr, 0, nullptr, st, &call->launches,
-                                 e0);
-      };
-      chunks.push_back(std::move(ch));
-    }
-  }
-  if (auto r = run_pipe(c, s, chunks)) return r;
-  CUDA_OK(call->finish(kAllGather));
-  return cemuSuccess;
-}
-
-// ---- wire mode -------------------------------------------------------------
-// The call runs the reference worker's op (collective.cpp:268-355) with the
-// buffer on the GPU: each outgoing chunk is read back from HBM, each incoming
-// DATA payload is copied up and folded by launch_wire_fold.  Host-synchronous
-// (the protocol is a conversation); results and the per-step arrival times
-// land in the call record, next to the device model's floors for the same
-// call, so the reference engine's releases can be checked against them.
-cemuResult_t wire_call(cemuComm* c, int coll, const void* send, void* recv, uint64_t buf_bytes, uint64_t model_bytes,
-                       uint32_t es, cudaStream_t s) {
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  CUDA_OK(cudaStreamIsCapturing(s, &cap));
-  if (cap != cudaStreamCaptureStatusNone) {
-    return fail(cemuInvalidUsage, "wire mode: collectives are host-synchronous and cannot be captured");
-  }
-  auto* r8 = static_cast<uint8_t*>(recv);
-  if (coll == kAllReduce && send != recv) CUDA_OK(cudaMemcpyAsync(recv, send, buf_bytes, cudaMemcpyDeviceToDevice, s));
-  if (coll == kAllGather) {
-    uint8_t* own = r8 + static_cast<uint64_t>(c->rank) * model_bytes;
-    if (send != own) CUDA_OK(cudaMemcpyAsync(own, send, model_bytes, cudaMemcpyDeviceToDevice, s));
-  }
-  CUDA_OK(cudaStreamSynchronize(s));
-  const uint64_t id = c->calls++;
-  const uint32_t i = static_cast<uint32_t>(id % cemuComm::kSlots);
-  auto& m = c->meta[i];
-  m.call_id = id;
-  m.coll = coll;
-  m.delay = true;  // the record holds the wire arrivals
-  m.k = to_real_count(coll, c->W, c->real);
-  m.bytes = model_bytes;
-  m.latency = call_latency_us(c->delay, coll, c->W, model_bytes, m.k);
-  int launches = 0;
-  cudaError_t cerr = cudaSuccess;
-  auto load = [&](uint64_t off, uint64_t len, uint8_t* host) {
-    if (cerr == cudaSuccess) cerr = cudaMemcpy(host, r8 + off, len, cudaMemcpyDeviceToHost);
-  };
-  auto store = [&](uint64_t off, const uint8_t* host, uint64_t len, bool reduce) {
-    if (cerr != cudaSuccess || len == 0) return;
-    if (!reduce) {
-      cerr = cudaMemcpy(r8 + off, host, len, cudaMemcpyHostToDevice);
-      return;
-    }
-    if (c->wire_buf_bytes < len) {
-      if (c->wire_buf) cudaFree(c->wire_buf);
-      c->wire_buf = nullptr;
-      c->wire_buf_bytes = 0;
-      if ((cerr = cudaMalloc(&c->wire_buf, len)) != cudaSuccess) return;
-      c->wire_buf_bytes = len;
-    }
-    if ((cerr = cudaMemcpyAsync(c->wire_buf, host, len, cudaMemcpyHostToDevice, s)) != cudaSuccess) return;
-    if ((cerr = launch_wire_fold(r8 + off, c->wire_buf, len, es == 4, s, &launches)) != cudaSuccess) return;
-    cerr = cudaStreamSynchronize(s);
-  };
-  int64_t t_open = 0;
-  std::vector<int64_t> arrivals;
-  try {
-    c->wire->run(coll, buf_bytes, es, load, store, &t_open, &arrivals);
-  } catch (const WireError& e) {
-    c->launches += launches;
-    return fail(cemuRemoteError, e.what());
-  }
-  c->launches += launches;
-  CUDA_OK(cerr);
-  // call record: model floors beside the reference engine's observed releases
-  const std::vector<double> offs = release_offsets(c->delay, coll, c->W, model_bytes, m.k);
-  std::vector<int64_t> rec(slot_words(c->kmax), 0);
-  rec[0] = t_open;
-  int64_t maxf = 0;
-  for (uint32_t j = 0; j < m.k; ++j) {
-    const int64_t f = std::llround(offs[j]);
-    maxf = std::max(maxf, f);
-    rec[kSlotHeader + j] = f;
-    rec[kSlotHeader + c->kmax + j] = j < arrivals.size() ? arrivals[j] : 0;
-    std::memcpy(&rec[kSlotHeader + 2 * c->kmax + j], &offs[j], 8);
-  }
-  rec[1] = arrivals.empty() ? t_open : arrivals.back();
-  rec[2] = maxf;
-  rec[3] = m.k;
-  CUDA_OK(cudaMemcpy(c->d_slots + i * slot_words(c->kmax), rec.data(), rec.size() * 8, cudaMemcpyHostToDevice));
-  return cemuSuccess;
-}
-
 // A collective is planned into phases (closures); nothing runs at planning
 // time.  Alone, its phases run back to back.  In a group, cemuGroupEnd runs
 // "rounds" -- the i-th call of every communicator -- phase by phase, each
@@ -1196,7 +635,7 @@ cemuResult_t run_or_defer(cemuComm* c, F&& plan) {
   return cemuSuccess;
 }
 
-}  // namespace
+}  // namespace cemu_b200
 
 // =============================================================================
 // C-ABI
@@ -1378,34 +817,6 @@ cemuResult_t cemuAllReduce(const void* send, void* recv, size_t count, cemuDataT
   return run_or_defer(c, [=](Phases& ph) { return do_allreduce(send, recv, count, dt, c, s, ph); });
 }
 
-cemuResult_t cemuAllReduceHost(const void* send, void* recv, size_t count, cemuDataType_t dt, cemuRedOp_t op,
-                               cemuComm_t c, cemuStream_t stream) {
-  if (auto r = check_common(c, dt, "cemuAllReduceHost")) return r;
-  if (auto r = check_op(op, "cemuAllReduceHost")) return r;
-  if (count && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllReduceHost: null buffer");
-  if (g_group_depth > 0) return fail(cemuInvalidUsage, "cemuAllReduceHost: host-buffer collectives cannot be grouped");
-  if (c->wire) return fail(cemuInvalidUsage, "cemuAllReduceHost: not available in wire mode");
-  if (count == 0) return cemuSuccess;
-  try {
-    return host_allreduce(send, recv, count, dt, c, reinterpret_cast<cudaStream_t>(stream));
-  } catch (const std::exception& e) {
-    return fail(cemuInternalError, e.what());
-  }
-}
-
-cemuResult_t cemuAllGatherHost(const void* send, void* recv, size_t sc, cemuDataType_t dt, cemuComm_t c,
-                               cemuStream_t stream) {
-  if (auto r = check_common(c, dt, "cemuAllGatherHost")) return r;
-  if (sc && (!send || !recv)) return fail(cemuInvalidArgument, "cemuAllGatherHost: null buffer");
-  if (g_group_depth > 0) return fail(cemuInvalidUsage, "cemuAllGatherHost: host-buffer collectives cannot be grouped");
-  if (c->wire) return fail(cemuInvalidUsage, "cemuAllGatherHost: not available in wire mode");
-  if (sc == 0) return cemuSuccess;
-  try {
-    return host_allgather(send, recv, sc, dt, c, reinterpret_cast<cudaStream_t>(stream));
-  } catch (const std::exception& e) {
-    return fail(cemuInternalError, e.what());
-  }
-}
 
 cemuResult_t cemuAllGather(const void* send, void* recv, size_t sc, cemuDataType_t dt, cemuComm_t c,
                            cemuStream_t stream) {
@@ -1646,34 +1057,5 @@ int cemuCommEventLog(cemuComm_t c, uint64_t id, char* out, size_t cap) {
 }  // extern "C"
 
 // launch counter for bench.py's gpu_launches (not part of the public header)
-extern "C" cemuResult_t cemuCommAttachEmulator(cemuComm_t c, const cemuPlanEntry* plan, size_t nplan,
-                                               int timeoutMs) {
-  if (!c) return fail(cemuInvalidArgument, "cemuCommAttachEmulator: comm is null");
-  if (nplan && !plan) return fail(cemuInvalidArgument, "cemuCommAttachEmulator: plan is null");
-  if (c->wire) return fail(cemuInvalidUsage, "cemuCommAttachEmulator: already attached");
-  if (c->k != 1) return fail(cemuInvalidUsage, "cemuCommAttachEmulator: wire mode serves one real rank per box");
-  std::vector<WirePlanEntry> p;
-  for (size_t j = 0; j < nplan; ++j) {
-    if (plan[j].coll != kAllReduce && plan[j].coll != kAllGather) {
-      return fail(cemuInvalidArgument, "cemuCommAttachEmulator: plan entry " + std::to_string(j) +
-                                           " is not allreduce/allgather");
-    }
-    p.push_back(WirePlanEntry{plan[j].coll, plan[j].bytes, plan[j].elemSize});
-  }
-  try {
-    c->wire = std::make_unique<WireSession>(c->cfg, c->rank, std::move(p), timeoutMs > 0 ? timeoutMs : 10000);
-  } catch (const WireError& e) {
-    return fail(cemuRemoteError, e.what());
-  } catch (const std::exception& e) {
-    return fail(cemuSystemError, e.what());
-  }
-  return cemuSuccess;
-}
-
-extern "C" cemuResult_t cemuCommDetachEmulator(cemuComm_t c) {
-  if (!c) return fail(cemuInvalidArgument, "cemuCommDetachEmulator: comm is null");
-  c->wire.reset();
-  return cemuSuccess;
-}
 
 extern "C" uint64_t cemuCommKernelLaunches(cemuComm_t c) { return c ? c->launches : 0; }

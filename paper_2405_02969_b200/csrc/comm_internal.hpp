@@ -1,0 +1,333 @@
+// comm_internal.hpp -- what the communicator's translation units share
+// (comm.cpp: lifecycle, collective bodies, the C-ABI; host_pipe.cpp: the
+// host-buffer pipeline; comm_wire.cpp: wire mode).  Not part of the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "cemu_b200.h"
+#include "config.hpp"
+#include "delay_math.cuh"
+#include "kernels.hpp"
+#include "payload.cuh"
+#include "schedule.hpp"
+#include "wire.hpp"
+
+namespace cemu_b200 {
+
+// cemuGetLastError's text: the last failure on this thread
+extern thread_local std::string g_last_error;
+cemuResult_t fail(cemuResult_t code, const std::string& msg);
+
+// ---- NCCL, loaded on demand (only jobs with several real GPUs need it) ----
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int,
+                         ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const Nccl* nccl();
+
+size_t dtype_size(int dt);
+
+// Deferred calls between cemuGroupStart/End (NCCL group semantics: nothing
+// needs to start before ncclGroupEnd).  The composite ops chain NCCL calls
+// with our kernels, so they are replayed in order at GroupEnd.
+using Phases = std::vector<std::function<cemuResult_t()>>;
+struct GroupOp {
+  cemuComm* c;
+  Phases phases;
+};
+extern thread_local int g_group_depth;
+extern thread_local std::vector<GroupOp> g_group_ops;
+
+}  // namespace cemu_b200
+
+// The communicator is the C-ABI's opaque cemuComm (a global name); its
+// members use the library's types.  This header is private to the three
+// communicator translation units.
+using namespace cemu_b200;
+
+struct cemuComm {
+  JobConfig cfg;
+  uint32_t W = 0, rank = 0;
+  int device = 0;
+  std::vector<uint32_t> real;  // ascending world ranks of the real GPUs
+  uint32_t k = 1, li = 0;      // number of real ranks, my index among them
+  bool contiguous = true;      // real ranks form one block [real[0], real[0]+k)
+  cemuDelayModel delay{};
+  bool delay_active = false;
+  // delay-model plugin (cemuCommSetDelayModel): offsets per call from the
+  // user's function, staged through pinned memory into the record slot
+  cemuDelayModelFn delay_fn = nullptr;
+  void* delay_user = nullptr;
+  bool config_delay_active = false;
+  double* h_offsets = nullptr;            // pinned, kSlots x kmax
+  cudaEvent_t offsets_copied[64] = {};    // per slot: the staging may be rewritten
+  uint64_t seed = 1;
+  PayloadMode mode = PayloadMode::kHash;
+  std::vector<uint32_t> virt;  // emulated ranks, ascending
+  uint32_t* d_virt_keys = nullptr;
+  uint32_t* d_virt_ranks = nullptr;
+  // per-call record ring
+  static constexpr uint32_t kSlots = 64;
+  uint32_t kmax = 1;
+  int64_t* d_slots = nullptr;
+  struct Meta {
+    uint64_t call_id = ~0ull;
+    int32_t coll = 0;
+    bool delay = false;
+    uint32_t k = 0;
+    uint64_t bytes = 0;
+    int64_t latency = 0;
+  } meta[kSlots];
+  uint64_t calls = 0;
+  ncclComm_t inner = nullptr;
+  uint64_t launches = 0;
+  // fused multi-GPU path (k > 1): IPC-mapped signal areas and symmetric buffers
+  uint8_t* sig = nullptr;  // local: flags[16] u64 | counter u32 @256 | error u32 @260 | epoch u64 @264
+  uint8_t* peer_sig[kMaxReal] = {};       // every real GPU's area (own = sig)
+  bool fused = true;
+  int64_t fused_timeout_ns = 30'000'000'000LL;
+  struct Region {
+    uint8_t* base = nullptr;
+    size_t bytes = 0;
+    uint8_t* peer[kMaxReal] = {};  // own = base
+  };
+  std::vector<Region> regions;
+  void* scratch = nullptr;  // aligned staging for misaligned local outputs
+  size_t scratch_bytes = 0;
+  // host-buffer collectives (cemuAllReduceHost / cemuAllGatherHost): chunks
+  // ride a 3-stage pipeline -- H2D copy engine, synthesis kernel, D2H copy
+  // engine -- over kPipeBufs rotating device buffers, so both PCIe
+  // directions and the SMs work at once
+  static constexpr int kPipeBufs = 4;
+  struct HostPipe {
+    bool ready = false;
+    size_t chunk = 0;                 // bytes per chunk (multiple of 1 MiB)
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    cudaEvent_t start = nullptr;
+    cudaEvent_t loaded[kPipeBufs] = {}, done[kPipeBufs] = {}, drained[kPipeBufs] = {};
+    void* buf[kPipeBufs] = {};
+    bool symmetric = false;            // k > 1: buffers are regions mapped on every real GPU
+    uint8_t* peer[kPipeBufs][kMaxReal] = {};
+  } pipe;
+  // wire mode (cemuCommAttachEmulator): collectives travel the CEMU protocol
+  // to a reference emulator instead of being synthesised
+  std::unique_ptr<WireSession> wire;
+  void* wire_buf = nullptr;  // device staging of one received DATA payload
+  size_t wire_buf_bytes = 0;
+
+  // Releases every resource held, in dependency order; also runs when
+  // initialisation fails half way (init_comm owns the comm in a unique_ptr).
+  ~cemuComm() {
+    cudaSetDevice(device);
+    wire.reset();  // BYE to the emulator
+    auto& p = pipe;
+    for (cudaStream_t st : {p.h2d, p.comp, p.d2h}) {
+      if (st) cudaStreamSynchronize(st);
+    }
+    for (int b = 0; b < kPipeBufs; ++b) {
+      if (!p.symmetric && p.buf[b]) cudaFree(p.buf[b]);  // symmetric buffers are regions (below)
+      for (cudaEvent_t ev : {p.loaded[b], p.done[b], p.drained[b]}) {
+        if (ev) cudaEventDestroy(ev);
+      }
+    }
+    if (p.start) cudaEventDestroy(p.start);
+    for (cudaStream_t st : {p.h2d, p.comp, p.d2h}) {
+      if (st) cudaStreamDestroy(st);
+    }
+    for (auto& r : regions) {
+      for (uint32_t g = 0; g < k; ++g) {
+        if (g != li && r.peer[g]) cudaIpcCloseMemHandle(r.peer[g]);
+      }
+      cudaFree(r.base);
+    }
+    for (uint32_t g = 0; g < k && g < static_cast<uint32_t>(kMaxReal); ++g) {
+      if (g != li && peer_sig[g]) cudaIpcCloseMemHandle(peer_sig[g]);
+    }
+    cudaFree(sig);
+    cudaFree(scratch);
+    cudaFree(wire_buf);
+    if (inner) {
+      if (const Nccl* n = nccl()) n->CommDestroy(inner);
+    }
+    for (cudaEvent_t ev : offsets_copied) {
+      if (ev) cudaEventDestroy(ev);
+    }
+    if (h_offsets) cudaFreeHost(h_offsets);
+    cudaFree(d_virt_keys);
+    cudaFree(d_virt_ranks);
+    cudaFree(d_slots);
+  }
+};
+
+namespace cemu_b200 {
+
+struct Call {
+  cemuComm* c;
+  int64_t* slot = nullptr;
+  bool stamped = false;
+  int launches = 0;
+  cudaStream_t s;
+
+  uint32_t i = 0;  // record slot of this call
+  std::vector<double> plugin;  // a delay-model plugin's offsets for this call
+  std::string error;           // set when the plugin failed: the call must not run
+
+  Call(cemuComm* comm, int coll, uint64_t model_bytes, cudaStream_t stream) : c(comm), s(stream) {
+    const uint64_t id = c->calls++;
+    i = static_cast<uint32_t>(id % cemuComm::kSlots);
+    auto& m = c->meta[i];
+    m.call_id = id;
+    m.coll = coll;
+    m.delay = c->delay_active;
+    m.k = to_real_count(coll, c->W, c->real);
+    m.bytes = model_bytes;
+    if (c->delay_fn) {
+      // DelayModelFn(boundary, bytes) -> offsets (delay.hpp:52-55): the
+      // boundary is closed-form here, so the plugin sees (coll, n, bytes, K)
+      plugin.assign(m.k, 0.0);
+      const int rc = c->delay_fn(coll, c->W, model_bytes, m.k, plugin.data(), c->delay_user);
+      if (rc != 0) {
+        error = "delay model plugin returned " + std::to_string(rc) + " for call " + std::to_string(id);
+      }
+      int64_t lat = 0;
+      for (double o : plugin) lat = std::max<int64_t>(lat, std::llround(o));
+      m.latency = lat;
+    } else {
+      m.latency = c->delay_active ? call_latency_us(c->delay, coll, c->W, model_bytes, m.k) : 0;
+    }
+    if (c->delay_active) slot = c->d_slots + i * slot_words(c->kmax);
+  }
+  // pointer the first kernel of the call writes t_start into (or null)
+  int64_t* take_stamp() {
+    if (!slot || stamped) return nullptr;
+    stamped = true;
+    return slot;
+  }
+  cudaError_t stamp_now() {
+    if (!slot || stamped) return cudaSuccess;
+    stamped = true;
+    return launch_stamp(slot, s, &launches);
+  }
+  cudaError_t finish(int coll) {
+    c->launches += launches;
+    if (!slot) return cudaSuccess;
+    const auto& m = c->meta[i];
+    DelayLaunch d;
+    d.model = c->delay;
+    d.coll = coll;
+    d.n = c->W;
+    d.bytes = m.bytes;
+    d.k = m.k;
+    d.kmax = c->kmax;
+    d.self_stamp = stamped ? 0 : 1;
+    d.preloaded = 0;
+    if (!plugin.empty()) {
+      // stage the plugin's offsets into the slot's offsets region, in stream
+      // order; the pinned staging of slot i is reused 64 calls later
+      cudaEvent_t& ev = c->offsets_copied[i];
+      if (!ev) {
+        if (const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) return e;
+      } else if (const cudaError_t e = cudaEventSynchronize(ev)) {
+        return e;
+      }
+      double* h = c->h_offsets + static_cast<size_t>(i) * c->kmax;
+      std::memcpy(h, plugin.data(), plugin.size() * sizeof(double));
+      auto* dev_offs = reinterpret_cast<double*>(slot + kSlotHeader + 2 * static_cast<size_t>(c->kmax));
+      if (const cudaError_t e = cudaMemcpyAsync(dev_offs, h, plugin.size() * sizeof(double),
+                                                cudaMemcpyHostToDevice, s)) {
+        return e;
+      }
+      if (const cudaError_t e = cudaEventRecord(ev, s)) return e;
+      d.preloaded = 1;
+    }
+    int l = 0;
+    const cudaError_t e = launch_delay_spin(d, slot, s, &l);
+    c->launches += l;
+    return e;
+  }
+};
+
+#define CUDA_OK(expr)                                                                   \
+  do {                                                                                  \
+    const cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(cemuUnhandledCudaError, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NCCL_OK(expr)                                                                       \
+  do {                                                                                      \
+    const ncclResult_t r_ = (expr);                                                         \
+    if (r_ != ncclSuccess)                                                                  \
+      return fail(static_cast<cemuResult_t>(r_),                                            \
+                  std::string(#expr) + ": " +                                               \
+                      (nccl()->GetErrorString ? nccl()->GetErrorString(r_) : "nccl error")); \
+  } while (0)
+
+// ---- shared helpers (comm.cpp) ----
+// Maps every real GPU's allocation `local` (collectively) into this process.
+cemuResult_t map_peers(cemuComm* c, void* local, size_t bytes, uint8_t** peers);
+cemuResult_t ensure_scratch(cemuComm* c, size_t bytes);
+// 20-bit signature of a fused call; every real rank must compute the same
+uint32_t op_sig(int coll, int dt, uint64_t count);
+const cemuComm::Region* find_region(const cemuComm* c, const void* p, size_t bytes);
+cemuResult_t check_common(cemuComm* c, int dt, const char* what);
+cemuResult_t check_op(int op, const char* what);
+FusedArgs fused_allreduce_args(const cemuComm* c, int dt, uint64_t count, uint64_t e0, uint8_t* const* src,
+                               uint8_t* const* dst);
+cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, cemuComm* c, cudaStream_t s,
+                          Phases& ph);
+cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuComm* c, cudaStream_t s,
+                          Phases& ph);
+
+template <typename A>
+void set_barrier(cemuComm* c, A& a) {
+  for (uint32_t g = 0; g < c->k; ++g) a.peer_flags[g] = reinterpret_cast<uint64_t*>(c->peer_sig[g]);
+  a.k = static_cast<int>(c->k);
+  a.me = static_cast<int>(c->li);
+  a.flags = reinterpret_cast<uint64_t*>(c->sig);
+  a.counter = reinterpret_cast<uint32_t*>(c->sig + 256);
+  a.error = reinterpret_cast<uint32_t*>(c->sig + 260);
+  a.epoch = reinterpret_cast<uint64_t*>(c->sig + 264);
+  a.timeout_ns = c->fused_timeout_ns;
+}
+
+// ---- host_pipe.cpp ----
+cemuResult_t host_allreduce(const void* send, void* recv, size_t count, int dt, cemuComm* c, cudaStream_t s);
+cemuResult_t host_allgather(const void* send, void* recv, size_t sc, int dt, cemuComm* c, cudaStream_t s);
+
+// ---- comm_wire.cpp ----
+cemuResult_t wire_call(cemuComm* c, int coll, const void* send, void* recv, uint64_t buf_bytes,
+                       uint64_t model_bytes, uint32_t es, cudaStream_t s);
+
+}  // namespace cemu_b200
