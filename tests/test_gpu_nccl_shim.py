@@ -51,3 +51,25 @@ def test_world_size_mismatch_is_reported(cuda, tmp_path):
                        env=dict(os.environ, CEMU_CONFIG=str(cfg), LD_PRELOAD=SHIM),
                        capture_output=True, text=True, timeout=120)
     assert r.returncode != 0 and "ncclCommInitRank" in r.stderr
+
+
+def test_shim_refuses_what_it_does_not_emulate(cuda, tmp_path):
+    """Entry points outside the emulated world fail loudly in the shim instead
+    of reaching the real libnccl with an emulated communicator; the config /
+    abort / registration entry points work."""
+    import ctypes as C
+    shim = C.CDLL(os.path.join(ROOT, "paper_2405_02969_b200", "libnccl_cemu.so"))
+    cfg = tmp_path / "job.cfg"
+    cfg.write_text("world_size = 4\nreal_ranks = 0\nbucket_bytes = 1\n")
+    os.environ["CEMU_CONFIG"] = str(cfg)
+    comm = C.c_void_p()
+    from paper_2405_02969_b200._capi import UniqueId
+    uid = UniqueId()  # passed by value, as ncclUniqueId is
+    assert shim.ncclCommInitRankConfig(C.byref(comm), 4, uid, 0, None) == 0
+    shim.ncclGetLastError.restype = C.c_char_p
+    assert shim.ncclSend(None, C.c_size_t(4), 7, 1, comm, None) == 5
+    assert b"point-to-point" in shim.ncclGetLastError(comm)
+    assert shim.ncclReduce(None, None, C.c_size_t(4), 7, 0, 0, comm, None) == 5
+    h = C.c_void_p(1)
+    assert shim.ncclCommRegister(comm, None, C.c_size_t(0), C.byref(h)) == 0 and not h.value
+    assert shim.ncclCommAbort(comm) == 0

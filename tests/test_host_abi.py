@@ -47,7 +47,8 @@ def test_nccl_interposer_exports_ncclapi():
     exported = {line.split()[-1] for line in out.splitlines()}
     for name in ("ncclAllReduce", "ncclAllGather", "ncclReduceScatter", "ncclBroadcast", "ncclCommInitRank",
                  "ncclCommDestroy", "ncclCommCount", "ncclCommUserRank", "ncclGetUniqueId", "ncclGroupStart",
-                 "ncclGroupEnd", "ncclGetErrorString"):
+                 "ncclGroupEnd", "ncclGetErrorString", "ncclCommInitRankConfig", "ncclCommAbort",
+                 "ncclCommRegister", "ncclCommDeregister", "ncclCommSplit", "ncclReduce", "ncclSend", "ncclRecv"):
         assert name in exported, name
 
 
