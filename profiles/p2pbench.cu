@@ -6,6 +6,22 @@
 __global__ void copyk(const uint4* __restrict__ s, uint4* d, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) d[i] = s[i];
 }
+struct u8x { uint32_t a[8]; };
+__device__ __forceinline__ u8x ld8(const u8x* p) {
+  u8x v; asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : "=r"(v.a[0]), "=r"(v.a[1]), "=r"(v.a[2]), "=r"(v.a[3]), "=r"(v.a[4]), "=r"(v.a[5]), "=r"(v.a[6]), "=r"(v.a[7]) : "l"(p)); return v;
+}
+__device__ __forceinline__ void st8(u8x* p, u8x v) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" :: "l"(p), "r"(v.a[0]), "r"(v.a[1]), "r"(v.a[2]), "r"(v.a[3]), "r"(v.a[4]), "r"(v.a[5]), "r"(v.a[6]), "r"(v.a[7]) : "memory");
+}
+__global__ void copy8(const u8x* s, u8x* d, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) st8(d + i, ld8(s + i));
+}
+__global__ void mix8(const u8x* peer_src, u8x* local_dst, const u8x* local_src, u8x* peer_dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    st8(local_dst + i, ld8(peer_src + i));
+    st8(peer_dst + i, ld8(local_src + i));
+  }
+}
 // mixed: pull half from peer into local, push other half from local to peer
 __global__ void mixk(const uint4* peer_src, uint4* local_dst, const uint4* local_src, uint4* peer_dst, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -45,6 +61,16 @@ int main() {
     run(nm, [&](int g) { copyk<<<sms * bps, 256, 0, st[g]>>>((const uint4*)a[g], (uint4*)b[1 - g], n); }, (double)bytes);
     snprintf(nm, 80, "mixed pull+push (half each) bps%d", bps);
     run(nm, [&](int g) { mixk<<<sms * bps, 256, 0, st[g]>>>((const uint4*)a[1 - g], (uint4*)b[g], (const uint4*)c[g], (uint4*)c[1 - g], n / 2); }, (double)bytes);
+  }
+  const uint64_t n8 = bytes / 32;
+  for (int bps : {4, 8}) {
+    char nm[80];
+    snprintf(nm, 80, "v8 pull bps%d", bps);
+    run(nm, [&](int g) { copy8<<<sms * bps, 256, 0, st[g]>>>((const u8x*)a[1 - g], (u8x*)b[g], n8); }, (double)bytes);
+    snprintf(nm, 80, "v8 push bps%d", bps);
+    run(nm, [&](int g) { copy8<<<sms * bps, 256, 0, st[g]>>>((const u8x*)a[g], (u8x*)b[1 - g], n8); }, (double)bytes);
+    snprintf(nm, 80, "v8 mixed bps%d", bps);
+    run(nm, [&](int g) { mix8<<<sms * bps, 256, 0, st[g]>>>((const u8x*)a[1 - g], (u8x*)b[g], (const u8x*)c[g], (u8x*)c[1 - g], n8 / 2); }, (double)bytes);
   }
   run("cudaMemcpyPeerAsync push", [&](int g) { cudaMemcpyPeerAsync(b[1 - g], 1 - g, a[g], g, bytes, st[g]); }, (double)bytes);
   return 0;
