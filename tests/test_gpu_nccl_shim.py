@@ -73,3 +73,26 @@ def test_shim_refuses_what_it_does_not_emulate(cuda, tmp_path):
     h = C.c_void_p(1)
     assert shim.ncclCommRegister(comm, None, C.c_size_t(0), C.byref(h)) == 0 and not h.value
     assert shim.ncclCommAbort(comm) == 0
+
+
+def test_integration_recipe_cpp_session(cuda, tmp_path):
+    """INTEGRATION.md's C++ drop-in for WorkerSession (tests/apps/
+    b200_session.cpp): host-span allreduce (int32 lanes) and allgather
+    (bytes) through the C-ABI, real rank 2 of a world of 6."""
+    app = os.path.join(ROOT, "tests", "apps", "b200_session")
+    cfg = tmp_path / "job.cfg"
+    cfg.write_text("world_size = 6\nreal_ranks = 2\nbucket_bytes = 65536\n")
+    n, blk, W, rank = 100003, 1000, 6, 2
+    out = tmp_path / "out.bin"
+    r = subprocess.run([app, str(cfg), str(rank), str(n), str(out)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert f"b200_session ok rank {rank} world {W}" in r.stdout
+    raw = np.fromfile(out, dtype=np.uint8)
+    got_ar = raw[:4 * n].view(np.int32)
+    got_ag = raw[4 * n:]
+    x = (np.arange(n, dtype=np.int64) * 7 + rank).astype(np.int32)
+    want_ar = P.allreduce(2, P.PAYLOAD_HASH, W, [rank], rank, 1, [x], n)
+    assert np.array_equal(got_ar, want_ar)
+    own = ((np.arange(blk) + rank + 1) % 256).astype(np.uint8)
+    want_ag = P.allgather(1, P.PAYLOAD_HASH, W, [rank], rank, 1, [own], blk)
+    assert np.array_equal(got_ag, want_ag)
