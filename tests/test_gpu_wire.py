@@ -17,6 +17,7 @@ on the GPU.  Checked:
 from __future__ import annotations
 
 import socket
+import time
 
 import numpy as np
 import pytest
@@ -48,6 +49,20 @@ def wire_config(W: int, alpha=500.0, beta=0.0001, gamma=0.0, kind="alpha_beta") 
     return "\n".join(lines) + "\n"
 
 
+def start_emulator(W: int, **kw):
+    """A reference emulator on fresh ports: the ports come from bind(0) and
+    are released before the emulator binds them, so another socket can take
+    one in between (a long test session); retry with new ones."""
+    last = None
+    for _ in range(5):
+        text = wire_config(W, **kw)
+        try:
+            return text, R.Emulator(text)
+        except R.RefError as e:
+            last = e
+    raise last
+
+
 def test_digests_agree_with_the_reference_parser(cuda):
     text = wire_config(8)
     assert pb.JobConfig.parse(text).digest == R.config_digest(text)
@@ -55,10 +70,10 @@ def test_digests_agree_with_the_reference_parser(cuda):
 
 @pytest.mark.parametrize("W", [2, 4, 8])
 def test_wire_allreduce_and_allgather_equal_the_reference_worker(cuda, W):
-    text = wire_config(W, alpha=50.0)
     count, sc = 4096 + 4 * W, 1000
     plan = [pb.CollectivePlanEntry("allreduce", count * 4, 4), pb.CollectivePlanEntry("allgather", sc, 1)]
-    with R.Emulator(text) as emu:
+    text, emu = start_emulator(W, alpha=50.0)
+    with emu:
         comm = pb.Communicator(text, 0, 0)
         comm.attach_emulator(plan)
         for it in range(2):  # op ids 0..3 over the two plan entries
@@ -80,6 +95,10 @@ def test_wire_allreduce_and_allgather_equal_the_reference_worker(cuda, W):
             R.emulated_collective(W, 1, ref, sc, 1)
             assert_bit_equal(to_np(full), ref, f"wire allgather W={W} it={it}")
         comm.close()  # BYE
+        # the emulator counts a session when its handler returns, just after the BYE
+        deadline = time.time() + 5
+        while emu.sessions < 1 and time.time() < deadline:
+            time.sleep(0.01)
         assert emu.sessions >= 1
 
 
@@ -88,10 +107,10 @@ def test_wire_float_buffer_folds_as_int32_lanes_like_the_reference(cuda):
     emulator's zero payload the result equals the device zero mode (-0.0
     kept, not turned into +0.0 by a float add)."""
     W = 4
-    text = wire_config(W, alpha=20.0)
     h = host_input(7, 8192, seed=3)
     h[::7] = -0.0
-    with R.Emulator(text):
+    text, emu = start_emulator(W, alpha=20.0)
+    with emu:
         comm = pb.Communicator(text, 0, 0)
         comm.attach_emulator([pb.CollectivePlanEntry("allreduce", h.numel() * 4, 4)])
         y = torch.empty(h.numel(), device="cuda")
@@ -107,9 +126,9 @@ def test_wire_float_buffer_folds_as_int32_lanes_like_the_reference(cuda):
 
 def test_reference_engine_releases_no_earlier_than_the_device_floors(cuda):
     W = 4
-    text = wire_config(W, alpha=3000.0, beta=0.001, gamma=0.0001)  # floors of several ms per step
+    text, emu = start_emulator(W, alpha=3000.0, beta=0.001, gamma=0.0001)  # floors of several ms per step
     nbytes = 1 << 16
-    with R.Emulator(text):
+    with emu:
         comm = pb.Communicator(text, 0, 0)
         comm.attach_emulator([pb.CollectivePlanEntry("allreduce", nbytes, 4)])
         x = torch.zeros(nbytes // 4, dtype=torch.int32, device="cuda")
@@ -135,8 +154,8 @@ def test_reference_engine_releases_no_earlier_than_the_device_floors(cuda):
 
 def test_wire_mode_errors_are_loud(cuda):
     W = 4
-    text = wire_config(W)
-    with R.Emulator(text):
+    text, emu = start_emulator(W)
+    with emu:
         comm = pb.Communicator(text, 0, 0)
         comm.attach_emulator([pb.CollectivePlanEntry("allreduce", 64, 4)])
         x = torch.zeros(16, dtype=torch.int32, device="cuda")
