@@ -26,12 +26,16 @@ def _port():
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
-def test_multi_gpu_collectives_match_oracle():
+@pytest.mark.parametrize("kmax", ["auto", "8"])
+def test_multi_gpu_collectives_match_oracle(kmax):
+    """kmax=8 forces the fused kernels' 8-GPU instantiation at any k, so a
+    2- or 4-GPU box runs the code an 8-GPU job would."""
     n = min(torch.cuda.device_count(), 4)
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "mgpu_worker.py")
+    env = dict(os.environ, **({"CEMU_FUSED_KMAX": "8"} if kmax == "8" else {}))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                         "--master-addr", "127.0.0.1", "--master-port", str(_port()), worker],
-                       capture_output=True, text=True, timeout=420)
+                       capture_output=True, text=True, timeout=420, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"MGPU OK {n}" in r.stdout
 
