@@ -72,27 +72,65 @@ def workload(args, n):
 REF_SAMPLE_MIB = 64  # the reference's 64 MiB frame cap rejects 1 GiB at world 8
 
 
-def time_reference(steps: int, warmup: int, world: int):
+def time_reference_parallel(steps: int, warmup: int, world: int, sessions: int):
+    """`sessions` independent reference emulated allreduces at once (each its
+    own WorkerSession + EmulatorServer, 5 threads; ctypes releases the GIL),
+    started together; aggregate = sum of the per-session throughputs of
+    their timed calls, which all overlap."""
+    import threading
+
     import numpy as np
     from oracle import ref
     sample = REF_SAMPLE_MIB << 20
-    buf = np.random.default_rng(1).integers(0, 2**31, size=sample // 4, dtype=np.int64).astype(np.int32)
-    times = ref.emulated_collective(world, 0, buf, sample, 4, kind=0, warmup=warmup, reps=steps)
-    mean_us = float(np.mean(times))
-    return {"value": 2 * sample / (mean_us * 1e-6) / 1e9, "mean_ms": mean_us / 1e3,
-            "best_ms": float(np.min(times)) / 1e3, "sample_bytes": sample, "calls": steps}
+    bufs = [np.random.default_rng(i + 1).integers(0, 2**31, size=sample // 4, dtype=np.int64).astype(np.int32)
+            for i in range(sessions)]
+    out = [None] * sessions
+    gate = threading.Barrier(sessions)
+
+    def worker(i):
+        gate.wait()
+        for _ in range(3):  # a loopback port picked by bind(0) can be taken in between: retry
+            try:
+                out[i] = ref.emulated_collective(world, 0, bufs[i], sample, 4, kind=0, warmup=warmup, reps=steps)
+                return
+            except ref.RefError:
+                continue
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(sessions)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    done = [o for o in out if o is not None]
+    means = [float(np.mean(o)) for o in done]
+    return {"value": sum(2 * sample / (m * 1e-6) / 1e9 for m in means), "sessions": len(done),
+            "mean_ms": float(np.mean(means)) / 1e3, "sample_bytes": sample, "calls": steps * len(done)}
+
+
+def best_reference(steps: int, warmup: int, world: int):
+    """One session, and as many as the host's cores carry (each session keeps
+    2-3 of its 5 threads busy); the better aggregate is the baseline."""
+    cpus = os.cpu_count() or 1
+    runs = [time_reference_parallel(steps, warmup, world, 1)]
+    for many in sorted({max(1, cpus // 3), max(1, cpus // 2)} - {1}):
+        runs.append(time_reference_parallel(steps, warmup, world, many))
+    best = max(runs, key=lambda r: r["value"])
+    best["tried"] = {r["sessions"]: round(r["value"], 3) for r in runs}
+    return best
 
 
 def cpu_baseline_block(steps: int, warmup: int, world: int):
     from oracle import ref
     if ref.available():
-        r = time_reference(steps, warmup, world)
-        return {"value": round(r["value"], 4), "unit": UNIT, "cores": 5, "kind": "reference",
+        r = best_reference(steps, warmup, world)
+        return {"value": round(r["value"], 4), "unit": UNIT, "cores": min(os.cpu_count() or 1, 5 * r["sessions"]),
+                "kind": "reference",
                 "sample": (f"reference cemu WorkerSession(rank 0) + in-thread EmulatorServer over loopback "
                            f"TCP, world {world}, {REF_SAMPLE_MIB} MiB elem_size=4 allreduce (1 GiB exceeds its "
-                           f"64 MiB frame cap at world 8), {steps} timed calls after {warmup} warm-up; "
-                           f"mean {r['mean_ms']:.1f} ms/call, best {r['best_ms']:.1f} ms; 5 threads "
-                           f"(engine, reader, acceptor, emulator receive, poller) on a {os.cpu_count()}-core host"),
+                           f"64 MiB frame cap at world 8), {steps} timed calls after {warmup} warm-up per "
+                           f"session; {r['sessions']} concurrent independent sessions (5 threads each: engine, "
+                           f"reader, acceptor, emulator receive, poller) on a {os.cpu_count()}-core host, "
+                           f"aggregate GB/s by sessions tried: {r['tried']}; mean {r['mean_ms']:.1f} ms/call"),
                 "mean_ms_per_call": round(r["mean_ms"], 3)}
     # the port, single thread (only if the reference was never built)
     import numpy as np
@@ -114,10 +152,13 @@ def run_reference_arm(args, rank):
     world = RANKS_PER_GPU * n
     from oracle import ref
     if ref.available():
-        r = time_reference(args.steps, args.warmup, world)
-        cb = {"value": round(r["value"], 4), "unit": UNIT, "cores": 5, "kind": "reference",
+        r = best_reference(args.steps, args.warmup, world)
+        cb = {"value": round(r["value"], 4), "unit": UNIT, "cores": min(os.cpu_count() or 1, 5 * r["sessions"]),
+              "kind": "reference",
               "sample": (f"each step = one reference emulated allreduce of {REF_SAMPLE_MIB} MiB (elem_size 4) "
-                         f"at world {world} over loopback TCP; 1 GiB exceeds the reference's 64 MiB frame cap")}
+                         f"at world {world} over loopback TCP, in each of {r['sessions']} concurrent independent "
+                         f"sessions (all the host threads they can use; aggregate GB/s by sessions tried: "
+                         f"{r['tried']}); 1 GiB exceeds the reference's 64 MiB frame cap")}
     else:
         cb = cpu_baseline_block(args.steps, args.warmup, world)
         r = {"mean_ms": None}
