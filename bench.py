@@ -107,9 +107,15 @@ def time_reference_parallel(steps: int, warmup: int, world: int, sessions: int):
             "mean_ms": float(np.mean(means)) / 1e3, "sample_bytes": sample, "calls": steps * len(done)}
 
 
+REF_CALLS_CAP, REF_WARMUP_CAP = 20, 2  # per session: keeps the arm to well under a minute
+
+
 def best_reference(steps: int, warmup: int, world: int):
     """One session, and as many as the host's cores carry (each session keeps
-    2-3 of its 5 threads busy); the better aggregate is the baseline."""
+    2-3 of its 5 threads busy); the better aggregate is the baseline.  Each
+    session times min(steps, 20) calls after min(warmup, 2) warm-up calls (a
+    bounded sample: the whole arm stays well under a minute for any K)."""
+    steps, warmup = max(1, min(steps, REF_CALLS_CAP)), min(warmup, REF_WARMUP_CAP)
     cpus = os.cpu_count() or 1
     runs = [time_reference_parallel(steps, warmup, world, 1)]
     for many in sorted({max(1, cpus // 3), max(1, cpus // 2)} - {1}):

@@ -31,6 +31,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <mutex>
 #include <set>
 #include <span>
 #include <string>
@@ -318,6 +319,12 @@ int ref_emulated_collective(uint32_t n, int coll, uint8_t* buf,
                             double a, double b, double g, double fixed,
                             double inject, int warmup, int reps,
                             double* times_us, char* err, size_t errcap) {
+  // Concurrent callers (the bench's multi-session reference arm): choosing
+  // loopback ports, binding the emulator and the worker's listener, and the
+  // handshake happen under one process-wide lock, so two sessions can never
+  // pick the same port; the timed calls run unlocked.
+  static std::mutex setup_mu;
+  std::unique_lock<std::mutex> setup(setup_mu);
   try {
     const DelayModelParams d = delay_params(kind, a, b, g, fixed, inject);
     const JobConfig cfg = make_cfg(n, /*emulated=*/true, d);
@@ -330,6 +337,7 @@ int ref_emulated_collective(uint32_t n, int coll, uint8_t* buf,
       std::vector<CollectivePlanEntry> plan = {
           {coll_of(coll), plan_bytes, elem}};
       WorkerSession s(cfg, 0, plan);
+      setup.unlock();
       const uint64_t len = coll == 0 ? plan_bytes : plan_bytes * n;
       std::span<uint8_t> sp(buf, len);
       for (int i = 0; i < warmup + reps; ++i) {
@@ -348,11 +356,13 @@ int ref_emulated_collective(uint32_t n, int coll, uint8_t* buf,
     } catch (const std::exception& e) {
       failure = e.what();
     }
+    if (setup.owns_lock()) setup.unlock();
     server.request_stop();
     th.join();
     if (!failure.empty()) throw std::runtime_error(failure);
     return 0;
   } catch (const std::exception& e) {
+    if (setup.owns_lock()) setup.unlock();
     put_err(err, errcap, e.what());
     return -1;
   }
