@@ -14,7 +14,6 @@ from __future__ import annotations
 import os
 import time
 
-import numpy as np
 import pytest
 import torch
 
