@@ -201,3 +201,15 @@ def test_ring_order_is_ascending_and_involutive():
     for r in range(4):
         assert L.cemuRingSuccessor(4, L.cemuRingPredecessor(4, r)) == r
     assert L.cemuRingSuccessor(2, 0) == 1 and L.cemuRingSuccessor(2, 1) == 0
+
+
+def test_exerciser_host_hash_equals_the_library_spec():
+    """coll.py's vectorised payload words (its verify mode's expectation)
+    equal cemuPayloadWord, including word indices past 2^32."""
+    from paper_2405_02969_b200 import coll
+    rng = random.Random(11)
+    for _ in range(20):
+        key = S.payload_key(rng.randrange(1 << 40), rng.randrange(4096))
+        j0 = rng.choice([0, rng.randrange(1 << 31), (1 << 32) - 3, rng.randrange(1 << 40)])
+        w = coll.payload_words(key, j0, 8)
+        assert [int(v) for v in w] == [S.payload_word(key, j0 + i) for i in range(8)]
