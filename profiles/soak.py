@@ -45,16 +45,16 @@ while True:
             s_ = torch.zeros(count * W, dtype=TORCH[dt], device="cuda"); o = torch.empty(count, dtype=TORCH[dt], device="cuda")
             comm.reduce_scatter(s_, o)
     # one checked call
-    sends = [host_input(dt, count, seed=calls + i) for i in range(n)]
+    if dt in (7, 9) and n > 1:  # dyadic (<= 5 significant bits): any real-part order sums exactly
+        sends = [torch.from_numpy((np.random.default_rng(calls + i).integers(-16, 16, size=count) / 8)
+                                  .astype(np.float32)).to(TORCH[dt]) for i in range(n)]
+    else:
+        sends = [host_input(dt, count, seed=calls + i) for i in range(n)]
     y = torch.empty(count, dtype=TORCH[dt], device="cuda")
     comm.all_reduce(sends[local].cuda(), y)
     torch.cuda.synchronize()
     want = P.allreduce(dt, P.PAYLOAD_HASH, W, real, local, 1, [to_np(s) for s in sends], count)
-    if dt in (7, 9) and n > 1:  # NCCL's real-part order: compare within tolerance
-        got = y.float().cpu().numpy(); w = torch.from_numpy(want.view(np.int16) if dt == 9 else want).view(TORCH[dt]).float().numpy()
-        assert np.allclose(got, w, rtol=1e-2 if dt == 9 else 1e-6, atol=1e-2 if dt == 9 else 1e-6)
-    else:
-        assert_bit_equal(to_np(y), want, f"soak call {calls}")
+    assert_bit_equal(to_np(y), want, f"soak call {calls}")
     checks += 1; calls += 1
 torch.cuda.synchronize()
 assert comm.async_error() is None
