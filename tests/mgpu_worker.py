@@ -97,6 +97,21 @@ def run():
                     rs = to_np(sends[real.index(root)]) if root in real else None
                     want = P.broadcast(dt, P.PAYLOAD_HASH, W, real, me, root, 1, rs, count)
                     assert_bit_equal(to_np(b), want, f"broadcast root={root} dt={dt}")
+        # NCCL path (plain buffers) with arbitrary floats: the real part is
+        # summed in NCCL's order, so the result is held to the north star's
+        # tolerances (fp32 1e-6, bf16 1e-2), relative to the inputs' magnitude
+        for dt, rtol in ((7, 1e-6), (9, 1e-2)):
+            count = 3 * 4096 + 7
+            sends = [torch.from_numpy(np.random.default_rng(900 + i).standard_normal(count).astype(np.float32) * 3)
+                     .to(TORCH[dt]) for i in range(n)]
+            y = torch.empty(count, dtype=TORCH[dt], device="cuda")
+            comm.all_reduce(sends[local].cuda(), y)
+            torch.cuda.synchronize()
+            want = P.allreduce(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(s) for s in sends], count)
+            w = torch.from_numpy(want.view(np.int16) if dt == 9 else want).view(TORCH[dt]).double().numpy()
+            g = y.double().cpu().numpy()
+            scale = sum(np.abs(s.double().numpy()) for s in sends) + np.abs(w) + 1.0
+            assert np.max(np.abs(g - w) / scale) <= rtol, (dt, float(np.max(np.abs(g - w) / scale)))
         # host-buffer allreduce: chunks pipelined through symmetric pipe buffers,
         # one fused kernel per chunk (1 MiB chunks: the buffers rotate)
         for dt in (7, 9, 2):
