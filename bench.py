@@ -118,7 +118,7 @@ def best_reference(steps: int, warmup: int, world: int):
     steps, warmup = max(1, min(steps, REF_CALLS_CAP)), min(warmup, REF_WARMUP_CAP)
     cpus = os.cpu_count() or 1
     runs = [time_reference_parallel(steps, warmup, world, 1)]
-    for many in sorted({max(1, cpus // 3), max(1, cpus // 2)} - {1}):
+    for many in sorted({min(16, max(1, cpus // 3)), min(16, max(1, cpus // 2))} - {1}):  # <= 16 sessions
         runs.append(time_reference_parallel(steps, warmup, world, many))
     best = max(runs, key=lambda r: r["value"])
     best["tried"] = {r["sessions"]: round(r["value"], 3) for r in runs}
