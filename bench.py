@@ -72,39 +72,67 @@ def workload(args, n):
 REF_SAMPLE_MIB = 64  # the reference's 64 MiB frame cap rejects 1 GiB at world 8
 
 
+REF_SESSION_DEADLINE_S = 60.0  # a session stalled past this is killed (see oracle/ref_session.py)
+
+
+def _run_ref_sessions(steps: int, warmup: int, world: int, sessions: int, sample: int):
+    """Starts `sessions` reference sessions as processes, releases them
+    together once all are ready, and collects their per-call times; a session
+    still running at the deadline is killed and counted as stalled."""
+    root = os.path.dirname(os.path.abspath(__file__))
+    procs = [subprocess.Popen([sys.executable, "-m", "oracle.ref_session", str(world), str(warmup), str(steps),
+                               str(i + 1), str(sample)], cwd=root, stdin=subprocess.PIPE,
+                              stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+             for i in range(sessions)]
+    try:
+        for p in procs:
+            if p.stdout.readline().strip() != "ready":
+                raise RuntimeError("reference session failed to start")
+        for p in procs:
+            p.stdin.write("go\n")
+            p.stdin.flush()
+        deadline = time.monotonic() + REF_SESSION_DEADLINE_S
+        times, stalled = [], 0
+        for p in procs:
+            try:
+                out, _ = p.communicate(timeout=max(0.1, deadline - time.monotonic()))
+            except subprocess.TimeoutExpired:
+                stalled += 1
+                continue
+            try:
+                t = json.loads(out.strip().splitlines()[-1])
+            except (ValueError, IndexError):
+                continue
+            if isinstance(t, list) and t:
+                times.append(t)
+        return times, stalled
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+                p.wait()
+
+
 def time_reference_parallel(steps: int, warmup: int, world: int, sessions: int):
     """`sessions` independent reference emulated allreduces at once (each its
-    own WorkerSession + EmulatorServer, 5 threads; ctypes releases the GIL),
-    started together; aggregate = sum of the per-session throughputs of
-    their timed calls, which all overlap."""
-    import threading
-
+    own process: WorkerSession + EmulatorServer, 5 threads), started
+    together; aggregate = sum of the per-session throughputs of their timed
+    calls, which all overlap.  A run with a stalled session is repeated once;
+    stalls are reported, never hidden."""
     import numpy as np
-    from oracle import ref
     sample = REF_SAMPLE_MIB << 20
-    bufs = [np.random.default_rng(i + 1).integers(0, 2**31, size=sample // 4, dtype=np.int64).astype(np.int32)
-            for i in range(sessions)]
-    out = [None] * sessions
-    gate = threading.Barrier(sessions)
-
-    def worker(i):
-        gate.wait()
-        for _ in range(3):  # a loopback port picked by bind(0) can be taken in between: retry
-            try:
-                out[i] = ref.emulated_collective(world, 0, bufs[i], sample, 4, kind=0, warmup=warmup, reps=steps)
-                return
-            except ref.RefError:
-                continue
-
-    th = [threading.Thread(target=worker, args=(i,)) for i in range(sessions)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    done = [o for o in out if o is not None]
+    stalls = 0
+    for _ in range(2):
+        done, stalled = _run_ref_sessions(steps, warmup, world, sessions, sample)
+        stalls += stalled
+        if not stalled and len(done) == sessions:
+            break
+    if not done:
+        raise RuntimeError(f"no reference session completed ({stalls} stalled)")
     means = [float(np.mean(o)) for o in done]
     return {"value": sum(2 * sample / (m * 1e-6) / 1e9 for m in means), "sessions": len(done),
-            "mean_ms": float(np.mean(means)) / 1e3, "sample_bytes": sample, "calls": steps * len(done)}
+            "mean_ms": float(np.mean(means)) / 1e3, "sample_bytes": sample, "calls": steps * len(done),
+            "stalled": stalls}
 
 
 REF_CALLS_CAP, REF_WARMUP_CAP = 20, 2  # per session: keeps the arm to well under a minute
@@ -117,11 +145,18 @@ def best_reference(steps: int, warmup: int, world: int):
     bounded sample: the whole arm stays well under a minute for any K)."""
     steps, warmup = max(1, min(steps, REF_CALLS_CAP)), min(warmup, REF_WARMUP_CAP)
     cpus = os.cpu_count() or 1
-    runs = [time_reference_parallel(steps, warmup, world, 1)]
-    for many in sorted({min(16, max(1, cpus // 3)), min(16, max(1, cpus // 2))} - {1}):  # <= 16 sessions
-        runs.append(time_reference_parallel(steps, warmup, world, many))
+    runs, failed = [], 0
+    for many in sorted({1, min(16, max(1, cpus // 3)), min(16, max(1, cpus // 2))}):  # <= 16 sessions
+        try:
+            runs.append(time_reference_parallel(steps, warmup, world, many))
+        except RuntimeError:  # every session of that run stalled twice
+            failed += 2 * many
+    if not runs:
+        raise RuntimeError("every reference session stalled")
+    runs[0]["stalled"] += failed
     best = max(runs, key=lambda r: r["value"])
     best["tried"] = {r["sessions"]: round(r["value"], 3) for r in runs}
+    best["stalled_total"] = sum(r["stalled"] for r in runs)
     return best
 
 
@@ -131,12 +166,14 @@ def cpu_baseline_block(steps: int, warmup: int, world: int):
         r = best_reference(steps, warmup, world)
         return {"value": round(r["value"], 4), "unit": UNIT, "cores": min(os.cpu_count() or 1, 5 * r["sessions"]),
                 "kind": "reference",
-                "sample": (f"reference cemu WorkerSession(rank 0) + in-thread EmulatorServer over loopback "
+                "sample": (f"reference cemu WorkerSession(rank 0) + EmulatorServer over loopback "
                            f"TCP, world {world}, {REF_SAMPLE_MIB} MiB elem_size=4 allreduce (1 GiB exceeds its "
                            f"64 MiB frame cap at world 8), {steps} timed calls after {warmup} warm-up per "
-                           f"session; {r['sessions']} concurrent independent sessions (5 threads each: engine, "
+                           f"session; {r['sessions']} concurrent independent session processes (5 threads each: engine, "
                            f"reader, acceptor, emulator receive, poller) on a {os.cpu_count()}-core host, "
-                           f"aggregate GB/s by sessions tried: {r['tried']}; mean {r['mean_ms']:.1f} ms/call"),
+                           f"aggregate GB/s by sessions tried: {r['tried']}; mean {r['mean_ms']:.1f} ms/call; "
+                           f"{r['stalled_total']} session(s) stalled in the reference transport and were killed "
+                           f"after {REF_SESSION_DEADLINE_S:.0f} s and re-run"),
                 "mean_ms_per_call": round(r["mean_ms"], 3)}
     # the port, single thread (only if the reference was never built)
     import numpy as np
@@ -163,8 +200,10 @@ def run_reference_arm(args, rank):
               "kind": "reference",
               "sample": (f"each step = one reference emulated allreduce of {REF_SAMPLE_MIB} MiB (elem_size 4) "
                          f"at world {world} over loopback TCP, in each of {r['sessions']} concurrent independent "
-                         f"sessions (all the host threads they can use; aggregate GB/s by sessions tried: "
-                         f"{r['tried']}); 1 GiB exceeds the reference's 64 MiB frame cap")}
+                         f"session processes (all the host threads they can use; aggregate GB/s by sessions tried: "
+                         f"{r['tried']}; {r['stalled_total']} session(s) stalled in the reference transport, killed "
+                         f"after {REF_SESSION_DEADLINE_S:.0f} s and re-run); 1 GiB exceeds the reference's 64 MiB "
+                         f"frame cap")}
     else:
         cb = cpu_baseline_block(args.steps, args.warmup, world)
         r = {"mean_ms": None}
