@@ -159,6 +159,26 @@ def test_host_delay_new_models_equal_oracle():
         assert S.call_latency_us(m1, coll, n, nbytes, k) == P.call_latency_us(m2, coll, n, nbytes, k)
 
 
+def test_c3_config_and_hierarchical_latency():
+    """BASELINE config 3 as paper_2405_02969_b200.c3 builds it: 128 ranks =
+    16 nodes x 8 GPUs, this node's k GPUs real; the host's hierarchical
+    latency equals the oracle's and the model the B200 run recorded
+    (profiles/r01_c3.json: 186 / 667 / 2135 us at 1 / 64 / 256 MiB)."""
+    from paper_2405_02969_b200 import c3
+    from paper_2405_02969_b200.fsdp import NET
+    for k in (1, 2, 4):
+        cfg = pb.JobConfig.parse(c3.config(k, True))
+        assert cfg.world_size == 128 and cfg.real_ranks == list(range(k))
+        assert "collective_algo = hierarchical" in cfg.render() and "topology.gpus_per_node = 8" in cfg.render()
+        args = (S.ALPHA_BETA, S.HIERARCHICAL, NET["alpha_inter_us"], NET["beta_inter_us_per_byte"],
+                NET["gamma_us_per_byte"], 0.0, 0.0, 8, NET["alpha_intra_us"], NET["beta_intra_us_per_byte"])
+        m1, m2 = S.delay_model(*args), P.delay_model(*args)
+        steps = S.to_real_count(S.ALLREDUCE, 128, list(range(k)))
+        for mib, want in ((1, 186), (64, 667), (256, 2135)):
+            got = S.call_latency_us(m1, S.ALLREDUCE, 128, mib << 20, steps)
+            assert got == P.call_latency_us(m2, S.ALLREDUCE, 128, mib << 20, steps) == want, (k, mib, got)
+
+
 def test_host_payload_equals_oracle():
     for key, j, word in golden("payload.json")["words"]:
         assert S.payload_word(key, j) == word
