@@ -333,6 +333,16 @@ cemuResult_t cemuSpinUs(cemuStream_t stream, uint64_t us);
  * deadline + us, so launch gaps do not accumulate.  resync != 0 restarts the
  * chain at this kernel's start (use after a cross-stream wait). */
 cemuResult_t cemuSpinChainUs(cemuStream_t stream, uint64_t us, int64_t* deviceChain, int resync);
+/* The join after a cross-stream wait on a collective: in stream order,
+ * *deviceChain = max(*deviceChain, *deviceOther).  With deviceOther = the
+ * collective's release end (cemuCommLastReleaseEnd) the compute timeline
+ * continues from the later of the two, instead of from the next kernel's
+ * start after the event-to-kernel gap (resync). */
+cemuResult_t cemuChainJoin(cemuStream_t stream, int64_t* deviceChain, const int64_t* deviceOther);
+/* Device word (%globaltimer ns) holding the release end of the last delayed
+ * call enqueued on `comm`; *out = NULL when the delay is off.  The word is
+ * rewritten 64 calls later (the record ring). */
+cemuResult_t cemuCommLastReleaseEnd(cemuComm_t comm, const int64_t** out);
 
 #ifdef __cplusplus
 }

@@ -269,4 +269,12 @@ cemuResult_t cemuSpinChainUs(cemuStream_t stream, uint64_t us, int64_t* chain, i
              : cemuUnhandledCudaError;
 }
 
+cemuResult_t cemuChainJoin(cemuStream_t stream, int64_t* chain, const int64_t* other) {
+  if (!chain || !other) return cemuInvalidArgument;
+  int l = 0;
+  return launch_chain_join(chain, other, reinterpret_cast<cudaStream_t>(stream), &l) == cudaSuccess
+             ? cemuSuccess
+             : cemuUnhandledCudaError;
+}
+
 }  // extern "C"

@@ -20,6 +20,7 @@
 // Shared declarations: comm_internal.hpp; the host-buffer pipeline lives in
 // host_pipe.cpp, wire mode in comm_wire.cpp.
 #include "comm_internal.hpp"
+#include "harness.hpp"
 
 namespace cemu_b200 {
 
@@ -635,6 +636,10 @@ cemuResult_t run_or_defer(cemuComm* c, F&& plan) {
   return cemuSuccess;
 }
 
+const int64_t* stream_release_end(cemuComm_t c, cudaStream_t s) {
+  return (c && c->last_slot && c->last_stream == s) ? c->last_slot + 1 : nullptr;
+}
+
 }  // namespace cemu_b200
 
 // =============================================================================
@@ -1059,3 +1064,9 @@ int cemuCommEventLog(cemuComm_t c, uint64_t id, char* out, size_t cap) {
 // launch counter for bench.py's gpu_launches (not part of the public header)
 
 extern "C" uint64_t cemuCommKernelLaunches(cemuComm_t c) { return c ? c->launches : 0; }
+
+extern "C" cemuResult_t cemuCommLastReleaseEnd(cemuComm_t c, const int64_t** out) {
+  if (!c || !out) return cemuInvalidArgument;
+  *out = c->last_slot ? c->last_slot + 1 : nullptr;
+  return cemuSuccess;
+}

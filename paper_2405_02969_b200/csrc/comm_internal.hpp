@@ -110,6 +110,10 @@ struct cemuComm {
     int64_t latency = 0;
   } meta[kSlots];
   uint64_t calls = 0;
+  // the previous delayed call's record slot and stream: a call queued right
+  // behind it on the same stream starts when it ended (queue_gap_ns())
+  int64_t* last_slot = nullptr;
+  cudaStream_t last_stream = nullptr;
   ncclComm_t inner = nullptr;
   uint64_t launches = 0;
   // fused multi-GPU path (k > 1): IPC-mapped signal areas and symmetric buffers
@@ -271,9 +275,13 @@ struct Call {
       if (const cudaError_t e = cudaEventRecord(ev, s)) return e;
       d.preloaded = 1;
     }
+    d.prev_end = (c->last_slot && c->last_stream == s) ? c->last_slot + 1 : nullptr;
+    d.queue_gap_ns = queue_gap_ns();
     int l = 0;
     const cudaError_t e = launch_delay_spin(d, slot, s, &l);
     c->launches += l;
+    c->last_slot = slot;
+    c->last_stream = s;
     return e;
   }
 };

@@ -191,7 +191,14 @@ std::vector<IterTrace> run_training_loop(cemuComm_t comm, const ModelSpec& m, ui
     // last event implies every bucket
     if (nb) {
       CK(cudaStreamWaitEvent(compute, E[3 + 2 * (nb - 1)], 0));
-      resync = true;  // the compute stream may have waited on the network
+      // the compute stream may have waited on the network: continue the
+      // chain from the later of the two timelines (or from the next
+      // kernel's own start when the network end is not on the device)
+      if (const int64_t* net_end = resync ? nullptr : stream_release_end(comm, net)) {
+        CK(launch_chain_join(chain, net_end, compute, &spins));
+      } else {
+        resync = true;
+      }
     }
     compute_us(m.update_us);
     CK(cudaEventRecord(E[1], compute));

@@ -68,4 +68,8 @@ std::vector<IterTrace> run_training_loop(cemuComm_t comm, const ModelSpec& m,
 double predicted_iteration_us(const ModelSpec& m, uint64_t bucket_bytes,
                               const std::vector<double>& bucket_latency_us);
 
+// Device word holding the end (%globaltimer ns) of the last delayed call
+// `comm` enqueued on `stream`, or null (delay off, or another stream).
+const int64_t* stream_release_end(cemuComm_t comm, cudaStream_t stream);
+
 }  // namespace cemu_b200

@@ -1011,14 +1011,28 @@ __global__ void spin_ns_kernel(int64_t ns, int64_t* chain, int resync) {
   if (chain) *chain = end;
 }
 
+// Join of two timelines: the compute chain continues from the later of its
+// own deadline and the network's last release (the wait-all of a training
+// step), so the event-to-kernel gap after a cross-stream wait is not added to
+// the emulated compute.
+__global__ void chain_join_kernel(int64_t* chain, const int64_t* other) {
+  const int64_t o = *other;
+  if (o > *chain) *chain = o;
+}
+
 __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int64_t* slot) {
   int64_t* floors = slot + kSlotHeader;
   int64_t* release = floors + d.kmax;
   double* offs = reinterpret_cast<double*>(release + d.kmax);
   __shared__ int64_t t0_s;
   if (threadIdx.x == 0) {
-    t0_s = d.self_stamp ? globaltimer_ns() : slot[0];
-    if (d.self_stamp) slot[0] = t0_s;
+    int64_t t0 = d.self_stamp ? globaltimer_ns() : slot[0];
+    if (d.prev_end) {
+      const int64_t pe = *d.prev_end;
+      if (pe > 0 && t0 >= pe && t0 - pe <= d.queue_gap_ns) t0 = pe;
+    }
+    t0_s = t0;
+    slot[0] = t0;
   }
   // Evaluate the model on the device: delay.cpp:23-47 offsets and
   // engine.cpp:41 llround floors, strided over the block.  A delay-model
@@ -1489,6 +1503,20 @@ cudaError_t launch_spin_ns(int64_t ns, cudaStream_t s, int* launches, int64_t* c
   ++*launches;
   spin_ns_kernel<<<1, 1, 0, s>>>(ns, chain, resync ? 1 : 0);
   return cudaGetLastError();
+}
+
+cudaError_t launch_chain_join(int64_t* chain, const int64_t* other, cudaStream_t s, int* launches) {
+  ++*launches;
+  chain_join_kernel<<<1, 1, 0, s>>>(chain, other);
+  return cudaGetLastError();
+}
+
+int64_t queue_gap_ns() {
+  static const int64_t gap = [] {
+    const char* e = std::getenv("CEMU_QUEUE_GAP_US");
+    return e ? std::max<int64_t>(0, std::atoll(e)) * 1000 : int64_t{10'000};
+  }();
+  return gap;
 }
 
 cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t s, int* launches) {

@@ -30,7 +30,21 @@ struct DelayLaunch {
   uint32_t kmax;
   int32_t self_stamp;  // 1: this kernel records t_start itself
   int32_t preloaded;   // 1: the K offsets are already in the slot (a delay-model plugin's)
+  // Back-to-back calls on one stream: the end time (slot[1]) of the previous
+  // delayed call on this stream, or null.  A call whose start lies within
+  // queue_gap_ns after it was queued behind that call, and its network time
+  // starts at that end rather than after the emulator's own kernel-dispatch
+  // gap (an in-order channel starts the next collective when the previous
+  // one leaves the wire).
+  const int64_t* prev_end;
+  int64_t queue_gap_ns;
 };
+
+// *chain = max(*chain, *other) in stream order (one 1-thread kernel).
+cudaError_t launch_chain_join(int64_t* chain, const int64_t* other, cudaStream_t stream, int* launches);
+
+// CEMU_QUEUE_GAP_US (default 10 us; 0 disables the back-to-back chaining)
+int64_t queue_gap_ns();
 
 // dst[i] = src[i] (+) sum over `nkeys` emulated peers of their payload at
 // element elem_base + i.  src may equal dst.  Returns the number of kernel

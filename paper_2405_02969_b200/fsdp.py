@@ -31,6 +31,8 @@ import math
 import numpy as np
 
 from ._capi import lib
+
+C_VOID = C.c_void_p
 from . import whatif as _whatif  # noqa: F401  (declares cemuSpinChainUs / cemuCommModelLatencyUs)
 
 LLAMA3_8B = {"hidden": 4096, "intermediate": 14336, "layers": 32, "heads": 32, "kv_heads": 8,
@@ -144,7 +146,9 @@ def run_trace(comm, plan, iterations: int = 2, device: int = 0):
         fn()
         d = torch.cuda.Event()
         d.record(net)
-        return d
+        end = C_VOID()
+        lib.cemuCommLastReleaseEnd(comm._h, C.byref(end))
+        return d, end
 
     def ag(i):
         s = plan[i]["shard"]
@@ -155,8 +159,14 @@ def run_trace(comm, plan, iterations: int = 2, device: int = 0):
         return lambda: comm.reduce_scatter(full[:s * W], rs_out[:s], stream=net)
 
     def wait(d):
-        compute.wait_event(d)
-        state["resync"] = True
+        ev, end = d
+        compute.wait_event(ev)
+        if end.value and not state["resync"]:
+            # continue the compute chain from max(its deadline, the
+            # collective's release end), not after the event-to-kernel gap
+            lib.cemuChainJoin(compute.cuda_stream, C.c_void_p(chain.data_ptr()), end)
+        else:
+            state["resync"] = True
 
     starts, ends = [], []
     for _ in range(iterations):

@@ -55,6 +55,10 @@ lib.cemuSpinUs.restype = C.c_int
 lib.cemuSpinUs.argtypes = [C_VOID, C.c_uint64]
 lib.cemuSpinChainUs.restype = C.c_int
 lib.cemuSpinChainUs.argtypes = [C_VOID, C.c_uint64, C_VOID, C.c_int]
+lib.cemuChainJoin.restype = C.c_int
+lib.cemuChainJoin.argtypes = [C_VOID, C_VOID, C_VOID]
+lib.cemuCommLastReleaseEnd.restype = C.c_int
+lib.cemuCommLastReleaseEnd.argtypes = [C_VOID, C.POINTER(C_VOID)]
 
 
 class ModelSpec:
