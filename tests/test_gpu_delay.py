@@ -273,3 +273,51 @@ def test_plugin_failure_is_loud_and_none_restores_the_config(cuda):
     torch.cuda.synchronize()
     assert not comm.call_record()["delay_active"]  # the config has no delay
     comm.close()
+
+
+def test_back_to_back_calls_on_one_stream_chain_their_network_time(cuda):
+    """An in-order channel starts the next collective when the previous one
+    leaves the wire: a call enqueued behind another on the same stream starts
+    at the previous call's end, not after the kernel-dispatch gap.  The
+    per-call latency stays exactly the model's."""
+    comm = pb.Communicator(delay_config(8, 2, fixed=200.0), 0, 0)
+    x = torch.zeros(1 << 20, device="cuda")
+    for _ in range(6):
+        comm.all_reduce(x, x)
+    torch.cuda.synchronize()
+    last = comm.last_call_id
+    recs = [comm.call_record(i) for i in range(last - 5, last + 1)]
+    for a, b in zip(recs, recs[1:]):
+        assert b["t_start_ns"] == a["t_end_ns"]  # chained: zero gap between calls
+    for r in recs:
+        assert abs((r["t_end_ns"] - r["t_start_ns"]) / 1e3 - 200) <= 2.0
+    # a call issued after an idle stream is not chained
+    torch.cuda._sleep(50_000_000)  # ~25 ms of GPU time on the current stream
+    comm.all_reduce(x, x)
+    torch.cuda.synchronize()
+    r = comm.call_record()
+    assert r["t_start_ns"] - recs[-1]["t_end_ns"] > 1_000_000
+    comm.close()
+
+
+def test_chain_join_continues_compute_from_the_release_end(cuda):
+    """cemuChainJoin: *chain = max(*chain, *release_end) in stream order."""
+    import ctypes as C
+    from paper_2405_02969_b200 import whatif  # noqa: F401  (declares the entry points)
+    from paper_2405_02969_b200._capi import lib
+    comm = pb.Communicator(delay_config(4, 2, fixed=100.0), 0, 0)
+    x = torch.zeros(4096, device="cuda")
+    comm.all_reduce(x, x)
+    end = C.c_void_p()
+    assert lib.cemuCommLastReleaseEnd(comm._h, C.byref(end)) == 0 and end.value
+    s = torch.cuda.current_stream().cuda_stream
+    chain = torch.zeros(1, dtype=torch.int64, device="cuda")
+    assert lib.cemuChainJoin(s, C.c_void_p(chain.data_ptr()), end) == 0
+    torch.cuda.synchronize()
+    assert int(chain.item()) == comm.call_record()["t_end_ns"]  # the later timeline wins
+    chain.fill_(1 << 62)
+    assert lib.cemuChainJoin(s, C.c_void_p(chain.data_ptr()), end) == 0
+    torch.cuda.synchronize()
+    assert int(chain.item()) == 1 << 62
+    assert lib.cemuChainJoin(s, None, end) != 0  # null chain: invalid argument
+    comm.close()
