@@ -245,7 +245,10 @@ struct Call {
   }
   cudaError_t finish(int coll) {
     c->launches += launches;
-    if (!slot) return cudaSuccess;
+    if (!slot) {
+      c->last_slot = nullptr;  // nothing to chain to / join with
+      return cudaSuccess;
+    }
     const auto& m = c->meta[i];
     DelayLaunch d;
     d.model = c->delay;
