@@ -365,6 +365,7 @@ def whatif_block(device, with_reference):
         res = sweep(model, [0, 500, 1000, 2000, 4000, 6000, 8000, 10000], world, bb, device, extra, iters,
                     reference_fn=ref_fn)
         out[name] = {k: (round(v, 6) if isinstance(v, float) else v) for k, v in res.items() if k != "points"}
+        out[name]["model"] = os.path.relpath(model, ROOT) if os.path.isabs(model) else model
         out[name]["points"] = [[p["inject_us"], round(p["mean_us"], 1), round(p["ideal_us"], 1),
                                 round(100 * p["rel_err"], 4)] +
                                ([round(p["reference_mean_us"], 1), round(100 * p["reference_rel_err"], 2)]
