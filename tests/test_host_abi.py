@@ -67,6 +67,17 @@ def test_version_and_errors():
     assert _capi.lib.cemuGetErrorString(5) == b"invalid usage"
 
 
+def test_chain_entry_points_reject_null_arguments_without_a_device():
+    import ctypes as C
+    from paper_2405_02969_b200 import whatif  # noqa: F401  (declares the argtypes)
+    lib = _capi.lib
+    x = C.c_int64(0)
+    assert lib.cemuChainJoin(None, None, C.byref(x)) == 4   # null chain
+    assert lib.cemuChainJoin(None, C.byref(x), None) == 4   # null release end
+    out = C.c_void_p(1)
+    assert lib.cemuCommLastReleaseEnd(None, C.byref(out)) == 4  # null communicator
+
+
 # ---- job config (config.cpp) ------------------------------------------------
 def test_shipped_configs_render_and_digest_like_reference():
     for name, c in golden("configs.json")["shipped"].items():
