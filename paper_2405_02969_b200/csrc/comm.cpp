@@ -270,6 +270,7 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
     const char* fe = std::getenv("CEMU_FUSED");
     c->fused = !preinit && c->k <= static_cast<uint32_t>(kMaxReal) && !(fe && std::string(fe) == "0");
     if (const char* t = std::getenv("CEMU_FUSED_TIMEOUT_S")) c->fused_timeout_ns = std::atoll(t) * 1'000'000'000LL;
+    if (const char* ce = std::getenv("CEMU_CE")) c->ce = std::string(ce) == "0" ? 0 : std::string(ce) == "1" ? 1 : 2;
     if (c->fused) {
       CUDA_OK(cudaMalloc(&c->sig, 4096));
       CUDA_OK(cudaMemset(c->sig, 0, 4096));
@@ -308,6 +309,100 @@ FusedArgs fused_allreduce_args(const cemuComm* c, int dt, uint64_t count, uint64
   a.keys = c->d_virt_keys;
   a.nkeys = static_cast<uint32_t>(c->virt.size());
   return a;
+}
+
+// Copy-engine allreduce at k = 2 (probe: profiles/
+// ce_pipeline_probe.cu): start barrier; per chunk of this GPU's slice the
+// copy engine pulls the peer's chunk into staging, the fused kernel in
+// fold-only mode adds local + staged (ascending real rank, as the fused
+// path) and the emulated ranks into the local recv, and the copy engine
+// pushes the result into the peer's recv; done barrier after the pushes.
+// Bit-identical to the fused kernel (same fold code).  Chosen only where it
+// measured faster: two real GPUs, >= 512 MiB, no ragged tail, <= 16
+// emulated ranks (CEMU_CE=1 forces it, CEMU_CE=0 disables it).
+constexpr uint64_t kCeMinBytes = 512ull << 20;
+
+// Chunk of the slice: at most CEMU_CE_CHUNK_MIB (default 256; measured
+// 1 GiB k = 2: 256 MiB chunks 1.452 ms, 128 MiB 1.517, one chunk 1.764) and
+// at least two chunks, so the pull, the fold and the push overlap.
+uint64_t ce_chunk_vecs(uint64_t slice_vecs) {
+  static const uint64_t cap = [] {
+    const char* e = std::getenv("CEMU_CE_CHUNK_MIB");
+    return (e ? std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) : uint64_t{256}) << 20;
+  }() / 16;
+  const uint64_t n = std::max<uint64_t>(2, (slice_vecs + cap - 1) / cap);
+  return (slice_vecs + n - 1) / n;
+}
+
+// Auto mode also needs a cheap synthesis: the pipeline serialises the
+// first pull and the last push around the folds, which only pays while the
+// NVLink legs dominate (measured 1 GiB k = 2: 14 emulated ranks fp32 1.55 vs
+// 1.64 ms fused, bf16 1.11 vs 1.26; 126 emulated ranks bf16 3.19 vs 2.45).
+constexpr size_t kCeMaxAutoPeers = 16;
+
+bool ce_allreduce_fits(const cemuComm* c, const FusedArgs& a, uint64_t bytes) {
+  if (!c->ce || c->k != 2 || bytes < kCeMinBytes || a.ntail != 0) return false;
+  if (c->ce == 2 && c->virt.size() > kCeMaxAutoPeers) return false;
+  const uint64_t sv = a.v_end - a.v_begin;
+  return (sv + ce_chunk_vecs(sv) - 1) / ce_chunk_vecs(sv) <= 64;  // the event pool
+}
+
+cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, cudaStream_t s, Call* call) {
+  auto& p = c->cep;
+  const uint64_t slice = (a.v_end - a.v_begin) * 16;
+  if (!p.pull) CUDA_OK(cudaStreamCreateWithFlags(&p.pull, cudaStreamNonBlocking));
+  if (!p.push) CUDA_OK(cudaStreamCreateWithFlags(&p.push, cudaStreamNonBlocking));
+  for (cudaEvent_t& ev : p.ev) {
+    if (!ev) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  if (p.stage_bytes < slice) {
+    CUDA_OK(cudaDeviceSynchronize());  // the old staging may still be in use
+    cudaFree(p.stage);
+    p.stage = nullptr;
+    p.stage_bytes = 0;
+    CUDA_OK(cudaMalloc(&p.stage, slice));
+    p.stage_bytes = slice;
+  }
+  const int peer = 1 - a.me;
+  const uint4* peer_send = a.src[peer];
+  uint4* peer_recv = a.dst[peer];
+  uint4* my_recv = a.dst[a.me];
+  a.stamp = call->take_stamp();
+  CUDA_OK(launch_peer_barrier(a, 0, s, &call->launches));
+  cudaEvent_t started = p.ev[0], pushed = p.ev[1];
+  CUDA_OK(cudaEventRecord(started, s));
+  CUDA_OK(cudaStreamWaitEvent(p.pull, started, 0));
+  CUDA_OK(cudaStreamWaitEvent(p.push, started, 0));
+  // the staging, indexed like the buffers: element vector v at stage[v - v_begin]
+  const auto stage_at = reinterpret_cast<uintptr_t>(p.stage) - a.v_begin * 16;
+  FusedArgs f = a;
+  f.barriers = 0;
+  f.stamp = nullptr;
+  f.ndst = 1;
+  f.dst[0] = my_recv;
+  f.src[peer] = reinterpret_cast<const uint4*>(stage_at);
+  const uint64_t cvec = ce_chunk_vecs(a.v_end - a.v_begin);
+  int ci = 0;
+  for (uint64_t v0 = a.v_begin; v0 < a.v_end; v0 += cvec, ++ci) {
+    const uint64_t v1 = std::min(a.v_end, v0 + cvec);
+    const size_t n = (v1 - v0) * 16;
+    cudaEvent_t pulled = p.ev[2 + 2 * ci], folded = p.ev[3 + 2 * ci];
+    CUDA_OK(cudaMemcpyAsync(reinterpret_cast<void*>(stage_at + v0 * 16), peer_send + v0, n,
+                            cudaMemcpyDeviceToDevice, p.pull));
+    CUDA_OK(cudaEventRecord(pulled, p.pull));
+    CUDA_OK(cudaStreamWaitEvent(s, pulled, 0));
+    f.v_begin = v0;
+    f.v_end = v1;
+    CUDA_OK(launch_fused_allreduce(dt, f, s, &call->launches));
+    CUDA_OK(cudaEventRecord(folded, s));
+    CUDA_OK(cudaStreamWaitEvent(p.push, folded, 0));
+    CUDA_OK(cudaMemcpyAsync(peer_recv + v0, my_recv + v0, n, cudaMemcpyDeviceToDevice, p.push));
+  }
+  CUDA_OK(cudaEventRecord(pushed, p.push));
+  CUDA_OK(cudaStreamWaitEvent(s, pushed, 0));
+  CUDA_OK(launch_peer_barrier(a, 1, s, &call->launches));
+  CUDA_OK(call->finish(kAllReduce));
+  return cemuSuccess;
 }
 
 cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, cemuComm* c,
@@ -358,6 +453,14 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
       dp[g] = rr->peer[g] + roff;
     }
     FusedArgs a = fused_allreduce_args(c, dt, count, 0, sp, dp);
+    if ((soff | roff) % 16 == 0 && ce_allreduce_fits(c, a, count * es)) {
+      ph.push_back([=]() mutable -> cemuResult_t {
+        set_barrier(c, a);
+        a.sig = op_sig(kAllReduce, dt, count);
+        return ce_allreduce(c, dt, a, s, call.get());
+      });
+      return cemuSuccess;
+    }
     if ((soff | roff) % 16 == 0) ph.push_back([=]() mutable -> cemuResult_t {
       set_barrier(c, a);
       a.sig = op_sig(kAllReduce, dt, count);

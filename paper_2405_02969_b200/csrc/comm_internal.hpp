@@ -149,6 +149,16 @@ struct cemuComm {
   std::unique_ptr<WireSession> wire;
   void* wire_buf = nullptr;  // device staging of one received DATA payload
   size_t wire_buf_bytes = 0;
+  // copy-engine allreduce (k = 2, large symmetric buffers):
+  // the NVLink legs ride the copy engines, the fold + synthesis the SMs
+  int ce = 2;  // CEMU_CE: 0 off, 1 forced, 2 (default) auto -- see ce_allreduce_fits
+  struct CePipe {
+    static constexpr int kEvents = 2 * 64 + 2;
+    cudaStream_t pull = nullptr, push = nullptr;
+    cudaEvent_t ev[kEvents] = {};
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
+  } cep;
 
   // Releases every resource held, in dependency order; also runs when
   // initialisation fails half way (init_comm owns the comm in a unique_ptr).
@@ -178,6 +188,16 @@ struct cemuComm {
     for (uint32_t g = 0; g < k && g < static_cast<uint32_t>(kMaxReal); ++g) {
       if (g != li && peer_sig[g]) cudaIpcCloseMemHandle(peer_sig[g]);
     }
+    for (cudaStream_t st : {cep.pull, cep.push}) {
+      if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+      }
+    }
+    for (cudaEvent_t ev : cep.ev) {
+      if (ev) cudaEventDestroy(ev);
+    }
+    cudaFree(cep.stage);
     cudaFree(sig);
     cudaFree(scratch);
     cudaFree(wire_buf);

@@ -709,12 +709,12 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
   const uint64_t epoch = *a.epoch + 1;
   if (a.stamp && blockIdx.x == 0 && threadIdx.x == 0) *a.stamp = t0;
   // start barrier: announce, then wait for every peer's announcement
-  if (blockIdx.x == 0 && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
+  if (a.barriers && blockIdx.x == 0 && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
     st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(epoch, a.sig));
   }
   if (threadIdx.x == 0) abort_s = 0;
   load_keys(skeys, a.keys, a.nkeys, key_shift(kMode));
-  if (threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
+  if (a.barriers && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
     const int w = wait_flag(a.flags + threadIdx.x, epoch, a.sig, true, t0, a.timeout_ns);
     if (w) {
       atomicExch(a.error, static_cast<uint32_t>(w));
@@ -766,6 +766,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
     fused_tail_elem<DT>(a, threadIdx.x, skeys + key_shift(kMode));
   }
 
+  if (!a.barriers) return;
   // done barrier: the last CTA on this GPU publishes and waits
   __threadfence_system();
   __syncthreads();
@@ -784,6 +785,31 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
       }
       *a.epoch = epoch;
     }
+  }
+}
+
+// The fused kernel's barriers alone (one warp): phase 0 = start (peers'
+// send buffers complete, recv buffers free), phase 1 = done (every peer's
+// copies into my recv have completed -- each peer launches this after its
+// copy-engine pushes, in stream order -- then the epoch advances).
+__global__ void peer_barrier_kernel(const __grid_constant__ FusedArgs a, int phase) {
+  const uint64_t epoch = *a.epoch + 1;
+  const int64_t t0 = globaltimer_ns();
+  const int g = static_cast<int>(threadIdx.x);
+  const bool peer = g < a.k && g != a.me;
+  if (phase == 0) {
+    if (a.stamp && g == 0) *a.stamp = t0;
+    if (peer) st_release_sys(a.peer_flags[g] + a.me, flag_word(epoch, a.sig));
+    if (peer) {
+      const int w = wait_flag(a.flags + g, epoch, a.sig, true, t0, a.timeout_ns);
+      if (w) atomicExch(a.error, static_cast<uint32_t>(w));
+    }
+  } else {
+    __threadfence_system();
+    if (peer) st_release_sys(a.peer_flags[g] + 8 + a.me, flag_word(epoch, 0));
+    if (peer && wait_flag(a.flags + 8 + g, epoch, 0, false, t0, a.timeout_ns)) atomicExch(a.error, 2u);
+    __syncwarp();
+    if (g == 0) *a.epoch = epoch;
   }
 }
 
@@ -1433,6 +1459,13 @@ cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t s
     case cemuUint32: return fused_kind<kI32, cemuUint32>(a, s);
     default: --*launches; return cudaErrorNotSupported;
   }
+}
+
+cudaError_t launch_peer_barrier(const FusedArgs& a, int phase, cudaStream_t s, int* launches) {
+  if (a.k < 2 || a.k > 32) return cudaErrorInvalidValue;
+  ++*launches;
+  peer_barrier_kernel<<<1, 32, 0, s>>>(a, phase);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fused_allgather(int dtype, const FusedGatherArgs& a, cudaStream_t s, int* launches) {

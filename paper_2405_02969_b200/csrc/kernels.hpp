@@ -87,9 +87,16 @@ struct FusedArgs {
   uint32_t sig = 0;                 // op signature (coll, dtype, count): must agree across ranks
   int64_t* stamp = nullptr;
   int64_t timeout_ns = 0;
+  // 0: fold only -- no start / done barrier, epoch untouched (one chunk of
+  // the copy-engine pipeline, whose barriers are launch_peer_barrier's)
+  int barriers = 1;
 };
 // Returns cudaErrorNotSupported for datatypes without a vector path.
 cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t stream, int* launches);
+// The fused kernel's start (phase 0: announce + wait, stamps a.stamp) or
+// done (phase 1: announce + wait, then the epoch advances) barrier alone, as
+// a one-warp kernel: brackets a copy-engine allreduce.
+cudaError_t launch_peer_barrier(const FusedArgs& a, int phase, cudaStream_t stream, int* launches);
 
 // One-kernel multi-GPU allgather: push the own block to every real GPU over
 // NVLink while the same launch synthesises the emulated blocks locally.

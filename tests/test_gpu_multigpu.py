@@ -42,6 +42,28 @@ def test_multi_gpu_collectives_match_oracle(kmax):
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
+def test_copy_engine_allreduce_equals_the_fused_kernel():
+    """Two real GPUs, >= 512 MiB: the copy-engine pipeline (default there)
+    is bit-identical to the fused kernel (CEMU_CE=0) -- itself pinned to the
+    oracle by mgpu_worker.py -- on arbitrary fp32 / bf16 / int32, out of
+    place and in place (tests/ce_check.py)."""
+    import json
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ce_check.py")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()), worker],
+                       capture_output=True, text=True, timeout=420)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 2
+    for res in lines:
+        for case in res["cases"]:
+            assert case["equal"] and case["equal_in_place"], case
+            assert case["ce_launches"] > case["fused_launches"] == 1  # the pipeline really ran
+            assert case["errors"] == [None, None], case
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
 def test_single_process_init_all(tmp_path):
     """ncclCommInitAll shape: one process drives every GPU (grouped calls)."""
     import numpy as np
