@@ -78,6 +78,21 @@ def test_chain_entry_points_reject_null_arguments_without_a_device():
     assert lib.cemuCommLastReleaseEnd(None, C.byref(out)) == 4  # null communicator
 
 
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="needs a host without a GPU")
+def test_no_cpu_fallback_without_a_device():
+    # the product path has no CPU route: a communicator cannot come up
+    # without a CUDA device, through the Python mirror or the C-ABI
+    import ctypes as C
+    from gpu_util import config
+    from paper_2405_02969_b200 import comm
+    with pytest.raises(_capi.CemuError, match="cudaSetDevice"):
+        comm.Communicator(config(8), 0, device=0)
+    h = C.c_void_p()
+    uid = comm.UniqueId()
+    assert _capi.lib.cemuCommInitRankConfig(C.byref(h), config(8).encode(), uid, 0, 0) != 0
+    assert h.value is None
+
+
 # ---- job config (config.cpp) ------------------------------------------------
 def test_shipped_configs_render_and_digest_like_reference():
     for name, c in golden("configs.json")["shipped"].items():
