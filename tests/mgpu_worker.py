@@ -36,6 +36,18 @@ def main():
     os._exit(0)
 
 
+CANARY = 0xA5
+
+
+def check_guards(base, off, count, what):
+    """Every byte of `base` outside elements [off, off + count) still holds the canary."""
+    torch.cuda.synchronize()
+    es = base.element_size()
+    raw = base.view(torch.uint8).cpu()
+    bad = int((raw[:off * es] != CANARY).sum()) + int((raw[(off + count) * es:] != CANARY).sum())
+    assert bad == 0, f"{what}: {bad} guard bytes overwritten"
+
+
 def run():
     os.environ["CEMU_HOST_CHUNK_MIB"] = "1"  # host-buffer pipeline: many chunks per call
     local = int(os.environ["LOCAL_RANK"])
@@ -147,8 +159,15 @@ def run():
                     sends.append(v)
                 off = int(g.integers(0, 64)) * 16 // torch.empty(0, dtype=TORCH[dt]).element_size()
                 trace(f"fused real={real} dt={dt} count={count}")
-                x = comm.alloc(count + off, TORCH[dt])[off:]
-                y = comm.alloc(count + off, TORCH[dt])[off:]
+                # guard band of canary bytes after each buffer (and the
+                # offset's bytes before it): the fused kernel's peer pushes
+                # must land inside every GPU's [off, off + count)
+                guard = 4096 // torch.empty(0, dtype=TORCH[dt]).element_size()
+                xb = comm.alloc(count + off + guard, TORCH[dt])
+                yb = comm.alloc(count + off + guard, TORCH[dt])
+                for b in (xb, yb):
+                    b.view(torch.uint8).fill_(CANARY)
+                x, y = xb[off:off + count], yb[off:off + count]
                 x.copy_(sends[local].cuda())
                 torch.cuda.synchronize()
                 before = comm.kernel_launches
@@ -159,11 +178,15 @@ def run():
                 assert comm.async_error() is None
                 want = P.allreduce(dt, P.PAYLOAD_HASH, W, real, me, 1, [to_np(s) for s in sends], count)
                 assert_bit_equal(to_np(y), want, f"fused allreduce real={real} dt={dt} n={count}")
+                assert_bit_equal(to_np(x), to_np(sends[local]), f"fused input modified real={real} dt={dt}")
+                check_guards(xb, off, count, f"fused send real={real} dt={dt} n={count}")
+                check_guards(yb, off, count, f"fused recv real={real} dt={dt} n={count}")
                 comm.all_reduce(x, x)  # in place
                 torch.cuda.synchronize()
                 assert_bit_equal(to_np(x), want, f"fused in-place real={real} dt={dt} n={count}")
-                comm.free(x._base if x._base is not None else x)
-                comm.free(y._base if y._base is not None else y)
+                check_guards(xb, off, count, f"fused in-place real={real} dt={dt} n={count}")
+                comm.free(xb)
+                comm.free(yb)
                 # fused reduce-scatter (symmetric send) and allgather (symmetric recv)
                 rc = max(count // 3, 8) // 8 * 8  # 16-byte chunks: the fused path (checked below)
                 full = [torch.cat([v] * -(-rc * W // count))[: rc * W] for v in sends]
