@@ -104,3 +104,37 @@ def test_collectives_stay_inside_their_buffers(cuda, W, dt):
             assert_bit_equal(to_np(o.t), want, "broadcast " + what)
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("dt", [7, 9, 2])
+def test_host_buffer_calls_stay_inside_their_buffers(cuda, dt, monkeypatch):
+    """cemuAllReduceHost / cemuAllGatherHost: the chunked D2H copies land only
+    inside the pinned output span (1 MiB chunks, so many chunks per call)."""
+    monkeypatch.setenv("CEMU_HOST_CHUNK_MIB", "1")
+    W = 8
+    comm = pb.Communicator(config(W, (0,), "hash", 5), 0, 0)
+    t = TORCH[dt]
+    es = torch.empty(0, dtype=t).element_size()
+    try:
+        for count in (5, (3 << 20) // es + 7):
+            h = host_input(dt, count, seed=count + dt)
+            want = P.allreduce(dt, P.PAYLOAD_HASH, W, [0], 0, 5, [to_np(h)], count)
+            raw = torch.full((2 * GUARD + count * es + es,), CANARY, dtype=torch.uint8).pin_memory()
+            lo = GUARD + es  # element-aligned, not 16-byte aligned
+            out = raw[lo:lo + count * es].view(t)
+            src = h.pin_memory()
+            comm.all_reduce_host(src, out)
+            torch.cuda.synchronize()
+            assert_bit_equal(to_np(out), want, f"host allreduce dt={dt} n={count}")
+            assert_bit_equal(to_np(src), to_np(h), f"host allreduce input modified dt={dt} n={count}")
+            assert int((raw[:lo] != CANARY).sum()) == 0 and int((raw[lo + count * es:] != CANARY).sum()) == 0
+            blk = min(count, 1 << 16)
+            want = P.allgather(dt, P.PAYLOAD_HASH, W, [0], 0, 5, [to_np(h[:blk])], blk)
+            raw = torch.full((2 * GUARD + W * blk * es,), CANARY, dtype=torch.uint8).pin_memory()
+            out = raw[GUARD:GUARD + W * blk * es].view(t)
+            comm.all_gather_host(h[:blk].contiguous().pin_memory(), out)
+            torch.cuda.synchronize()
+            assert_bit_equal(to_np(out), want, f"host allgather dt={dt} blk={blk}")
+            assert int((raw[:GUARD] != CANARY).sum()) == 0 and int((raw[GUARD + W * blk * es:] != CANARY).sum()) == 0
+    finally:
+        comm.close()
