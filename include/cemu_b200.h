@@ -157,6 +157,19 @@ cemuResult_t cemuCommDetachEmulator(cemuComm_t comm);
  * reduce-scatter + synthesis + NCCL allgather.  One real GPU: plain memory. */
 cemuResult_t cemuMemAlloc(cemuComm_t comm, size_t bytes, void** ptr);
 cemuResult_t cemuMemFree(cemuComm_t comm, void* ptr);
+/* Caller memory as a symmetric range: replaces ncclCommRegister /
+ * ncclCommDeregister (nccl.h 2.27.3:243-248) and ncclCommWindowRegister /
+ * ncclCommWindowDeregister (nccl.h:251-256).  Collective over the job's real
+ * ranks on this box: each rank exports the cudaMalloc allocation holding
+ * [buff, buff + size) through CUDA IPC and maps every peer's, so
+ * collectives whose buffers lie in registered ranges (at the same offsets
+ * on every real rank) take the fused NVLink kernels, as with cemuMemAlloc.
+ * The caller keeps ownership; deregister before freeing.  Memory that
+ * cannot be exported (e.g. cuMem VMM allocations) fails on every rank with
+ * cemuInvalidUsage.  One real GPU: bookkeeping only.  A null buffer or zero
+ * size registers nothing (*handle = NULL). */
+cemuResult_t cemuCommRegister(cemuComm_t comm, void* buff, size_t size, void** handle);
+cemuResult_t cemuCommDeregister(cemuComm_t comm, void* handle);
 /* Errors raised inside the fused kernel (a peer that never arrived at a
  * barrier within CEMU_FUSED_TIMEOUT_S); synchronous read. */
 cemuResult_t cemuCommGetAsyncError(cemuComm_t comm, cemuResult_t* asyncError);

@@ -107,49 +107,181 @@ cudaError_t exchange_records(cemuComm* c, const void* rec, size_t bytes, std::ve
   return e;
 }
 
+// What each real rank publishes for one symmetric range: the IPC handle of
+// the allocation holding it, where the range starts inside that allocation
+// and how long it is.  `ok` = 0 when this rank could not export its range:
+// every rank still takes part in the exchange, so all of them fail together
+// instead of one hanging in it.
 struct IpcRecord {
   cudaIpcMemHandle_t handle;
+  uint64_t offset;
   uint64_t bytes;
+  int32_t ok;
+  int32_t pad;
 };
 
-// Maps every real GPU's allocation `local` (collectively) into this process.
-cemuResult_t map_peers(cemuComm* c, void* local, size_t bytes, uint8_t** peers) {
+void* open_peer(cemuComm* c, uint32_t g, const cudaIpcMemHandle_t& h, cudaError_t* err) {
+  std::string key(reinterpret_cast<const char*>(&h), sizeof h);
+  key.push_back(static_cast<char>(g));
+  auto& m = c->ipc_maps[key];
+  if (!m.ptr) {
+    *err = cudaIpcOpenMemHandle(&m.ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (*err != cudaSuccess) {
+      c->ipc_maps.erase(key);
+      return nullptr;
+    }
+  }
+  ++m.refs;
+  return m.ptr;
+}
+
+void close_peer(cemuComm* c, void* ptr) {
+  for (auto it = c->ipc_maps.begin(); it != c->ipc_maps.end(); ++it) {
+    if (it->second.ptr != ptr) continue;
+    if (--it->second.refs == 0) {
+      cudaIpcCloseMemHandle(ptr);
+      c->ipc_maps.erase(it);
+    }
+    return;
+  }
+}
+
+// Collective: every real rank publishes (handle, offset, bytes) of its
+// range [alloc_base + offset, + bytes) and maps every peer's.
+cemuResult_t map_range(cemuComm* c, void* alloc_base, uint64_t offset, size_t bytes, bool exportable,
+                       const std::string& why, uint8_t** peers, uint8_t** peer_maps) {
   IpcRecord mine{};
-  cudaError_t e = cudaIpcGetMemHandle(&mine.handle, local);
-  if (e != cudaSuccess) return fail(cemuUnhandledCudaError, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  mine.offset = offset;
   mine.bytes = bytes;
+  mine.ok = exportable ? 1 : 0;
+  std::string local_err = why;
+  if (exportable) {
+    const cudaError_t e = cudaIpcGetMemHandle(&mine.handle, alloc_base);
+    if (e != cudaSuccess) {
+      mine.ok = 0;
+      local_err = std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e);
+      cudaGetLastError();
+    }
+  }
   std::vector<uint8_t> all;
   ncclResult_t nr = ncclSuccess;
-  e = exchange_records(c, &mine, sizeof mine, &all, &nr);
+  const cudaError_t e = exchange_records(c, &mine, sizeof mine, &all, &nr);
   if (nr != ncclSuccess) return fail(static_cast<cemuResult_t>(nr), "ipc handle exchange: nccl error");
   if (e != cudaSuccess) return fail(cemuUnhandledCudaError, std::string("ipc handle exchange: ") + cudaGetErrorString(e));
+  std::vector<IpcRecord> rec(c->k);
+  for (uint32_t g = 0; g < c->k; ++g) std::memcpy(&rec[g], all.data() + g * sizeof(IpcRecord), sizeof(IpcRecord));
   for (uint32_t g = 0; g < c->k; ++g) {
-    IpcRecord r;
-    std::memcpy(&r, all.data() + g * sizeof r, sizeof r);
-    if (r.bytes != bytes) {
-      return fail(cemuInvalidUsage, "cemuMemAlloc: real ranks asked for different sizes (" + std::to_string(bytes) +
-                                        " vs " + std::to_string(r.bytes) + ")");
+    if (!rec[g].ok) {
+      return fail(cemuInvalidUsage, g == c->li ? "symmetric range: " + local_err
+                                                : "symmetric range: real rank index " + std::to_string(g) +
+                                                      " could not export its buffer");
     }
+    if (rec[g].bytes != bytes) {
+      return fail(cemuInvalidUsage, "symmetric range: real ranks asked for different sizes (" + std::to_string(bytes) +
+                                        " vs " + std::to_string(rec[g].bytes) + ")");
+    }
+  }
+  uint8_t* maps[kMaxReal] = {};
+  for (uint32_t g = 0; g < c->k; ++g) {
     if (g == c->li) {
-      peers[g] = static_cast<uint8_t*>(local);
+      peers[g] = static_cast<uint8_t*>(alloc_base) + offset;
       continue;
     }
-    void* p = nullptr;
-    e = cudaIpcOpenMemHandle(&p, r.handle, cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess) return fail(cemuUnhandledCudaError, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
-    peers[g] = static_cast<uint8_t*>(p);
+    cudaError_t oe = cudaSuccess;
+    void* p = open_peer(c, g, rec[g].handle, &oe);
+    if (!p) {
+      for (uint32_t h = 0; h < g; ++h) {
+        if (maps[h]) close_peer(c, maps[h]);
+      }
+      return fail(cemuUnhandledCudaError, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(oe));
+    }
+    maps[g] = static_cast<uint8_t*>(p);
+    peers[g] = maps[g] + rec[g].offset;
+  }
+  if (peer_maps) {
+    for (uint32_t g = 0; g < c->k; ++g) peer_maps[g] = maps[g];
   }
   return cemuSuccess;
 }
 
+// Maps every real GPU's allocation `local` (collectively) into this process.
+cemuResult_t map_peers(cemuComm* c, void* local, size_t bytes, uint8_t** peers, uint8_t** peer_maps) {
+  return map_range(c, local, 0, bytes, true, "", peers, peer_maps);
+}
+
+void unmap_region(cemuComm* c, cemuComm::Region& r) {
+  for (uint32_t g = 0; g < c->k; ++g) {
+    if (g != c->li && r.peer_map[g]) close_peer(c, r.peer_map[g]);
+    r.peer_map[g] = nullptr;
+  }
+  if (c->k > 1 && c->fused) {  // every peer unmapped before anyone frees
+    std::vector<uint8_t> all;
+    ncclResult_t nr = ncclSuccess;
+    const uint8_t one = 1;
+    exchange_records(c, &one, 1, &all, &nr);
+  }
+}
+
+cemuResult_t grow_buffer(cemuComm* c, void** buf, size_t* have, size_t bytes, const char* what) {
+  if (*have >= bytes) return cemuSuccess;
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) return fail(cemuUnhandledCudaError, std::string(what) + ": " + cudaGetErrorString(e));
+  if (*buf) c->retired.push_back(*buf);  // an enqueued or captured call may still use it
+  *buf = p;
+  *have = bytes;
+  return cemuSuccess;
+}
+
 cemuResult_t ensure_scratch(cemuComm* c, size_t bytes) {
-  if (c->scratch_bytes >= bytes) return cemuSuccess;
-  if (c->scratch) cudaFree(c->scratch);
-  c->scratch = nullptr;
-  c->scratch_bytes = 0;
-  const cudaError_t e = cudaMalloc(&c->scratch, bytes);
-  if (e != cudaSuccess) return fail(cemuUnhandledCudaError, std::string("staging buffer: ") + cudaGetErrorString(e));
-  c->scratch_bytes = bytes;
+  return grow_buffer(c, &c->scratch, &c->scratch_bytes, bytes, "staging buffer");
+}
+
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
+}
+
+// CEMU_ORDER=0 removes the ordering (diagnostic: tests/interleave_worker.py
+// shows what goes wrong without it)
+bool ordering_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("CEMU_ORDER");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
+cemuResult_t order_begin(cemuComm* c, cudaStream_t s) {
+  if (!ordering_on() || !c->order_recorded || c->order_stream == s) return cemuSuccess;  // stream order suffices
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  CUDA_OK(cudaStreamGetCaptureInfo(s, &st, &id));
+  if (st == cudaStreamCaptureStatusActive) {
+    if (c->order_capture == id) {
+      CUDA_OK(cudaStreamWaitEvent(s, c->order_ev, 0));  // recorded earlier in this capture
+    } else if (c->order_capture == 0) {
+      // recorded eagerly: the graph waits, at each launch, for the event's
+      // latest record (an external event node)
+      CUDA_OK(cudaStreamWaitEvent(s, c->order_ev, cudaEventWaitExternal));
+    }
+    // recorded inside another capture: that graph's launch orders it
+  } else if (c->order_capture == 0) {
+    CUDA_OK(cudaStreamWaitEvent(s, c->order_ev, 0));
+  }
+  return cemuSuccess;
+}
+
+cemuResult_t order_end(cemuComm* c, cudaStream_t s) {
+  if (!ordering_on()) return cemuSuccess;
+  if (!c->order_ev) CUDA_OK(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  CUDA_OK(cudaStreamGetCaptureInfo(s, &st, &id));
+  CUDA_OK(cudaEventRecord(c->order_ev, s));
+  c->order_stream = s;
+  c->order_recorded = true;
+  c->order_capture = st == cudaStreamCaptureStatusActive ? id : 0;
   return cemuSuccess;
 }
 
@@ -311,6 +443,20 @@ FusedArgs fused_allreduce_args(const cemuComm* c, int dt, uint64_t count, uint64
   return a;
 }
 
+// CEMU_DEBUG=INFO: one stderr line per call naming the path it took (the
+// NCCL_DEBUG analogue), so a job can see whether its buffers reach the
+// fused kernels.
+void log_path(const cemuComm* c, const char* coll, uint64_t bytes, const char* path) {
+  static const bool on = [] {
+    const char* e = std::getenv("CEMU_DEBUG");
+    return e && (std::string(e) == "INFO" || std::string(e) == "TRACE");
+  }();
+  if (on) {
+    std::fprintf(stderr, "cemu: rank %u %s %llu B -> %s\n", c->rank, coll, static_cast<unsigned long long>(bytes),
+                 path);
+  }
+}
+
 // Copy-engine allreduce at k = 2 (probe: profiles/
 // ce_pipeline_probe.cu): start barrier; per chunk of this GPU's slice the
 // copy engine pulls the peer's chunk into staging, the fused kernel in
@@ -340,29 +486,33 @@ uint64_t ce_chunk_vecs(uint64_t slice_vecs) {
 // 1.64 ms fused, bf16 1.11 vs 1.26; 126 emulated ranks bf16 3.19 vs 2.45).
 constexpr size_t kCeMaxAutoPeers = 16;
 
-bool ce_allreduce_fits(const cemuComm* c, const FusedArgs& a, uint64_t bytes) {
-  if (!c->ce || c->k != 2 || bytes < kCeMinBytes || a.ntail != 0) return false;
+// The larger of the two slices: every rank sizes its staging alike, so the
+// capture-time check below agrees across ranks.
+uint64_t ce_stage_vecs(uint64_t count, size_t es) { return (count / (16 / es) + 1) / 2; }
+
+// Every real rank must take the same decision (they meet in the barriers),
+// so it only looks at symmetric quantities: the count's ragged tail, not
+// this rank's share of it.  Inside a stream capture the staging cannot
+// grow (no allocation there), so such a call stays on the fused kernel.
+bool ce_allreduce_fits(const cemuComm* c, const FusedArgs& a, uint64_t count, size_t es, cudaStream_t s) {
+  const uint64_t bytes = count * es;
+  if (!c->ce || c->k != 2 || bytes < kCeMinBytes || count % (16 / es) != 0) return false;
   if (c->ce == 2 && c->virt.size() > kCeMaxAutoPeers) return false;
-  const uint64_t sv = a.v_end - a.v_begin;
+  const uint64_t sv = ce_stage_vecs(count, es);
+  if (c->cep.stage_bytes < sv * 16 && capturing(s)) return false;
+  (void)a;
   return (sv + ce_chunk_vecs(sv) - 1) / ce_chunk_vecs(sv) <= 64;  // the event pool
 }
 
-cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, cudaStream_t s, Call* call) {
+cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs, cudaStream_t s, Call* call) {
   auto& p = c->cep;
-  const uint64_t slice = (a.v_end - a.v_begin) * 16;
+  const uint64_t slice = stage_vecs * 16;
   if (!p.pull) CUDA_OK(cudaStreamCreateWithFlags(&p.pull, cudaStreamNonBlocking));
   if (!p.push) CUDA_OK(cudaStreamCreateWithFlags(&p.push, cudaStreamNonBlocking));
   for (cudaEvent_t& ev : p.ev) {
     if (!ev) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
-  if (p.stage_bytes < slice) {
-    CUDA_OK(cudaDeviceSynchronize());  // the old staging may still be in use
-    cudaFree(p.stage);
-    p.stage = nullptr;
-    p.stage_bytes = 0;
-    CUDA_OK(cudaMalloc(&p.stage, slice));
-    p.stage_bytes = slice;
-  }
+  if (auto r = grow_buffer(c, &p.stage, &p.stage_bytes, slice, "copy-engine staging")) return r;
   const int peer = 1 - a.me;
   const uint4* peer_send = a.src[peer];
   uint4* peer_recv = a.dst[peer];
@@ -431,8 +581,9 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
     CUDA_OK(call->finish(kAllReduce));
     return cemuSuccess;
   });
-  if (c->mode == PayloadMode::kZero) return cemuSuccess;
+  if (c->mode == PayloadMode::kZero) return log_path(c, "allreduce", count * es, "zero payload"), cemuSuccess;
   if (c->k == 1) {
+    log_path(c, "allreduce", count * es, "synthesis");
     ph.push_back([=]() -> cemuResult_t {
       CUDA_OK(launch_synth_reduce(dt, send, recv, count, 0, nv, nk, call->take_stamp(), s, &call->launches));
       CUDA_OK(call->finish(kAllReduce));
@@ -453,14 +604,16 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
       dp[g] = rr->peer[g] + roff;
     }
     FusedArgs a = fused_allreduce_args(c, dt, count, 0, sp, dp);
-    if ((soff | roff) % 16 == 0 && ce_allreduce_fits(c, a, count * es)) {
+    if ((soff | roff) % 16 == 0 && ce_allreduce_fits(c, a, count, es, s)) {
+      log_path(c, "allreduce", count * es, "copy-engine pipeline");
       ph.push_back([=]() mutable -> cemuResult_t {
         set_barrier(c, a);
         a.sig = op_sig(kAllReduce, dt, count);
-        return ce_allreduce(c, dt, a, s, call.get());
+        return ce_allreduce(c, dt, a, ce_stage_vecs(count, es), s, call.get());
       });
       return cemuSuccess;
     }
+    if ((soff | roff) % 16 == 0) log_path(c, "allreduce", count * es, "fused");
     if ((soff | roff) % 16 == 0) ph.push_back([=]() mutable -> cemuResult_t {
       set_barrier(c, a);
       a.sig = op_sig(kAllReduce, dt, count);
@@ -474,6 +627,7 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   }
   // k real GPUs: NCCL reduce-scatter of the real part, synthesis on this
   // GPU's 1/k shard only, NCCL allgather.
+  log_path(c, "allreduce", count * es, "nccl reduce-scatter + synthesis + nccl allgather");
   const Nccl* n = nccl();
   cemuShardPlan plan;
   cemuPlanShards(count, c->k, c->li, &plan);
@@ -501,6 +655,11 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   });
   ph.push_back([=]() -> cemuResult_t {  // phase 2: everyone's shards
     if (shard) NCCL_OK(n->AllGather(r8 + c->li * shard * es, r8, shard, ndt, c->inner, s));
+    return cemuSuccess;
+  });
+  // phase 3: the delay, after the allgather (in a group NCCL launches it at
+  // the phase's ncclGroupEnd, so it must not share a phase with our kernels)
+  ph.push_back([=]() -> cemuResult_t {
     CUDA_OK(call->finish(kAllReduce));
     return cemuSuccess;
   });
@@ -535,6 +694,7 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
     const cemuComm::Region* rr = find_region(c, recv, sc * es * c->W);
     const uint64_t roff = rr ? static_cast<uint64_t>(r8 - rr->base) : 1;
     if (rr && roff % 16 == 0 && (sc * es) % 16 == 0) {  // symmetric conditions only
+      log_path(c, "allgather", sc * es, "fused");
       ph.push_back([=]() -> cemuResult_t {
       const void* own_src = send;
       if (reinterpret_cast<uintptr_t>(send) % 16 != 0) {  // local: stage into the own block
@@ -559,6 +719,7 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
       return cemuSuccess;
     }
   }
+  log_path(c, "allgather", sc * es, c->k == 1 ? "synthesis" : "synthesis + nccl allgather");
   const void* own = (c->k == 1 && !own_in_place) ? send : nullptr;
   ph.push_back([=]() -> cemuResult_t {  // emulated blocks, written locally
     CUDA_OK(launch_synth_fill(dt, recv, sc, c->d_virt_ranks, c->d_virt_keys, nvirt, 0, 0, own, c->rank,
@@ -579,6 +740,9 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
       }
       NCCL_OK(n->GroupEnd());
     }
+    return cemuSuccess;
+  });
+  if (c->k > 1) ph.push_back([=]() -> cemuResult_t {  // the delay, after the grouped NCCL launch
     CUDA_OK(call->finish(kAllGather));
     return cemuSuccess;
   });
@@ -621,6 +785,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
   const cemuComm::Region* rs = c->fused ? find_region(c, send, rc * es * c->W) : nullptr;
   const uint64_t sbase = rs ? static_cast<uint64_t>(s8 - rs->base) : 1;
   if (rs && es <= 4 && nk > 0 && sbase % 16 == 0 && (rc * es) % 16 == 0) {
+    log_path(c, "reduce-scatter", rc * es, "fused");
     ph.push_back([=]() -> cemuResult_t {
     const uint64_t soff = sbase + mine * es;
     void* out = recv;
@@ -650,6 +815,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
     });
     return cemuSuccess;
   }
+  log_path(c, "reduce-scatter", rc * es, "nccl reduce-scatter + synthesis");
   const Nccl* n = nccl();
   const auto ndt = static_cast<ncclDataType_t>(dt);
   ph.push_back([=]() -> cemuResult_t {  // phase 0: the real part over NCCL
@@ -697,6 +863,7 @@ cemuResult_t do_broadcast(const void* send, void* recv, size_t count, int dt, in
       CUDA_OK(call->stamp_now());
       const int lroot = static_cast<int>(std::find(c->real.begin(), c->real.end(), r) - c->real.begin());
       NCCL_OK(nccl()->Broadcast(send, recv, count, static_cast<ncclDataType_t>(dt), lroot, c->inner, s));
+      return cemuSuccess;  // the delay in the next phase (after a grouped NCCL launch)
     }
   } else if (c->mode == PayloadMode::kZero) {
     CUDA_OK(call->stamp_now());
@@ -708,6 +875,10 @@ cemuResult_t do_broadcast(const void* send, void* recv, size_t count, int dt, in
   CUDA_OK(call->finish(kBroadcast));
   return cemuSuccess;
   });
+  if (c->cfg.is_real(r) && c->k > 1) ph.push_back([=]() -> cemuResult_t {
+    CUDA_OK(call->finish(kBroadcast));
+    return cemuSuccess;
+  });
   return cemuSuccess;
 }
 
@@ -718,16 +889,31 @@ cemuResult_t do_broadcast(const void* send, void* recv, size_t count, int dt, in
 // (cemuCommInitAll) never blocks in a device's NCCL call while another
 // device's matching call has not been issued.  Every phase re-selects its
 // communicator's device.
+// The call's first phase waits for the communicator's previous call when
+// that was issued on another stream; a last phase of its own (after any
+// grouped NCCL launch of the previous phase) records the order event.
 template <typename F>
-cemuResult_t run_or_defer(cemuComm* c, F&& plan) {
+cemuResult_t run_or_defer(cemuComm* c, cudaStream_t s, F&& plan) {
   auto ops = std::make_shared<Phases>();
   if (auto r = plan(*ops)) return r;
+  if (ops->empty()) return cemuSuccess;  // zero-size call: nothing enqueued
+  ops->insert(ops->begin(), [c, s]() { return order_begin(c, s); });
+  ops->push_back([c, s]() { return order_end(c, s); });
   Phases wrapped;
+  int idx = 0;
   for (auto& f : *ops) {
-    wrapped.push_back([c, f]() -> cemuResult_t {
+    wrapped.push_back([c, f, idx]() -> cemuResult_t {
       if (cudaSetDevice(c->device) != cudaSuccess) return fail(cemuUnhandledCudaError, "cannot select device");
+      // a launch reports cudaGetLastError(): drop an error some earlier,
+      // unrelated runtime call left behind (e.g. a destroyed communicator's
+      // IPC unmapping) so it cannot fail this call
+      const cudaError_t pend = cudaGetLastError();
+      if (pend && std::getenv("CEMU_DEBUG_ERR")) {
+        std::fprintf(stderr, "cemu: stale error before phase %d: %s\n", idx, cudaGetErrorString(pend));
+      }
       return f();
     });
+    ++idx;
   }
   if (g_group_depth > 0) {
     g_group_ops.push_back(GroupOp{c, std::move(wrapped)});
@@ -922,7 +1108,7 @@ cemuResult_t cemuAllReduce(const void* send, void* recv, size_t count, cemuDataT
     const uint64_t b = static_cast<uint64_t>(count) * dtype_size(dt);
     return wire_call(c, kAllReduce, send, recv, b, b, static_cast<uint32_t>(dtype_size(dt)), s);
   }
-  return run_or_defer(c, [=](Phases& ph) { return do_allreduce(send, recv, count, dt, c, s, ph); });
+  return run_or_defer(c, s, [=](Phases& ph) { return do_allreduce(send, recv, count, dt, c, s, ph); });
 }
 
 
@@ -936,7 +1122,7 @@ cemuResult_t cemuAllGather(const void* send, void* recv, size_t sc, cemuDataType
     const uint64_t b = static_cast<uint64_t>(sc) * dtype_size(dt);
     return wire_call(c, kAllGather, send, recv, b * c->W, b, static_cast<uint32_t>(dtype_size(dt)), s);
   }
-  return run_or_defer(c, [=](Phases& ph) { return do_allgather(send, recv, sc, dt, c, s, ph); });
+  return run_or_defer(c, s, [=](Phases& ph) { return do_allgather(send, recv, sc, dt, c, s, ph); });
 }
 
 cemuResult_t cemuReduceScatter(const void* send, void* recv, size_t rc, cemuDataType_t dt, cemuRedOp_t op,
@@ -946,7 +1132,7 @@ cemuResult_t cemuReduceScatter(const void* send, void* recv, size_t rc, cemuData
   if (rc && (!send || !recv)) return fail(cemuInvalidArgument, "cemuReduceScatter: null buffer");
   if (c->wire) return fail(cemuInvalidUsage, "wire mode: the CEMU protocol has allreduce and allgather only");
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  return run_or_defer(c, [=](Phases& ph) { return do_reducescatter(send, recv, rc, dt, c, s, ph); });
+  return run_or_defer(c, s, [=](Phases& ph) { return do_reducescatter(send, recv, rc, dt, c, s, ph); });
 }
 
 cemuResult_t cemuBroadcast(const void* send, void* recv, size_t count, cemuDataType_t dt, int root,
@@ -955,7 +1141,7 @@ cemuResult_t cemuBroadcast(const void* send, void* recv, size_t count, cemuDataT
   if (count && !recv) return fail(cemuInvalidArgument, "cemuBroadcast: null recvbuff");
   if (c->wire) return fail(cemuInvalidUsage, "wire mode: the CEMU protocol has allreduce and allgather only");
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  return run_or_defer(c, [=](Phases& ph) { return do_broadcast(send, recv, count, dt, root, c, s, ph); });
+  return run_or_defer(c, s, [=](Phases& ph) { return do_broadcast(send, recv, count, dt, root, c, s, ph); });
 }
 
 cemuResult_t cemuGroupStart(void) {
@@ -1042,8 +1228,9 @@ cemuResult_t cemuMemAlloc(cemuComm_t c, size_t bytes, void** ptr) {
   r.base = static_cast<uint8_t*>(p);
   r.bytes = rounded;
   r.peer[c->li] = r.base;
+  r.id = c->next_region_id++;
   if (c->k > 1 && c->fused) {
-    if (auto e = map_peers(c, p, rounded, r.peer)) {
+    if (auto e = map_peers(c, p, rounded, r.peer, r.peer_map)) {
       cudaFree(p);
       return e;
     }
@@ -1057,22 +1244,91 @@ cemuResult_t cemuMemFree(cemuComm_t c, void* ptr) {
   if (!c || !ptr) return fail(cemuInvalidArgument, "cemuMemFree: bad argument");
   for (size_t i = 0; i < c->regions.size(); ++i) {
     auto& r = c->regions[i];
-    if (r.base != ptr) continue;
+    if (r.base != ptr || !r.owned) continue;
     cudaSetDevice(c->device);
-    for (uint32_t g = 0; g < c->k; ++g) {
-      if (g != c->li && r.peer[g]) cudaIpcCloseMemHandle(r.peer[g]);
-    }
-    if (c->k > 1 && c->fused) {  // every peer unmapped before anyone frees
-      std::vector<uint8_t> all;
-      ncclResult_t nr = ncclSuccess;
-      const uint8_t one = 1;
-      exchange_records(c, &one, 1, &all, &nr);
-    }
+    if (c->order_ev) cudaEventSynchronize(c->order_ev);  // no call of this comm still uses it
+    unmap_region(c, r);
     cudaFree(r.base);
     c->regions.erase(c->regions.begin() + static_cast<long>(i));
     return cemuSuccess;
   }
   return fail(cemuInvalidArgument, "cemuMemFree: pointer was not returned by cemuMemAlloc");
+}
+
+namespace {
+// cuMemGetAddressRange through the runtime's driver entry point (no link
+// against libcuda): the allocation holding `p`.
+using GetRangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+bool allocation_of(const void* p, void** base, size_t* bytes) {
+  static GetRangeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<GetRangeFn>(nullptr);
+    }
+    return reinterpret_cast<GetRangeFn>(f);
+  }();
+  unsigned long long b = 0;
+  size_t n = 0;
+  if (!fn || fn(&b, &n, reinterpret_cast<unsigned long long>(p)) != 0) return false;
+  *base = reinterpret_cast<void*>(b);
+  *bytes = n;
+  return true;
+}
+}  // namespace
+
+// ncclCommRegister / ncclCommWindowRegister (nccl.h 2.27.3:243, 251): the
+// caller's device range becomes a symmetric range of this communicator, so
+// collectives on it (at the same offsets on every real rank) take the fused
+// NVLink kernels.  Collective over the job's real ranks on this box, like
+// NCCL's window registration: each rank exports the cudaMalloc allocation
+// holding its range (CUDA IPC) and maps every peer's.
+cemuResult_t cemuCommRegister(cemuComm_t c, void* buff, size_t size, void** handle) {
+  if (!c || !handle) return fail(cemuInvalidArgument, "cemuCommRegister: null argument");
+  *handle = nullptr;
+  if (!buff || size == 0) return cemuSuccess;  // nothing to register (NCCL accepts it too)
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(cemuUnhandledCudaError, "cemuCommRegister: cudaSetDevice");
+  cemuComm::Region r;
+  r.base = static_cast<uint8_t*>(buff);
+  r.bytes = size;
+  r.owned = false;
+  r.peer[c->li] = r.base;
+  r.id = c->next_region_id++;
+  if (c->k > 1 && c->fused) {
+    void* base = nullptr;
+    size_t abytes = 0;
+    bool ok = allocation_of(buff, &base, &abytes);
+    std::string why;
+    if (!ok) {
+      why = "cemuCommRegister: the range is not device memory of this process";
+    } else if (static_cast<uint8_t*>(buff) + size > static_cast<uint8_t*>(base) + abytes) {
+      ok = false;
+      why = "cemuCommRegister: the range spans more than one allocation";
+    }
+    const uint64_t off = ok ? static_cast<uint64_t>(static_cast<uint8_t*>(buff) - static_cast<uint8_t*>(base)) : 0;
+    if (auto e = map_range(c, base, off, size, ok, why, r.peer, r.peer_map)) return e;
+  }
+  c->regions.push_back(r);
+  *handle = reinterpret_cast<void*>(static_cast<uintptr_t>(r.id));
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommDeregister(cemuComm_t c, void* handle) {
+  if (!c) return fail(cemuInvalidArgument, "cemuCommDeregister: comm is null");
+  if (!handle) return cemuSuccess;
+  const uint64_t id = static_cast<uint64_t>(reinterpret_cast<uintptr_t>(handle));
+  for (size_t i = 0; i < c->regions.size(); ++i) {
+    auto& r = c->regions[i];
+    if (r.id != id || r.owned) continue;
+    cudaSetDevice(c->device);
+    if (c->order_ev) cudaEventSynchronize(c->order_ev);  // no call of this comm still uses it
+    unmap_region(c, r);
+    c->regions.erase(c->regions.begin() + static_cast<long>(i));
+    return cemuSuccess;
+  }
+  return fail(cemuInvalidArgument, "cemuCommDeregister: handle was not returned by cemuCommRegister");
 }
 
 cemuResult_t cemuCommGetAsyncError(cemuComm_t c, cemuResult_t* err) {

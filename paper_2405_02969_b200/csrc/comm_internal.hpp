@@ -121,14 +121,45 @@ struct cemuComm {
   uint8_t* peer_sig[kMaxReal] = {};       // every real GPU's area (own = sig)
   bool fused = true;
   int64_t fused_timeout_ns = 30'000'000'000LL;
+  // A symmetric range: mapped on every real GPU, so fused kernels reach the
+  // peers' copies over NVLink.  cemuMemAlloc allocations (owned), the host
+  // pipe's buffers (owned) and caller memory registered with
+  // cemuCommRegister (ncclCommRegister / ncclCommWindowRegister; not owned).
   struct Region {
     uint8_t* base = nullptr;
     size_t bytes = 0;
-    uint8_t* peer[kMaxReal] = {};  // own = base
+    uint8_t* peer[kMaxReal] = {};      // every real GPU's copy of `base` (own = base)
+    uint8_t* peer_map[kMaxReal] = {};  // the IPC mapping each peer[g] lies in (closed on release)
+    bool owned = true;                 // base is a cudaMalloc of this communicator
+    uint64_t id = 0;                   // registration handle (cemuCommRegister)
   };
   std::vector<Region> regions;
+  uint64_t next_region_id = 1;
+  // IPC mappings opened in this process, shared by every region inside the
+  // same peer allocation (a handle is opened once): key = peer index + handle
+  struct IpcMap {
+    void* ptr = nullptr;
+    int refs = 0;
+  };
+  std::map<std::string, IpcMap> ipc_maps;
   void* scratch = nullptr;  // aligned staging for misaligned local outputs
   size_t scratch_bytes = 0;
+  // Device buffers superseded by a larger one (scratch, copy-engine
+  // staging).  An enqueued call -- or a captured graph -- may still use them,
+  // so they are released only when the communicator is destroyed, never by
+  // a device-wide synchronize on the enqueue path.
+  std::vector<void*> retired;
+  // Per-communicator call order across streams (NCCL's semantics; the
+  // reference runs a session's ops strictly in order, one in flight:
+  // collective.hpp:43-47, collective.cpp:357-404).  Every call records
+  // order_ev on its stream when it is enqueued; a call on another stream
+  // first waits for it.  Fused multi-GPU kernels spin on peer flags, so two
+  // of them in flight at once would share the signal area's epoch and CTA
+  // counter -- and could deadlock on SM occupancy -- without this.
+  cudaEvent_t order_ev = nullptr;
+  cudaStream_t order_stream = nullptr;
+  bool order_recorded = false;
+  unsigned long long order_capture = 0;  // capture id of the last record (0: recorded eagerly)
   // host-buffer collectives (cemuAllReduceHost / cemuAllGatherHost): chunks
   // ride a 3-stage pipeline -- H2D copy engine, synthesis kernel, D2H copy
   // engine -- over kPipeBufs rotating device buffers, so both PCIe
@@ -166,9 +197,11 @@ struct cemuComm {
     cudaSetDevice(device);
     wire.reset();  // BYE to the emulator
     auto& p = pipe;
-    for (cudaStream_t st : {p.h2d, p.comp, p.d2h}) {
+    // every internal stream drains before any mapping is closed or memory freed
+    for (cudaStream_t st : {p.h2d, p.comp, p.d2h, cep.pull, cep.push}) {
       if (st) cudaStreamSynchronize(st);
     }
+    if (order_ev) cudaEventSynchronize(order_ev);
     for (int b = 0; b < kPipeBufs; ++b) {
       if (!p.symmetric && p.buf[b]) cudaFree(p.buf[b]);  // symmetric buffers are regions (below)
       for (cudaEvent_t ev : {p.loaded[b], p.done[b], p.drained[b]}) {
@@ -180,20 +213,16 @@ struct cemuComm {
       if (st) cudaStreamDestroy(st);
     }
     for (auto& r : regions) {
-      for (uint32_t g = 0; g < k; ++g) {
-        if (g != li && r.peer[g]) cudaIpcCloseMemHandle(r.peer[g]);
-      }
-      cudaFree(r.base);
+      if (r.owned) cudaFree(r.base);
     }
-    for (uint32_t g = 0; g < k && g < static_cast<uint32_t>(kMaxReal); ++g) {
-      if (g != li && peer_sig[g]) cudaIpcCloseMemHandle(peer_sig[g]);
+    for (auto& m : ipc_maps) {
+      if (m.second.ptr) cudaIpcCloseMemHandle(m.second.ptr);
     }
     for (cudaStream_t st : {cep.pull, cep.push}) {
-      if (st) {
-        cudaStreamSynchronize(st);
-        cudaStreamDestroy(st);
-      }
+      if (st) cudaStreamDestroy(st);
     }
+    if (order_ev) cudaEventDestroy(order_ev);
+    for (void* r : retired) cudaFree(r);
     for (cudaEvent_t ev : cep.ev) {
       if (ev) cudaEventDestroy(ev);
     }
@@ -211,6 +240,7 @@ struct cemuComm {
     cudaFree(d_virt_keys);
     cudaFree(d_virt_ranks);
     cudaFree(d_slots);
+    cudaGetLastError();  // a destructor reports nothing: leave no stale error behind
   }
 };
 
@@ -327,8 +357,17 @@ struct Call {
 
 // ---- shared helpers (comm.cpp) ----
 // Maps every real GPU's allocation `local` (collectively) into this process.
-cemuResult_t map_peers(cemuComm* c, void* local, size_t bytes, uint8_t** peers);
+cemuResult_t map_peers(cemuComm* c, void* local, size_t bytes, uint8_t** peers, uint8_t** peer_maps = nullptr);
+// Drops the region's peer mappings (every real rank collectively: no peer
+// still maps this GPU's memory when the call returns).
+void unmap_region(cemuComm* c, cemuComm::Region& r);
 cemuResult_t ensure_scratch(cemuComm* c, size_t bytes);
+// Grows *buf to >= bytes; the superseded buffer goes to c->retired.
+cemuResult_t grow_buffer(cemuComm* c, void** buf, size_t* have, size_t bytes, const char* what);
+// Call order across streams (see cemuComm::order_ev): before the call's
+// first enqueue / after its last one, on the call's stream.
+cemuResult_t order_begin(cemuComm* c, cudaStream_t s);
+cemuResult_t order_end(cemuComm* c, cudaStream_t s);
 // 20-bit signature of a fused call; every real rank must compute the same
 uint32_t op_sig(int coll, int dt, uint64_t count);
 const cemuComm::Region* find_region(const cemuComm* c, const void* p, size_t bytes);

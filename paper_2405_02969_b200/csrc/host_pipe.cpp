@@ -38,7 +38,8 @@ cemuResult_t ensure_pipe(cemuComm* c) {
       r.base = static_cast<uint8_t*>(d);
       r.bytes = rounded;
       r.peer[c->li] = r.base;
-      if (auto e = map_peers(c, d, rounded, r.peer)) {
+      r.id = c->next_region_id++;
+      if (auto e = map_peers(c, d, rounded, r.peer, r.peer_map)) {
         cudaFree(d);
         return e;
       }
@@ -215,7 +216,10 @@ cemuResult_t cemuAllReduceHost(const void* send, void* recv, size_t count, cemuD
   if (c->wire) return fail(cemuInvalidUsage, "cemuAllReduceHost: not available in wire mode");
   if (count == 0) return cemuSuccess;
   try {
-    return host_allreduce(send, recv, count, dt, c, reinterpret_cast<cudaStream_t>(stream));
+    const auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (auto r = order_begin(c, s)) return r;
+    if (auto r = host_allreduce(send, recv, count, dt, c, s)) return r;
+    return order_end(c, s);
   } catch (const std::exception& e) {
     return fail(cemuInternalError, e.what());
   }
@@ -229,7 +233,10 @@ cemuResult_t cemuAllGatherHost(const void* send, void* recv, size_t sc, cemuData
   if (c->wire) return fail(cemuInvalidUsage, "cemuAllGatherHost: not available in wire mode");
   if (sc == 0) return cemuSuccess;
   try {
-    return host_allgather(send, recv, sc, dt, c, reinterpret_cast<cudaStream_t>(stream));
+    const auto s = reinterpret_cast<cudaStream_t>(stream);
+    if (auto r = order_begin(c, s)) return r;
+    if (auto r = host_allgather(send, recv, sc, dt, c, s)) return r;
+    return order_end(c, s);
   } catch (const std::exception& e) {
     return fail(cemuInternalError, e.what());
   }

@@ -96,3 +96,50 @@ def test_integration_recipe_cpp_session(cuda, tmp_path):
     own = ((np.arange(blk) + rank + 1) % 256).astype(np.uint8)
     want_ag = P.allgather(1, P.PAYLOAD_HASH, W, [rank], rank, 1, [own], blk)
     assert np.array_equal(got_ag, want_ag)
+
+
+def run_mp_app(tmp_path, n, world, count, mode, iters=3, extra_env=None):
+    """Starts tests/apps/nccl_mp_app on GPUs 0..n-1 (real ranks 0..n-1 of a
+    world of `world`) under the interposer; returns [(result, stdout, stderr)]."""
+    app = os.path.join(ROOT, "tests", "apps", "nccl_mp_app")
+    cfg = tmp_path / f"job_{mode}.cfg"
+    cfg.write_text(f"world_size = {world}\nreal_ranks = {','.join(map(str, range(n)))}\nbucket_bytes = 1\n")
+    idfile = tmp_path / f"id_{mode}"
+    env = dict(os.environ, CEMU_CONFIG=str(cfg), LD_PRELOAD=SHIM, CEMU_DEBUG="INFO", **(extra_env or {}))
+    procs = []
+    for r in range(n):
+        out = tmp_path / f"out_{mode}_{r}.bin"
+        procs.append((out, subprocess.Popen([app, str(world), str(r), str(r), str(count), mode, str(idfile), str(out),
+                                             str(iters)], env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                            text=True)))
+    res = []
+    for out, p in procs:
+        so, se = p.communicate(timeout=240)
+        assert p.returncode == 0, so + se
+        res.append((np.fromfile(out, dtype=np.float32), so, se))
+    return res
+
+
+def mp_inputs(n, count):
+    i = np.arange(count, dtype=np.int64)
+    return [(((7 * i + 13 * r) % 61) - 30).astype(np.float32) * 0.125 for r in range(n)]
+
+
+@pytest.mark.skipif(not __import__("torch").cuda.is_available() or __import__("torch").cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("mode,path", [("plain", "nccl reduce-scatter"), ("register", "fused"), ("window", "fused")])
+def test_multi_process_nccl_app_reaches_the_fused_path(tmp_path, mode, path):
+    """An unmodified multi-process NCCL job (one process per GPU) under
+    LD_PRELOAD: buffers it registers (ncclCommRegister on cudaMalloc memory,
+    or ncclMemAlloc + ncclCommWindowRegister) take the fused NVLink kernel;
+    unregistered ones the NCCL reduce-scatter + synthesis + allgather path.
+    Every rank's result equals the oracle bit for bit."""
+    import torch
+    n = min(torch.cuda.device_count(), 4)
+    world, count = 8 * n, (3 << 20) + 16 * n
+    sends = mp_inputs(n, count)
+    for r, (got, so, se) in enumerate(run_mp_app(tmp_path, n, world, count, mode)):
+        assert f"mode {mode}" in so and "async_error 0" in so, so
+        assert f"allreduce {count * 4} B -> {path}" in se, se[-2000:]
+        want = P.allreduce(7, P.PAYLOAD_HASH, world, list(range(n)), r, 1, sends, count)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (mode, r)
