@@ -170,6 +170,21 @@ cemuResult_t cemuMemFree(cemuComm_t comm, void* ptr);
  * size registers nothing (*handle = NULL). */
 cemuResult_t cemuCommRegister(cemuComm_t comm, void* buff, size_t size, void** handle);
 cemuResult_t cemuCommDeregister(cemuComm_t comm, void* handle);
+/* Synthesis cache.  The emulated ranks' payloads depend only on
+ * (seed, rank, element index), so their per-element sums are the same in
+ * every call over the same element range.  A call over a range of >= 1 MiB
+ * with >= minPeers emulated ranks writes those sums into a per-communicator
+ * cache (2 bytes per element for the byte kinds up to 256 emulated ranks,
+ * else 4) and later calls over the range fold from it -- a memory-bound pass
+ * instead of issue-bound synthesis, with identical bits.  capBytes bounds
+ * each of the two caches (byte kinds / 32-bit integer kinds; default
+ * CEMU_SYNTH_CACHE_MB = 4096 MiB, minPeers CEMU_SYNTH_CACHE_MIN_PEERS = 16);
+ * capBytes = 0 turns caching off.  Calling this drops every entry. */
+cemuResult_t cemuCommSetSynthCache(cemuComm_t comm, size_t capBytes, uint32_t minPeers);
+/* Fills (misses that wrote entries) and hits so far, and the device bytes
+ * the caches hold. */
+cemuResult_t cemuCommSynthCacheStats(cemuComm_t comm, uint64_t* fills, uint64_t* hits, size_t* bytes);
+
 /* Errors raised inside the fused kernel (a peer that never arrived at a
  * barrier within CEMU_FUSED_TIMEOUT_S); synchronous read. */
 cemuResult_t cemuCommGetAsyncError(cemuComm_t comm, cemuResult_t* asyncError);

@@ -100,6 +100,10 @@ def _load():
         "cemuBroadcast": (i32, [vp, vp, sz, i32, i32, vp, vp]),
         "cemuMemAlloc": (i32, [vp, sz, C.POINTER(vp)]),
         "cemuMemFree": (i32, [vp, vp]),
+        "cemuCommRegister": (i32, [vp, vp, sz, C.POINTER(vp)]),
+        "cemuCommDeregister": (i32, [vp, vp]),
+        "cemuCommSetSynthCache": (i32, [vp, sz, u32]),
+        "cemuCommSynthCacheStats": (i32, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(sz)]),
         "cemuCommGetAsyncError": (i32, [vp, C.POINTER(i32)]),
         "cemuGroupStart": (i32, []),
         "cemuGroupEnd": (i32, []),

@@ -306,6 +306,29 @@ class Communicator:
         check(lib.cemuMemFree(self._h, C.c_void_p(ptr)), self._h)
         self._allocs.remove(ptr)
 
+    def register(self, t: torch.Tensor) -> int:
+        """cemuCommRegister (ncclCommRegister): collective over the real
+        ranks; collectives on registered tensors (same offsets on every rank)
+        take the fused kernels.  Returns the handle for deregister()."""
+        h = C.c_void_p()
+        check(lib.cemuCommRegister(self._h, C.c_void_p(t.data_ptr()), t.numel() * t.element_size(),
+                                   C.byref(h)), self._h)
+        return h.value or 0
+
+    def deregister(self, handle: int) -> None:
+        check(lib.cemuCommDeregister(self._h, C.c_void_p(handle)), self._h)
+
+    # -- synthesis cache (DESIGN §4) -------------------------------------------
+    def set_synth_cache(self, cap_bytes: int, min_peers: int = 16) -> None:
+        """Bound (0 = off) the per-element cache of the emulated ranks' sums;
+        drops every entry."""
+        check(lib.cemuCommSetSynthCache(self._h, cap_bytes, min_peers), self._h)
+
+    def synth_cache_stats(self) -> dict:
+        f, h, b = C.c_uint64(), C.c_uint64(), C.c_size_t()
+        check(lib.cemuCommSynthCacheStats(self._h, C.byref(f), C.byref(h), C.byref(b)), self._h)
+        return {"fills": f.value, "hits": h.value, "bytes": b.value}
+
     def async_error(self) -> str | None:
         e = C.c_int()
         check(lib.cemuCommGetAsyncError(self._h, C.byref(e)), self._h)

@@ -242,6 +242,115 @@ bool capturing(cudaStream_t s) {
   return cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
 }
 
+// ---- synthesis cache ----------------------------------------------------
+namespace {
+bool covered(const cemuComm::SynthCache& sc, uint64_t b, uint64_t e) {
+  for (const auto& r : sc.covered) {
+    if (r.first <= b && e <= r.second) return true;
+  }
+  return false;
+}
+
+void cover(cemuComm::SynthCache& sc, uint64_t b, uint64_t e) {
+  sc.covered.emplace_back(b, e);
+  std::sort(sc.covered.begin(), sc.covered.end());
+  std::vector<std::pair<uint64_t, uint64_t>> m;
+  for (const auto& r : sc.covered) {
+    if (!m.empty() && r.first <= m.back().second) {
+      m.back().second = std::max(m.back().second, r.second);
+    } else {
+      m.push_back(r);
+    }
+  }
+  sc.covered.swap(m);
+}
+
+bool cacheable_dtype(int dt) {
+  return dt == cemuFloat32 || dt == cemuBfloat16 || dt == cemuFloat16 || dt == cemuUint8 || dt == cemuInt8 ||
+         dt == cemuInt32 || dt == cemuUint32;
+}
+
+// The cache to use for elements [b, e) of dtype dt, or none.  *fill: the
+// entries must be written first (this call's own pass fills them).
+CacheRef cache_for(cemuComm* c, int dt, uint64_t b, uint64_t e, cudaStream_t s, bool* fill) {
+  *fill = false;
+  if (c->mode != PayloadMode::kHash || c->cache_cap == 0 || c->virt.size() < c->cache_min_peers ||
+      !cacheable_dtype(dt) || b % 4 != 0 || e <= b) {
+    return {};
+  }
+  // small calls are launch-bound either way: not worth an entry
+  if ((e - b) * dtype_size(dt) < (1u << 20)) return {};
+  const bool words = dt == cemuInt32 || dt == cemuUint32;
+  auto& sc = words ? c->cache_words : c->cache_bytes;
+  if (sc.kind == kNoCache) sc.kind = (words || c->virt.size() > 256) ? kCacheWide32 : kCacheLanes16;
+  const uint64_t end = words ? e : (e + 3) / 4 * 4;  // the fill writes whole payload words
+  const size_t need = end * cache_entry_bytes(sc.kind);
+  if (need > c->cache_cap) return {};
+  const bool cap = capturing(s);
+  if (covered(sc, b, e) && sc.bytes >= need) {
+    ++c->cache_hits;
+    return CacheRef{sc.ptr, sc.kind};
+  }
+  if (cap) return {};  // no allocation and no fill inside a capture: synthesise
+  if (sc.bytes < need) {
+    // grow (64 MiB steps, within the cap); the old entries are dropped
+    const size_t step = 64ull << 20;
+    const size_t want = std::min(c->cache_cap, (need + step - 1) / step * step);
+    void* p = nullptr;
+    if (cudaMalloc(&p, want) != cudaSuccess) {
+      cudaGetLastError();
+      return {};
+    }
+    if (sc.ptr) c->retired.push_back(sc.ptr);  // an enqueued or captured call may still read it
+    sc.ptr = p;
+    sc.bytes = want;
+    sc.covered.clear();
+  }
+  cover(sc, b, e);  // every later call of this comm is ordered after this one's fill
+  ++c->cache_fills;
+  *fill = true;
+  return CacheRef{sc.ptr, sc.kind};
+}
+}  // namespace
+
+cudaError_t synth_reduce(cemuComm* c, int dt, const void* src, void* dst, uint64_t count, uint64_t e0,
+                         int64_t* stamp, cudaStream_t s, int* launches) {
+  const uint32_t nk = static_cast<uint32_t>(c->virt.size());
+  const bool al = (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 == 0;
+  bool fill = false;
+  const CacheRef cr = al ? cache_for(c, dt, e0, e0 + count, s, &fill) : CacheRef{};
+  if (!cr.ptr) return launch_synth_reduce(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches);
+  if (fill) {
+    if (stamp) {  // the call starts with the fill
+      if (const cudaError_t e = launch_stamp(stamp, s, launches)) return e;
+      stamp = nullptr;
+    }
+    const bool words = dt == cemuInt32 || dt == cemuUint32;
+    if (const cudaError_t e = launch_synth_cache_fill(words, e0, count, c->d_virt_keys, nk, cr, s, launches)) return e;
+  }
+  return launch_synth_reduce(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, cr);
+}
+
+cudaError_t cache_fused(cemuComm* c, int dt, FusedArgs& a, cudaStream_t s, int* launches) {
+  const bool words = dt == cemuInt32 || dt == cemuUint32;
+  const uint64_t epv = 16 / dtype_size(dt);
+  auto elem_of = [&](uint64_t v) { return words ? a.word_base + v * 4 : (a.word_base + v * (epv / 4)) * 4; };
+  const uint64_t b = elem_of(a.v_begin), e = elem_of(a.v_end) + a.ntail;
+  bool fill = false;
+  const CacheRef cr = cache_for(c, dt, b, e, s, &fill);
+  if (!cr.ptr) return cudaSuccess;
+  if (fill) {
+    if (a.stamp) {
+      if (const cudaError_t r = launch_stamp(a.stamp, s, launches)) return r;
+      a.stamp = nullptr;
+    }
+    if (const cudaError_t r = launch_synth_cache_fill(words, b, e - b, a.keys, a.nkeys, cr, s, launches)) return r;
+  }
+  a.cache = cr.ptr;
+  a.cache_kind = cr.kind;
+  return cudaSuccess;
+}
+
 // CEMU_ORDER=0 removes the ordering (diagnostic: tests/interleave_worker.py
 // shows what goes wrong without it)
 bool ordering_on() {
@@ -358,6 +467,13 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
   c->delay.intra_beta_us_per_byte = cfg.intra_beta_us_per_byte;
   c->delay_active = cfg.delay_kind != DelayKind::kNone || cfg.delay_inject_us != 0.0;
   c->config_delay_active = c->delay_active;
+  {
+    const char* mb = std::getenv("CEMU_SYNTH_CACHE_MB");
+    c->cache_cap = (mb ? std::strtoull(mb, nullptr, 10) : 4096ull) << 20;
+    if (const char* mp = std::getenv("CEMU_SYNTH_CACHE_MIN_PEERS")) {
+      c->cache_min_peers = static_cast<uint32_t>(std::max(1, std::atoi(mp)));
+    }
+  }
   if (c->mode == PayloadMode::kZero && c->k != 1) {
     return fail(cemuInvalidUsage,
                 "payload.mode: zero reproduces the reference emulator, which serves exactly "
@@ -518,6 +634,7 @@ cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs,
   uint4* peer_recv = a.dst[peer];
   uint4* my_recv = a.dst[a.me];
   a.stamp = call->take_stamp();
+  CUDA_OK(cache_fused(c, dt, a, s, &call->launches));  // the fold-only chunks inherit it
   CUDA_OK(launch_peer_barrier(a, 0, s, &call->launches));
   cudaEvent_t started = p.ev[0], pushed = p.ev[1];
   CUDA_OK(cudaEventRecord(started, s));
@@ -561,7 +678,6 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   if (count == 0) return cemuSuccess;
   auto call = std::make_shared<Call>(c, kAllReduce, count * es, s);
   if (!call->error.empty()) return fail(cemuInvalidArgument, call->error);
-  const auto* nv = c->d_virt_keys;
   const uint32_t nk = static_cast<uint32_t>(c->virt.size());
   if (c->mode == PayloadMode::kZero) ph.push_back([=]() -> cemuResult_t {
     // A10: zero replies; the real rank keeps chunk (rank+1) mod W
@@ -585,7 +701,7 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   if (c->k == 1) {
     log_path(c, "allreduce", count * es, "synthesis");
     ph.push_back([=]() -> cemuResult_t {
-      CUDA_OK(launch_synth_reduce(dt, send, recv, count, 0, nv, nk, call->take_stamp(), s, &call->launches));
+      CUDA_OK(synth_reduce(c, dt, send, recv, count, 0, call->take_stamp(), s, &call->launches));
       CUDA_OK(call->finish(kAllReduce));
       return cemuSuccess;
     });
@@ -619,6 +735,7 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
       a.sig = op_sig(kAllReduce, dt, count);
       a.ndst = a.k;
       a.stamp = call->take_stamp();
+      CUDA_OK(cache_fused(c, dt, a, s, &call->launches));
       CUDA_OK(launch_fused_allreduce(dt, a, s, &call->launches));
       CUDA_OK(call->finish(kAllReduce));
       return cemuSuccess;
@@ -644,12 +761,12 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
   });
   ph.push_back([=]() -> cemuResult_t {  // phase 1: the emulated part on the own shard
     if (shard) {
-      CUDA_OK(launch_synth_reduce(dt, r8 + c->li * shard * es, r8 + c->li * shard * es, shard,
-                                  c->li * shard, nv, nk, nullptr, s, &call->launches));
+      CUDA_OK(synth_reduce(c, dt, r8 + c->li * shard * es, r8 + c->li * shard * es, shard, c->li * shard, nullptr,
+                           s, &call->launches));
     }
     if (rem) {
-      CUDA_OK(launch_synth_reduce(dt, r8 + c->k * shard * es, r8 + c->k * shard * es, rem,
-                                  c->k * shard, nv, nk, nullptr, s, &call->launches));
+      CUDA_OK(synth_reduce(c, dt, r8 + c->k * shard * es, r8 + c->k * shard * es, rem, c->k * shard, nullptr, s,
+                           &call->launches));
     }
     return cemuSuccess;
   });
@@ -769,7 +886,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
   const uint32_t nk = static_cast<uint32_t>(c->virt.size());
   if (c->k == 1) {
     ph.push_back([=]() -> cemuResult_t {
-      CUDA_OK(launch_synth_reduce(dt, s8 + mine * es, recv, rc, mine, c->d_virt_keys, nk,
+      CUDA_OK(synth_reduce(c, dt, s8 + mine * es, recv, rc, mine,
                                   call->take_stamp(), s, &call->launches));
       CUDA_OK(call->finish(kReduceScatter));
       return cemuSuccess;
@@ -808,6 +925,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
     a.keys = c->d_virt_keys;
     a.nkeys = nk;
     a.stamp = call->take_stamp();
+    CUDA_OK(cache_fused(c, dt, a, s, &call->launches));
     CUDA_OK(launch_fused_allreduce(dt, a, s, &call->launches));
     if (out != recv) CUDA_OK(cudaMemcpyAsync(recv, out, rc * es, cudaMemcpyDeviceToDevice, s));
     CUDA_OK(call->finish(kReduceScatter));
@@ -834,7 +952,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
   return cemuSuccess;
   });
   ph.push_back([=]() -> cemuResult_t {  // phase 1: the emulated part
-    CUDA_OK(launch_synth_reduce(dt, recv, recv, rc, mine, c->d_virt_keys, nk, nullptr, s, &call->launches));
+    CUDA_OK(synth_reduce(c, dt, recv, recv, rc, mine, nullptr, s, &call->launches));
     CUDA_OK(call->finish(kReduceScatter));
     return cemuSuccess;
   });
@@ -1329,6 +1447,30 @@ cemuResult_t cemuCommDeregister(cemuComm_t c, void* handle) {
     return cemuSuccess;
   }
   return fail(cemuInvalidArgument, "cemuCommDeregister: handle was not returned by cemuCommRegister");
+}
+
+cemuResult_t cemuCommSetSynthCache(cemuComm_t c, size_t cap, uint32_t min_peers) {
+  if (!c) return fail(cemuInvalidArgument, "cemuCommSetSynthCache: comm is null");
+  if (min_peers == 0) return fail(cemuInvalidArgument, "cemuCommSetSynthCache: minPeers must be >= 1");
+  c->cache_cap = cap;
+  c->cache_min_peers = min_peers;
+  for (auto* sc : {&c->cache_bytes, &c->cache_words}) {
+    sc->covered.clear();  // buffers stay (an enqueued call may read them); entries are refilled
+    if (sc->bytes > cap && sc->ptr) {
+      c->retired.push_back(sc->ptr);
+      sc->ptr = nullptr;
+      sc->bytes = 0;
+    }
+  }
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommSynthCacheStats(cemuComm_t c, uint64_t* fills, uint64_t* hits, size_t* bytes) {
+  if (!c) return fail(cemuInvalidArgument, "cemuCommSynthCacheStats: comm is null");
+  if (fills) *fills = c->cache_fills;
+  if (hits) *hits = c->cache_hits;
+  if (bytes) *bytes = c->cache_bytes.bytes + c->cache_words.bytes;
+  return cemuSuccess;
 }
 
 cemuResult_t cemuCommGetAsyncError(cemuComm_t c, cemuResult_t* err) {

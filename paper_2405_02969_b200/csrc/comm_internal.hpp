@@ -156,6 +156,22 @@ struct cemuComm {
   // first waits for it.  Fused multi-GPU kernels spin on peer flags, so two
   // of them in flight at once would share the signal area's epoch and CTA
   // counter -- and could deadlock on SM occupancy -- without this.
+  // Synthesis cache (kernels.hpp CacheRef): the emulated
+  // peers' per-element sums, written by the first call over an element
+  // range and folded from by every later call over it.  One cache for the
+  // byte kinds (u8/i8/fp16/bf16/fp32 share byte_r(e)), one for the 32-bit
+  // integer kinds.  Buffers only grow (the old one is retired, its coverage
+  // dropped); nothing is filled inside a stream capture.
+  struct SynthCache {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    int kind = kNoCache;
+    std::vector<std::pair<uint64_t, uint64_t>> covered;  // element ranges with entries: sorted, disjoint
+  };
+  SynthCache cache_bytes, cache_words;
+  size_t cache_cap = 0;           // bytes per cache (CEMU_SYNTH_CACHE_MB; 0 = off)
+  uint32_t cache_min_peers = 16;  // CEMU_SYNTH_CACHE_MIN_PEERS
+  uint64_t cache_fills = 0, cache_hits = 0;
   cudaEvent_t order_ev = nullptr;
   cudaStream_t order_stream = nullptr;
   bool order_recorded = false;
@@ -223,6 +239,8 @@ struct cemuComm {
     }
     if (order_ev) cudaEventDestroy(order_ev);
     for (void* r : retired) cudaFree(r);
+    cudaFree(cache_bytes.ptr);
+    cudaFree(cache_words.ptr);
     for (cudaEvent_t ev : cep.ev) {
       if (ev) cudaEventDestroy(ev);
     }
@@ -391,6 +409,14 @@ void set_barrier(cemuComm* c, A& a) {
   a.epoch = reinterpret_cast<uint64_t*>(c->sig + 264);
   a.timeout_ns = c->fused_timeout_ns;
 }
+
+// Synthesis through the cache where it applies (else plain synthesis):
+// launch_synth_reduce's arguments; fills the cache first on a miss.
+cudaError_t synth_reduce(cemuComm* c, int dt, const void* src, void* dst, uint64_t count, uint64_t e0,
+                         int64_t* stamp, cudaStream_t s, int* launches);
+// The fused kernel's slice through the cache (sets a.cache / a.cache_kind,
+// launches the fill on a miss).
+cudaError_t cache_fused(cemuComm* c, int dt, FusedArgs& a, cudaStream_t s, int* launches);
 
 // ---- host_pipe.cpp ----
 cemuResult_t host_allreduce(const void* send, void* recv, size_t count, int dt, cemuComm* c, cudaStream_t s);

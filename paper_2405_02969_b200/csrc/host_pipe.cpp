@@ -143,11 +143,12 @@ cemuResult_t host_allreduce(const void* send, void* recv, size_t count, int dt, 
         FusedArgs a = fused_allreduce_args(c, dt, n, e0, c->pipe.peer[b], c->pipe.peer[b]);  // in place
         set_barrier(c, a);
         a.sig = op_sig(kAllReduce, dt, n);
+        if (const cudaError_t e = cache_fused(c, dt, a, st, &call->launches)) return e;
         return launch_fused_allreduce(dt, a, st, &call->launches);
       };
     } else {
       ch.work = [c, call, dt, n, e0, nk](int, void* d, cudaStream_t st) {
-        return launch_synth_reduce(dt, d, d, n, e0, c->d_virt_keys, nk, nullptr, st, &call->launches);
+        return synth_reduce(c, dt, d, d, n, e0, nullptr, st, &call->launches);
       };
     }
     chunks.push_back(std::move(ch));

@@ -52,6 +52,12 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return v;
 }
 
+__device__ __forceinline__ uint2 ld_stream64(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
                "r"(v.z), "r"(v.w)
@@ -154,6 +160,34 @@ __device__ void elem_reduce(const void* src, void* dst, uint64_t i, uint64_t e,
   }
 }
 
+// elem_reduce from the synthesis cache: t = the peers' byte sum (or word
+// sum) of element e, so s = t - 128 n is elem_reduce's dyadic sum exactly.
+template <int DT>
+__device__ void elem_fold_cached(const void* src, void* dst, uint64_t i, uint64_t e, const void* cache, bool wide,
+                                 uint32_t nkeys) {
+  if constexpr (DT == cemuInt32 || DT == cemuUint32) {
+    static_cast<uint32_t*>(dst)[i] = static_cast<const uint32_t*>(src)[i] + static_cast<const uint32_t*>(cache)[e];
+  } else if constexpr (DT == cemuInt64 || DT == cemuUint64 || DT == cemuFloat64) {
+    __trap();  // never cached (scalar path only)
+  } else {
+    const uint32_t t = wide ? static_cast<const uint32_t*>(cache)[e] : static_cast<const uint16_t*>(cache)[e];
+    if constexpr (DT == cemuInt8 || DT == cemuUint8) {
+      static_cast<uint8_t*>(dst)[i] = static_cast<uint8_t>(static_cast<const uint8_t*>(src)[i] + t);
+    } else {
+      const int32_t sum = static_cast<int32_t>(t) - 128 * static_cast<int32_t>(nkeys);
+      if constexpr (DT == cemuFloat32) {
+        static_cast<float*>(dst)[i] = fold_f32(static_cast<const float*>(src)[i], sum);
+      } else if constexpr (DT == cemuFloat16) {
+        const __half x = static_cast<const __half*>(src)[i];
+        static_cast<__half*>(dst)[i] = __float2half_rn(fold_f32(__half2float(x), sum));
+      } else {
+        const __nv_bfloat16 x = static_cast<const __nv_bfloat16*>(src)[i];
+        static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(fold_f32(__bfloat162float(x), sum));
+      }
+    }
+  }
+}
+
 template <int DT>
 __device__ void elem_fill(void* dst, uint64_t i, uint64_t e, uint32_t raw_key) {
   const uint2 key = peer_consts(raw_key);
@@ -191,8 +225,14 @@ __device__ __forceinline__ void load_keys(uint2* skeys, const uint32_t* keys, ui
 //            so the pairs start on a 16-byte boundary
 //   kSeed2   even peer count: peers 0 and 1 seed the sums, pairs after
 //   kGroups  > 256 byte-kind peers: 256-peer groups, lanes flushed per group
-enum PeerMode { kSeed1 = 0, kSeed2 = 1, kGroups = 2 };
+//   kCache16 no synthesis: the peers' per-element byte sums t (<= 256
+//            peers, uint16 lanes) are read from the communicator's synthesis
+//            cache (synth_cache_fill wrote them; see "synthesis cache" below)
+//   kCache32 the same with uint32 entries: byte sums of > 256 peers, or the
+//            wrapping word sums of the 32-bit integer kinds
+enum PeerMode { kSeed1 = 0, kSeed2 = 1, kGroups = 2, kCache16 = 3, kCache32 = 4 };
 __host__ __device__ constexpr uint32_t key_shift(int mode) { return mode == kSeed1 ? 1u : 0u; }
+__host__ __device__ constexpr bool cached(int mode) { return mode >= kCache16; }
 inline int peer_mode(bool words, uint32_t nkeys) {
   if (!words && nkeys > 256) return kGroups;  // 16-bit lanes hold <= 257 bytes
   return (nkeys & 1) ? kSeed1 : kSeed2;
@@ -325,6 +365,39 @@ __device__ __forceinline__ void ah_to_lanes(uint32_t a, uint32_t h, uint32_t n, 
   }
 }
 
+// The same lanes from cached byte sums: t16 = the word's four uint16 lane
+// sums packed as (t0 | t1 << 16, t2 | t3 << 16) -- exactly the values
+// ah_to_lanes decodes from (A, H), so the result is bit-identical.
+template <int K>
+__device__ __forceinline__ void t16_to_lanes(uint32_t w01, uint32_t w23, uint32_t n, uint32_t* r) {
+  if constexpr (K == kU8) {
+    r[0] = __byte_perm(w01, w23, 0x6420);  // low byte of each lane sum
+  } else {
+    const float c = -(98304.0f + static_cast<float>(n));
+    const float2 d01 = add_f32x2(lane_float(w01, 0x7610), lane_float(w01, 0x7632), c, c);
+    const float2 d23 = add_f32x2(lane_float(w23, 0x7610), lane_float(w23, 0x7632), c, c);
+    r[0] = __float_as_uint(d01.x);
+    r[1] = __float_as_uint(d01.y);
+    r[2] = __float_as_uint(d23.x);
+    r[3] = __float_as_uint(d23.y);
+  }
+}
+
+// ... and from uint32 byte sums T_e (> 256 peers): the kGroups flush below
+// computes the same integers (sum over groups of t - 128 * group size).
+template <int K>
+__device__ __forceinline__ void t32_to_lanes(const uint4& t, uint32_t n, uint32_t* r) {
+  if constexpr (K == kU8) {
+    r[0] = (t.x & 0xFFu) | ((t.y & 0xFFu) << 8) | ((t.z & 0xFFu) << 16) | (t.w << 24);
+  } else {
+    const int32_t b = 128 * static_cast<int32_t>(n);
+    r[0] = __float_as_uint(__int2float_rn(static_cast<int32_t>(t.x) - b) * kDyadicScale);
+    r[1] = __float_as_uint(__int2float_rn(static_cast<int32_t>(t.y) - b) * kDyadicScale);
+    r[2] = __float_as_uint(__int2float_rn(static_cast<int32_t>(t.z) - b) * kDyadicScale);
+    r[3] = __float_as_uint(__int2float_rn(static_cast<int32_t>(t.w) - b) * kDyadicScale);
+  }
+}
+
 // Emulated-peer contribution of the U vectors of one thread-tile, as lanes
 // r[] ready for fold_vec:
 //   float kinds  r[4i + e] = float bits of (sum over peers of byte e of
@@ -332,12 +405,41 @@ __device__ __forceinline__ void ah_to_lanes(uint32_t a, uint32_t h, uint32_t n, 
 //   u8           r[4i]     = the four byte sums of word i, mod 256, packed
 //   word kinds   r[i]      = wrapping sum of word i
 // ctr[] holds the hoisted c1 values; nkeys >= 1 (launchers route 0 peers
-// elsewhere) and, for kSeed2, even.
+// elsewhere) and, for kSeed2, even.  Cached modes read the sums of words
+// j0 + u * kThreads * W + w from `cache` instead (ctr, skeys unused).
 template <int K, int U, int kMode>
 __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skeys, uint32_t nkeys,
-                                          uint32_t one, uint32_t* r) {
+                                          uint32_t one, uint32_t* r, const void* cache = nullptr,
+                                          uint64_t j0 = 0) {
   using T = VT<K>;
   constexpr int NW = U * T::WPV;
+  if constexpr (cached(kMode)) {
+    constexpr int W = T::WPV;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t jv = j0 + static_cast<uint64_t>(u) * kThreads * W;
+      if constexpr (T::kWords) {  // four words = four elements: one 16-byte entry
+        const uint4 c = ld_stream(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(cache) + jv));
+        r[u * 4 + 0] = c.x;
+        r[u * 4 + 1] = c.y;
+        r[u * 4 + 2] = c.z;
+        r[u * 4 + 3] = c.w;
+      } else if constexpr (kMode == kCache16) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const uint2 c = ld_stream64(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(cache) + 4 * (jv + w)));
+          t16_to_lanes<K>(c.x, c.y, nkeys, r + 4 * (u * W + w));
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const uint4 c = ld_stream(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(cache) + 4 * (jv + w)));
+          t32_to_lanes<K>(c, nkeys, r + 4 * (u * W + w));
+        }
+      }
+    }
+    return;
+  }
   constexpr bool kMulti = kMode == kGroups;
   constexpr uint32_t kShift = key_shift(kMode);
   constexpr uint32_t kSeed = kMode == kSeed1 ? 1 : 2;  // peers folded in before the pair loop
@@ -491,12 +593,12 @@ template <int K, int DT, int U, int kMode>
 __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     const uint4* __restrict__ src, uint4* dst, uint64_t nvec, uint64_t word_base,
     const uint32_t* __restrict__ keys, uint32_t nkeys, int64_t* stamp, const void* tail_src,
-    void* tail_dst, uint32_t ntail, uint64_t tail_e0, uint32_t one) {
+    void* tail_dst, uint32_t ntail, uint64_t tail_e0, uint32_t one, const void* __restrict__ cache) {
   using T = VT<K>;
   constexpr int W = T::WPV, NW = U * W;
   extern __shared__ uint2 skeys[];
   if (stamp && blockIdx.x == 0 && threadIdx.x == 0) *stamp = globaltimer_ns();
-  load_keys(skeys, keys, nkeys, key_shift(kMode));
+  if constexpr (!cached(kMode)) load_keys(skeys, keys, nkeys, key_shift(kMode));
 
   const uint64_t tile = static_cast<uint64_t>(kThreads) * U;
   for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * tile; base < nvec;
@@ -509,11 +611,13 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
       if (v < nvec) x[u] = ld_stream(src + v);
     }
+    const uint64_t j0 = word_base + (base + threadIdx.x) * W;
     uint32_t ctr[NW];
-    tile_ctrs<W, U>(word_base + (base + threadIdx.x) * W, ctr);
-    // 2. the emulated peers' sums (registers only), 3. fold + stream out
+    if constexpr (!cached(kMode)) tile_ctrs<W, U>(j0, ctr);
+    // 2. the emulated peers' sums (registers only; or the cached sums),
+    // 3. fold + stream out
     uint32_t r[T::kWords ? NW : NW * 4];
-    peer_sums<K, U, kMode>(ctr, skeys, nkeys, one, r);
+    peer_sums<K, U, kMode>(ctr, skeys, nkeys, one, r, cache, j0);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
@@ -522,7 +626,11 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
   }
   // ragged tail (< one vector): the last block's first threads
   if (ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < ntail) {
-    elem_reduce<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, skeys + key_shift(kMode), nkeys);
+    if constexpr (cached(kMode)) {
+      elem_fold_cached<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, cache, kMode == kCache32, nkeys);
+    } else {
+      elem_reduce<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, skeys + key_shift(kMode), nkeys);
+    }
   }
 }
 
@@ -586,6 +694,98 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_split(
   }
   if (ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < ntail) {
     elem_reduce<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, skeys, nkeys);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// synthesis cache
+// ---------------------------------------------------------------------------
+// The emulated peers' contribution to element e depends only on (seed,
+// rank, e), never on the call (payload.cuh).  A communicator that sees the
+// same element range again -- a training loop all-reduces the same buckets
+// every step -- folds it from a per-element cache of the peers' sums instead
+// of synthesising W-k payloads again: at >= 16 emulated peers synthesis is
+// issue-bound (8 issue slots per peer-word), the cached fold is a 3-stream
+// HBM pass (read x, read the entry, write y).  This kernel writes the
+// entries of payload words [word_begin, word_end) with the hot kernel's own
+// arithmetic (A = sum of words, H = sum of odd bytes, even lanes = A - H<<8),
+// so a cached fold is bit-identical to a synthesised one.
+//   kEntry 0: uint16 lane sums t0..t3 of each word, packed (t0|t1<<16, t2|t3<<16)
+//          1: uint32 byte sums (> 256 peers: 256-peer groups, summed exactly)
+//          2: uint32 wrapping word sums (32-bit integer kinds; word = element)
+template <int U, int kEntry>
+__global__ void __launch_bounds__(kThreads) synth_cache_fill(uint64_t word_begin, uint64_t word_end,
+                                                             const uint32_t* __restrict__ keys, uint32_t nkeys,
+                                                             void* cache, uint32_t one) {
+  constexpr int W = 4, NW = U * W;
+  extern __shared__ uint2 skeys[];
+  load_keys(skeys, keys, nkeys);
+  const uint64_t j0 = word_begin + (static_cast<uint64_t>(blockIdx.x) * kThreads * U + threadIdx.x) * W;
+  uint32_t ctr[NW];
+  tile_ctrs<W, U>(j0, ctr);
+  auto word_of = [&](int i) { return j0 + static_cast<uint64_t>(i / W) * kThreads * W + (i % W); };
+  if constexpr (kEntry == 2) {
+    uint32_t sum[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) sum[i] = 0;
+#pragma unroll 2
+    for (uint32_t q = 0; q < nkeys; ++q) {
+      const uint2 key = skeys[q];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) sum[i] = mad_add(payload_mix(key.x, key.y, ctr[i]), one, sum[i]);
+    }
+    auto* out = static_cast<uint32_t*>(cache);
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      if (word_of(i) < word_end) out[word_of(i)] = sum[i];
+    }
+  } else {
+    constexpr bool kWide = kEntry == 1;
+    uint32_t tw[kWide ? NW * 4 : NW * 2];
+    if constexpr (kWide) {
+#pragma unroll
+      for (int i = 0; i < NW * 4; ++i) tw[i] = 0;
+    }
+    const uint32_t groups = kWide ? (nkeys + 255) / 256 : 1;
+    for (uint32_t g = 0; g < groups; ++g) {
+      const uint32_t q0 = g * 256, q1 = kWide ? min(nkeys, q0 + 256) : nkeys;
+      uint32_t a[NW], h[NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) a[i] = h[i] = 0;
+#pragma unroll 2
+      for (uint32_t q = q0; q < q1; ++q) {
+        const uint2 key = skeys[q];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          const uint32_t w = payload_mix(key.x, key.y, ctr[i]);
+          a[i] = mad_add(w, one, a[i]);
+          h[i] = mad_add(__byte_perm(w, 0u, 0x4341), one, h[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        const uint32_t even = even_lanes(a[i], h[i]);
+        if constexpr (kWide) {
+          uint32_t t[4];
+          decode_byte_sums(a[i], h[i], t);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) tw[4 * i + e] += t[e];
+        } else {
+          tw[2 * i] = __byte_perm(even, h[i], 0x5410);      // t0 | t1 << 16
+          tw[2 * i + 1] = __byte_perm(even, h[i], 0x7632);  // t2 | t3 << 16
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const uint64_t j = word_of(i);
+      if (j >= word_end) continue;
+      if constexpr (kWide) {
+        reinterpret_cast<uint4*>(cache)[j] = make_uint4(tw[4 * i], tw[4 * i + 1], tw[4 * i + 2], tw[4 * i + 3]);
+      } else {
+        reinterpret_cast<uint2*>(cache)[j] = make_uint2(tw[2 * i], tw[2 * i + 1]);
+      }
+    }
   }
 }
 
@@ -672,7 +872,7 @@ __device__ __forceinline__ uint4 add_real(const uint4& a, const uint4& b) {
 }
 
 // ragged elements after the last full vector: same fold, one element
-template <int DT>
+template <int DT, int kMode>
 __device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* skeys) {
   using S = typename std::conditional<
       DT == cemuInt8 || DT == cemuUint8, uint8_t,
@@ -693,7 +893,11 @@ __device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* ske
     }
   }
   S out;
-  elem_reduce<DT>(&acc, &out, 0, a.tail_e0 + i, skeys, a.nkeys);
+  if constexpr (cached(kMode)) {
+    elem_fold_cached<DT>(&acc, &out, 0, a.tail_e0 + i, a.cache, kMode == kCache32, a.nkeys);
+  } else {
+    elem_reduce<DT>(&acc, &out, 0, a.tail_e0 + i, skeys, a.nkeys);
+  }
   for (int g = 0; g < a.ndst; ++g) reinterpret_cast<S*>(a.dst[g] + a.v_end)[i] = out;
 }
 
@@ -713,7 +917,11 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
     st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(epoch, a.sig));
   }
   if (threadIdx.x == 0) abort_s = 0;
-  load_keys(skeys, a.keys, a.nkeys, key_shift(kMode));
+  if constexpr (!cached(kMode)) {
+    load_keys(skeys, a.keys, a.nkeys, key_shift(kMode));
+  } else {
+    __syncthreads();  // abort_s initialised before any thread may set it
+  }
   if (a.barriers && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
     const int w = wait_flag(a.flags + threadIdx.x, epoch, a.sig, true, t0, a.timeout_ns);
     if (w) {
@@ -742,10 +950,11 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
         }
       }
     }
+    const uint64_t j0 = a.word_base + (base + threadIdx.x) * W;
     uint32_t ctr[NW];
-    tile_ctrs<W, U>(a.word_base + (base + threadIdx.x) * W, ctr);
+    if constexpr (!cached(kMode)) tile_ctrs<W, U>(j0, ctr);
     uint32_t r[T::kWords ? NW : NW * 4];
-    peer_sums<K, U, kMode>(ctr, skeys, a.nkeys, 1u, r);
+    peer_sums<K, U, kMode>(ctr, skeys, a.nkeys, 1u, r, a.cache, j0);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
@@ -763,7 +972,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
     }
   }
   if (a.ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < a.ntail) {
-    fused_tail_elem<DT>(a, threadIdx.x, skeys + key_shift(kMode));
+    fused_tail_elem<DT, kMode>(a, threadIdx.x, skeys + key_shift(kMode));
   }
 
   if (!a.barriers) return;
@@ -1190,7 +1399,31 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
   kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(
       static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, keys, nkeys,
       stamp, static_cast<const uint8_t*>(src) + nvec * T::EPV * es,
-      static_cast<uint8_t*>(dst) + nvec * T::EPV * es, ntail, elem_base + nvec * T::EPV, 1u);
+      static_cast<uint8_t*>(dst) + nvec * T::EPV * es, ntail, elem_base + nvec * T::EPV, 1u, nullptr);
+  return cudaGetLastError();
+}
+
+// The fold of a cached call: the hot kernel in a cached mode, one tile of
+// U = 2 vectors per thread per block (the memory-bound shape).
+template <int K, int DT>
+cudaError_t run_vec_cached(const void* src, void* dst, uint64_t count, uint64_t elem_base, uint32_t nkeys,
+                           int64_t* stamp, cudaStream_t s, CacheRef cache) {
+  using T = VT<K>;
+  constexpr int U = 2;
+  const uint64_t nvec = count / T::EPV;
+  const uint32_t ntail = static_cast<uint32_t>(count - nvec * T::EPV);
+  const size_t es = T::kWords ? 4 : (K == kF32 ? 4 : (K == kU8 ? 1 : 2));
+  const uint64_t word_base = T::kWords ? elem_base : elem_base / 4;
+  const uint64_t tiles = (nvec + static_cast<uint64_t>(kThreads) * U - 1) / (static_cast<uint64_t>(kThreads) * U);
+  const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, 0x7FFFFFFFull));
+  auto kern = synth_reduce_vec<K, DT, U, kCache32>;
+  if constexpr (!T::kWords) {
+    if (cache.kind == kCacheLanes16) kern = synth_reduce_vec<K, DT, U, kCache16>;
+  }
+  kern<<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
+      static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, nullptr, nkeys, stamp,
+      static_cast<const uint8_t*>(src) + nvec * T::EPV * es, static_cast<uint8_t*>(dst) + nvec * T::EPV * es, ntail,
+      elem_base + nvec * T::EPV, 1u, cache.ptr);
   return cudaGetLastError();
 }
 
@@ -1273,9 +1506,26 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t count,
                                 uint64_t elem_base, const uint32_t* d_keys, uint32_t nkeys,
-                                int64_t* stamp, cudaStream_t s, int* launches) {
+                                int64_t* stamp, cudaStream_t s, int* launches, CacheRef cache) {
   if (nkeys > kMaxKeys) return cudaErrorInvalidValue;
   if (count == 0) return cudaSuccess;
+  if (cache.ptr) {
+    // callers route only the vector kinds, aligned, word-aligned element offsets
+    if (!aligned16(src) || !aligned16(dst) || elem_base % 4 != 0 || nkeys == 0) return cudaErrorInvalidValue;
+    const bool words = dtype == cemuInt32 || dtype == cemuUint32;
+    if (words && cache.kind != kCacheWide32) return cudaErrorInvalidValue;
+    ++*launches;
+    switch (dtype) {
+      case cemuFloat32: return run_vec_cached<kF32, cemuFloat32>(src, dst, count, elem_base, nkeys, stamp, s, cache);
+      case cemuBfloat16: return run_vec_cached<kBF16, cemuBfloat16>(src, dst, count, elem_base, nkeys, stamp, s, cache);
+      case cemuFloat16: return run_vec_cached<kF16, cemuFloat16>(src, dst, count, elem_base, nkeys, stamp, s, cache);
+      case cemuUint8: return run_vec_cached<kU8, cemuUint8>(src, dst, count, elem_base, nkeys, stamp, s, cache);
+      case cemuInt8: return run_vec_cached<kU8, cemuInt8>(src, dst, count, elem_base, nkeys, stamp, s, cache);
+      case cemuInt32: return run_vec_cached<kI32, cemuInt32>(src, dst, count, elem_base, nkeys, stamp, s, cache);
+      case cemuUint32: return run_vec_cached<kI32, cemuUint32>(src, dst, count, elem_base, nkeys, stamp, s, cache);
+      default: --*launches; return cudaErrorInvalidValue;
+    }
+  }
   ++*launches;
   // vector path: 16-byte aligned pointers, payload words aligned to vectors,
   // at least one emulated peer (the vector kernels seed their sums from it)
@@ -1308,6 +1558,27 @@ cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t 
     case cemuFloat64: return run_scalar<cemuFloat64>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     default: --*launches; return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_synth_cache_fill(bool words, uint64_t elem_base, uint64_t count, const uint32_t* d_keys,
+                                    uint32_t nkeys, CacheRef cache, cudaStream_t s, int* launches) {
+  if (count == 0) return cudaSuccess;
+  if (!cache.ptr || nkeys == 0 || nkeys > kMaxKeys || (words && cache.kind != kCacheWide32)) {
+    return cudaErrorInvalidValue;
+  }
+  constexpr int U = 2;
+  const uint64_t wb = words ? elem_base : elem_base / 4;
+  const uint64_t we = words ? elem_base + count : (elem_base + count + 3) / 4;
+  const uint64_t per_block = static_cast<uint64_t>(kThreads) * U * 4;
+  const uint64_t grid = (we - wb + per_block - 1) / per_block;
+  if (grid > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  const size_t smem = static_cast<size_t>(nkeys) * 8;
+  auto kern = words ? synth_cache_fill<U, 2>
+                    : (cache.kind == kCacheLanes16 ? synth_cache_fill<U, 0> : synth_cache_fill<U, 1>);
+  if (const cudaError_t e = fit_smem(kern, smem)) return e;
+  ++*launches;
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(wb, we, d_keys, nkeys, cache.ptr, 1u);
+  return cudaGetLastError();
 }
 
 namespace {
@@ -1414,13 +1685,24 @@ cudaError_t fused_ku(const FusedArgs& a, cudaStream_t s) {
   auto kern = mode == kGroups ? fused_allreduce_vec<K, DT, KMAX, U, kGroups>
               : mode == kSeed1 ? fused_allreduce_vec<K, DT, KMAX, U, kSeed1>
                                : fused_allreduce_vec<K, DT, KMAX, U, kSeed2>;
+  size_t smem = (static_cast<size_t>(a.nkeys) + 1) * 8;
+  if (a.cache && a.cache_kind == kCacheWide32) {
+    kern = fused_allreduce_vec<K, DT, KMAX, U, kCache32>;
+    smem = 0;
+  }
+  if constexpr (!VT<K>::kWords) {
+    if (a.cache && a.cache_kind == kCacheLanes16) {
+      kern = fused_allreduce_vec<K, DT, KMAX, U, kCache16>;
+      smem = 0;
+    }
+  }
   const uint64_t nvec = a.v_end - a.v_begin;
   const uint64_t tiles = (nvec + static_cast<uint64_t>(U) * kThreads - 1) / (static_cast<uint64_t>(U) * kThreads);
   // persistent: NVLink-bound, and every CTA passes the start barrier (one
   // tile per block measured 1.64 -> 2.10 ms for the 1 GiB k=2 allreduce)
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count()) * bps));
-  if (const cudaError_t e = fit_smem(kern, (static_cast<size_t>(a.nkeys) + 1) * 8)) return e;
-  kern<<<static_cast<unsigned>(grid), kThreads, (static_cast<size_t>(a.nkeys) + 1) * 8, s>>>(a);
+  if (const cudaError_t e = fit_smem(kern, smem)) return e;
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 

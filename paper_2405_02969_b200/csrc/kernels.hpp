@@ -46,12 +46,35 @@ cudaError_t launch_chain_join(int64_t* chain, const int64_t* other, cudaStream_t
 // CEMU_QUEUE_GAP_US (default 10 us; 0 disables the back-to-back chaining)
 int64_t queue_gap_ns();
 
+// Synthesis cache (kernels.cu, "synthesis cache"): the emulated peers'
+// contribution depends only on (seed, rank, element index), never on the
+// call, so a communicator may keep it per element and fold repeat calls
+// from it.  Entries, indexed by absolute payload element e:
+//   kCacheLanes16  byte kinds (u8/i8/fp16/bf16/fp32), <= 256 peers: uint16
+//                  t_e = sum over peers of byte_r(e)
+//   kCacheWide32   byte kinds, > 256 peers: uint32 t_e;  32-bit integer
+//                  kinds: uint32 wrapping sum of word_r(e)
+enum CacheKind { kNoCache = 0, kCacheLanes16 = 1, kCacheWide32 = 2 };
+struct CacheRef {
+  void* ptr = nullptr;  // entry 0 = payload element 0
+  int kind = kNoCache;
+};
+// Cache entries of one element range need this many bytes per element.
+inline size_t cache_entry_bytes(int kind) { return kind == kCacheLanes16 ? 2 : 4; }
+
 // dst[i] = src[i] (+) sum over `nkeys` emulated peers of their payload at
 // element elem_base + i.  src may equal dst.  Returns the number of kernel
-// launches issued through *launches.
+// launches issued through *launches.  With a cache (whose entries cover
+// [elem_base, elem_base + count)) the sums are read instead of synthesised:
+// same bits.  Cached calls need 16-byte aligned src/dst and elem_base % 4 == 0.
 cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t count,
                                 uint64_t elem_base, const uint32_t* d_keys, uint32_t nkeys,
-                                int64_t* stamp, cudaStream_t stream, int* launches);
+                                int64_t* stamp, cudaStream_t stream, int* launches, CacheRef cache = {});
+// Writes the cache entries of elements [elem_base, elem_base + count)
+// (byte kinds: whole payload words, i.e. rounded out to multiples of 4).
+// `words`: the 32-bit integer kinds' entries.
+cudaError_t launch_synth_cache_fill(bool words, uint64_t elem_base, uint64_t count, const uint32_t* d_keys,
+                                    uint32_t nkeys, CacheRef cache, cudaStream_t stream, int* launches);
 
 // Writes whole per-rank blocks: for b in [0, nblocks) block dst_index[b]
 // (elements [dst_index[b]*block_elems, +block_elems) of dst) is filled with
@@ -90,6 +113,9 @@ struct FusedArgs {
   // 0: fold only -- no start / done barrier, epoch untouched (one chunk of
   // the copy-engine pipeline, whose barriers are launch_peer_barrier's)
   int barriers = 1;
+  // synthesis cache covering this GPU's slice (and tail), or none
+  const void* cache = nullptr;
+  int cache_kind = kNoCache;
 };
 // Returns cudaErrorNotSupported for datatypes without a vector path.
 cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t stream, int* launches);
