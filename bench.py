@@ -313,35 +313,70 @@ def delay_error_block(torch, pb, device):
                           "link.gamma_us_per_byte = 0.0001\n")
     comm = pb.Communicator(cfg, 0, device)
     x = torch.zeros(16 << 20, device=device)
-    errs, meas = [], []
-    for _ in range(4):
-        comm.all_reduce(x, x)
+
+    def timed_call(c, buf):
+        """(record, event-timed stream occupancy in us): the stream is kept
+        busy while the host enqueues, so the events bracket device work only."""
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(device)
-        rec = comm.call_record()
+        torch.cuda._sleep(2_000_000)
+        e0.record()
+        c.all_reduce(buf, buf)
+        e1.record()
+        torch.cuda.synchronize(device)
+        return c.call_record(), e0.elapsed_time(e1) * 1e3
+
+    errs, meas, evs, lates = [], [], [], []
+    for _ in range(4):
+        rec, ev = timed_call(comm, x)
         m = (rec["t_end_ns"] - rec["t_start_ns"]) / 1e3
         meas.append(round(m, 3))
+        evs.append(round(ev, 3))
+        lates.append(round(rec["overshoot_ns"] / 1e3, 3))
         errs.append(abs(m - rec["model_latency_us"]))
     out["config1_alpha_beta_64MiB_world8"] = {
-        "model_us": rec["model_latency_us"], "measured_us": meas,
+        "model_us": rec["model_latency_us"], "measured_us": meas, "event_timed_us": evs, "overshoot_us": lates,
         "max_err_us": round(max(errs), 3), "max_err_pct": round(100 * max(errs) / rec["model_latency_us"], 5),
+        "max_event_err_us": round(max(abs(e - rec["model_latency_us"]) for e in evs), 3),
         "floors_us": rec["floors_us"].tolist()}
     comm.close()
+    # a model shorter than the emulator's own work: world 64, bf16, 1 GiB,
+    # NVLink-class ring under the 2x bandwidth what-if (alpha 2 us, 1540 GB/s)
+    comm = pb.Communicator("world_size = 64\nreal_ranks = 0\nbucket_bytes = 1\ndelay.kind = alpha_beta\n"
+                           "link.alpha_us = 2\nlink.beta_us_per_byte = 0.000000649\n", 0, device)
+    xb = torch.zeros(1 << 29, dtype=torch.bfloat16, device=device)
+    over = {}
+    for tag, cap in (("synthesised", 0), ("synthesis_cache_warm", 4 << 30)):
+        comm.set_synth_cache(cap, 16)
+        timed_call(comm, xb)  # (fills the cache when on)
+        rec, ev = timed_call(comm, xb)
+        over[tag] = {"model_us": rec["model_latency_us"],
+                     "measured_us": round((rec["t_end_ns"] - rec["t_start_ns"]) / 1e3, 3),
+                     "event_timed_us": round(ev, 3), "overshoot_us": round(rec["overshoot_ns"] / 1e3, 3),
+                     "max_step_late_us": round(rec["late_ns"] / 1e3, 3)}
+    comm.close()
+    del xb
+    out["overshoot_world64_bf16_1GiB"] = over
     probes = {}
     for inject in (100, 1000, 5000):
         comm = pb.Communicator("world_size = 2\nreal_ranks = 0\nbucket_bytes = 1\n"
                                f"delay.inject_us = {inject}\n", 0, device)
         y = torch.zeros(1024, device=device)
-        es = []
+        es, ee = [], []
         for _ in range(10):
-            comm.all_reduce(y, y)
-            torch.cuda.synchronize(device)
-            rec = comm.call_record()
+            rec, ev = timed_call(comm, y)
             es.append((rec["t_end_ns"] - rec["t_start_ns"]) / 1e3 - inject)
+            ee.append(ev - inject)
         probes[f"inject_{inject}us_world2_4KiB"] = {"mean_err_us": round(statistics.mean(es), 3),
-                                                    "max_abs_err_us": round(max(abs(e) for e in es), 3)}
+                                                    "max_abs_err_us": round(max(abs(e) for e in es), 3),
+                                                    "event_timed_mean_err_us": round(statistics.mean(ee), 3)}
         comm.close()
     out["whatif_inject_probes"] = probes
     out["tolerance"] = "max(1% of model, 2 us)"
+    out["note"] = ("measured = device %globaltimer from the call's first kernel to the last release; "
+                   "event_timed = CUDA events around the call on its stream (device work only); "
+                   "overshoot = t_end - (start + modelled latency), > 0 when the emulator's own work "
+                   "outlasted the model; max_step_late = max over steps of release - (start + floor)")
     model = out["config1_alpha_beta_64MiB_world8"]["model_us"]
     out["pass"] = max(errs) <= max(0.01 * model, 2.0) and \
         all(p["max_abs_err_us"] <= max(0.01 * int(k.split("_")[1][:-2]), 2.0) for k, p in probes.items())

@@ -208,6 +208,14 @@ typedef struct {
   int64_t t_start_ns;    /* device %globaltimer at the call's first kernel */
   int64_t t_end_ns;      /* device %globaltimer when the last step released */
   int64_t device_latency_us; /* max_j floor_j as evaluated on the device */
+  int64_t t_origin_ns;   /* the schedule's origin: t_start_ns, or the previous
+                            call's t_end_ns when queue chaining applied */
+  int64_t late_ns;       /* max_j (release_j - (t_origin + floor_j)): > 0 when
+                            the emulator's own work (synthesis, NVLink legs)
+                            outlasted some step's floor -- that step's release
+                            was late even if the call ended on time */
+  int64_t overshoot_ns;  /* max(0, t_end - (t_origin + max_j floor_j)): how
+                            much longer than modelled the call itself took */
 } cemuCallRecord;
 
 /* Delay-model plugin: replaces DelayModelFn / make_delay_model
@@ -226,6 +234,14 @@ typedef struct {
 typedef int (*cemuDelayModelFn)(int coll, uint32_t worldSize, uint64_t bytes, uint32_t k,
                                 double* offsetsUs, void* user);
 cemuResult_t cemuCommSetDelayModel(cemuComm_t comm, cemuDelayModelFn fn, void* user);
+/* Queue chaining (off by default; CEMU_QUEUE_GAP_US sets the default): a
+ * delayed call whose first kernel starts within gapUs after the previous
+ * delayed call on the same stream ended was queued behind it, and its
+ * schedule starts at that end -- an in-order channel starts the next
+ * collective when the previous one leaves the wire, without the emulator's
+ * own kernel-dispatch gap.  The record keeps both instants (t_start_ns,
+ * t_origin_ns).  cemuRunTrainingLoop uses 10 us for its own loop. */
+cemuResult_t cemuCommSetQueueChaining(cemuComm_t comm, int64_t gapUs);
 
 cemuResult_t cemuCommLastCallId(cemuComm_t comm, uint64_t* callId);
 /* Copies the record (and up to `cap` floors / release times / offsets) of a

@@ -66,7 +66,8 @@ class CallRecord(C.Structure):
         ("call_id", C.c_uint64), ("coll", C.c_int32), ("delay_active", C.c_int32),
         ("steps", C.c_uint32), ("world", C.c_uint32), ("model_bytes", C.c_uint64),
         ("model_latency_us", C.c_int64), ("t_start_ns", C.c_int64), ("t_end_ns", C.c_int64),
-        ("device_latency_us", C.c_int64),
+        ("device_latency_us", C.c_int64), ("t_origin_ns", C.c_int64), ("late_ns", C.c_int64),
+        ("overshoot_ns", C.c_int64),
     ]
 
 
@@ -132,6 +133,7 @@ def _load():
         "cemuPayloadKey": (u32, [u64, u32]),
         "cemuPayloadWord": (u32, [u32, u64]),
         "cemuCommSetDelayModel": (i32, [vp, DELAY_MODEL_FN, vp]),
+        "cemuCommSetQueueChaining": (i32, [vp, i64]),
         "cemuConfigTopology": (u32, [vp, C.POINTER(TopoNode), C.POINTER(TopoEdge), sz]),
         "cemuRingSuccessor": (u32, [u32, u32]),
         "cemuRingPredecessor": (u32, [u32, u32]),

@@ -237,6 +237,12 @@ class Communicator:
         self._delay_cb = _capi.DELAY_MODEL_FN(cb)  # kept alive with the communicator
         check(lib.cemuCommSetDelayModel(self._h, self._delay_cb, None), self._h)
 
+    def set_queue_chaining(self, gap_us: int) -> None:
+        """cemuCommSetQueueChaining: a delayed call queued within gap_us
+        behind the previous delayed call on its stream starts its schedule at
+        that call's end (0 = off, the default)."""
+        check(lib.cemuCommSetQueueChaining(self._h, int(gap_us)), self._h)
+
     # -- wire mode (interop with a reference cemu-emulator) -------------------
     def attach_emulator(self, plan: list, timeout_ms: int = 10000) -> None:
         """cemuCommAttachEmulator: dial the config's emulator endpoint and
@@ -359,6 +365,7 @@ class Communicator:
             "steps": rec.steps, "world": rec.world, "model_bytes": rec.model_bytes,
             "model_latency_us": rec.model_latency_us, "t_start_ns": rec.t_start_ns,
             "t_end_ns": rec.t_end_ns, "device_latency_us": rec.device_latency_us,
+            "t_origin_ns": rec.t_origin_ns, "late_ns": rec.late_ns, "overshoot_ns": rec.overshoot_ns,
             "floors_us": floors[:k].copy(), "release_ns": release[:k].copy(),
             "offsets_us": offsets[:k].copy(),
         }

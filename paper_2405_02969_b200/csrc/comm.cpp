@@ -467,6 +467,7 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
   c->delay.intra_beta_us_per_byte = cfg.intra_beta_us_per_byte;
   c->delay_active = cfg.delay_kind != DelayKind::kNone || cfg.delay_inject_us != 0.0;
   c->config_delay_active = c->delay_active;
+  c->queue_gap_ns = queue_gap_ns();
   {
     const char* mb = std::getenv("CEMU_SYNTH_CACHE_MB");
     c->cache_cap = (mb ? std::strtoull(mb, nullptr, 10) : 4096ull) << 20;
@@ -1043,6 +1044,12 @@ cemuResult_t run_or_defer(cemuComm* c, cudaStream_t s, F&& plan) {
   return cemuSuccess;
 }
 
+int64_t exchange_queue_gap_ns(cemuComm_t c, int64_t gap_ns) {
+  const int64_t old = c->queue_gap_ns;
+  c->queue_gap_ns = gap_ns;
+  return old;
+}
+
 const int64_t* stream_release_end(cemuComm_t c, cudaStream_t s) {
   return (c && c->last_slot && c->last_stream == s) ? c->last_slot + 1 : nullptr;
 }
@@ -1329,6 +1336,9 @@ cemuResult_t cemuCommCallRecord(cemuComm_t c, uint64_t id, cemuCallRecord* rec, 
   rec->t_start_ns = h[0];
   rec->t_end_ns = h[1];
   rec->device_latency_us = h[2];
+  rec->t_origin_ns = h[4];
+  rec->late_ns = h[5];
+  rec->overshoot_ns = h[6];
   const size_t n = std::min<size_t>(cap, m.k);
   if (floors) std::memcpy(floors, h.data() + kSlotHeader, n * 8);
   if (release) std::memcpy(release, h.data() + kSlotHeader + c->kmax, n * 8);
@@ -1503,6 +1513,12 @@ cemuResult_t cemuCommModelLatencyUs(cemuComm_t c, int coll, uint64_t bytes, int6
     return cemuSuccess;
   }
   *out = c->delay_active ? call_latency_us(c->delay, coll, c->W, bytes, k) : 0;
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommSetQueueChaining(cemuComm_t c, int64_t gap_us) {
+  if (!c || gap_us < 0) return fail(cemuInvalidArgument, "cemuCommSetQueueChaining: bad argument");
+  c->queue_gap_ns = gap_us * 1000;
   return cemuSuccess;
 }
 

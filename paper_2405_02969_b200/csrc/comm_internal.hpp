@@ -114,6 +114,7 @@ struct cemuComm {
   // behind it on the same stream starts when it ended (queue_gap_ns())
   int64_t* last_slot = nullptr;
   cudaStream_t last_stream = nullptr;
+  int64_t queue_gap_ns = 0;  // cemuCommSetQueueChaining (0: every call's schedule starts at its own start)
   ncclComm_t inner = nullptr;
   uint64_t launches = 0;
   // fused multi-GPU path (k > 1): IPC-mapped signal areas and symmetric buffers
@@ -327,9 +328,27 @@ struct Call {
     d.kmax = c->kmax;
     d.self_stamp = stamped ? 0 : 1;
     d.preloaded = 0;
+    d.prev_end = (c->last_slot && c->last_stream == s) ? c->last_slot + 1 : nullptr;
+    d.queue_gap_ns = c->queue_gap_ns;
+    if (!plugin.empty() && plugin.size() <= static_cast<size_t>(kInlineOffsets)) {
+      // the offsets ride in the spin kernel's parameter block: nothing on
+      // the host to recycle, no host wait, graph-capture safe
+      auto offs = std::make_unique<InlineOffsets>();
+      std::memcpy(offs->us, plugin.data(), plugin.size() * sizeof(double));
+      int l = 0;
+      const cudaError_t e = launch_delay_spin(d, slot, s, &l, offs.get());
+      c->launches += l;
+      c->last_slot = slot;
+      c->last_stream = s;
+      return e;
+    }
     if (!plugin.empty()) {
-      // stage the plugin's offsets into the slot's offsets region, in stream
-      // order; the pinned staging of slot i is reused 64 calls later
+      // larger worlds: stage the plugin's offsets into the slot's offsets
+      // region, in stream order; the pinned staging of slot i is reused 64
+      // calls later (its previous copy has long completed in practice)
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      if (const cudaError_t e = cudaStreamIsCapturing(s, &cap)) return e;
+      if (cap != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;  // > 2048 steps
       cudaEvent_t& ev = c->offsets_copied[i];
       if (!ev) {
         if (const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) return e;
@@ -346,8 +365,6 @@ struct Call {
       if (const cudaError_t e = cudaEventRecord(ev, s)) return e;
       d.preloaded = 1;
     }
-    d.prev_end = (c->last_slot && c->last_stream == s) ? c->last_slot + 1 : nullptr;
-    d.queue_gap_ns = queue_gap_ns();
     int l = 0;
     const cudaError_t e = launch_delay_spin(d, slot, s, &l);
     c->launches += l;

@@ -166,6 +166,16 @@ std::vector<IterTrace> run_training_loop(cemuComm_t comm, const ModelSpec& m, ui
     resync = false;
   };
   CK(cudaEventRecord(ev[0], compute));
+  // The loop enqueues its buckets back to back on one in-order comm stream,
+  // so it models that channel: a bucket queued behind the previous one
+  // starts on the wire when that one leaves it (cemuCommSetQueueChaining),
+  // unless the caller chose a gap of its own.
+  struct GapGuard {
+    cemuComm_t c;
+    int64_t prev;
+    ~GapGuard() { exchange_queue_gap_ns(c, prev); }
+  } gap_guard{comm, exchange_queue_gap_ns(comm, 0)};
+  exchange_queue_gap_ns(comm, gap_guard.prev > 0 ? gap_guard.prev : 10'000);
   const uint32_t L = static_cast<uint32_t>(m.layers.size());
   for (uint32_t it = 0; it < m.iterations; ++it) {
     cudaEvent_t* E = ev.data() + 1 + per_it * it;

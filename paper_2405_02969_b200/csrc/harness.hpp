@@ -71,5 +71,7 @@ double predicted_iteration_us(const ModelSpec& m, uint64_t bucket_bytes,
 // Device word holding the end (%globaltimer ns) of the last delayed call
 // `comm` enqueued on `stream`, or null (delay off, or another stream).
 const int64_t* stream_release_end(cemuComm_t comm, cudaStream_t stream);
+// Sets the communicator's queue-chaining gap and returns the previous one.
+int64_t exchange_queue_gap_ns(cemuComm_t comm, int64_t gap_ns);
 
 }  // namespace cemu_b200

@@ -1255,26 +1255,32 @@ __global__ void chain_join_kernel(int64_t* chain, const int64_t* other) {
   if (o > *chain) *chain = o;
 }
 
-__global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int64_t* slot) {
+__device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* slot, const double* inline_offs) {
   int64_t* floors = slot + kSlotHeader;
   int64_t* release = floors + d.kmax;
   double* offs = reinterpret_cast<double*>(release + d.kmax);
   __shared__ int64_t t0_s;
   if (threadIdx.x == 0) {
-    int64_t t0 = d.self_stamp ? globaltimer_ns() : slot[0];
-    if (d.prev_end) {
+    // slot[0] keeps the call's real start (its first kernel's stamp); the
+    // schedule's origin slot[4] moves back to the previous call's end only
+    // when queue chaining is on (cemuCommSetQueueChaining) and this call was
+    // queued right behind it
+    const int64_t stamp = d.self_stamp ? globaltimer_ns() : slot[0];
+    int64_t t0 = stamp;
+    if (d.prev_end && d.queue_gap_ns > 0) {
       const int64_t pe = *d.prev_end;
       if (pe > 0 && t0 >= pe && t0 - pe <= d.queue_gap_ns) t0 = pe;
     }
     t0_s = t0;
-    slot[0] = t0;
+    slot[0] = stamp;
+    slot[4] = t0;
   }
   // Evaluate the model on the device: delay.cpp:23-47 offsets and
   // engine.cpp:41 llround floors, strided over the block.  A delay-model
   // plugin's offsets (DelayModelFn, delay.hpp:52-55) arrive preloaded.
   const double total = (!d.preloaded && d.model.kind == 1) ? model_total_us(d.model, d.coll, d.n, d.bytes) : 0.0;
   for (uint32_t j = threadIdx.x; j < d.k; j += blockDim.x) {
-    const double o = d.preloaded ? offs[j] : release_offset_us(d.model, total, j, d.k);
+    const double o = inline_offs ? inline_offs[j] : d.preloaded ? offs[j] : release_offset_us(d.model, total, j, d.k);
     offs[j] = o;
     floors[j] = llround(o);
   }
@@ -1286,8 +1292,14 @@ __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int
   slot[3] = d.k;
   // Head-of-line release (engine.cpp:58-70): step j leaves once its floor
   // has passed and step j-1 has left.
+  // A step released after its floor is late: the emulator's own work (the
+  // synthesis kernels before this one) outlasted that step's floor, or the
+  // spin overshot.  The largest lateness is recorded (slot[5]), and how far
+  // the whole call overran its modelled latency (slot[6]), so such a call
+  // is visible, never silently longer.
   const int64_t t0 = t0_s;
   int64_t t = globaltimer_ns();
+  int64_t late = 0;
   for (uint32_t j = 0; j < d.k; ++j) {
     const int64_t target = t0 + floors[j] * 1000;
     while (t < target) {
@@ -1295,8 +1307,24 @@ __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int
       t = globaltimer_ns();
     }
     release[j] = t;
+    late = max(late, t - target);
   }
-  slot[1] = globaltimer_ns();
+  slot[5] = late;
+  const int64_t end = globaltimer_ns();
+  slot[6] = max(int64_t{0}, end - (t0 + lat * 1000));  // the call itself ran long by this much
+  slot[1] = end;
+}
+
+__global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int64_t* slot) {
+  delay_spin_body(d, slot, nullptr);
+}
+
+// A plugin's offsets travel in the launch's own parameter block (<= 16 KB):
+// no host staging to recycle, and a captured graph keeps the captured call's
+// offsets.
+__global__ void __launch_bounds__(kThreads) delay_spin_inline_kernel(DelayLaunch d, int64_t* slot,
+                                                                     const __grid_constant__ InlineOffsets o) {
+  delay_spin_body(d, slot, o.us);
 }
 
 // ---------------------------------------------------------------------------
@@ -1829,14 +1857,20 @@ cudaError_t launch_chain_join(int64_t* chain, const int64_t* other, cudaStream_t
 int64_t queue_gap_ns() {
   static const int64_t gap = [] {
     const char* e = std::getenv("CEMU_QUEUE_GAP_US");
-    return e ? std::max<int64_t>(0, std::atoll(e)) * 1000 : int64_t{10'000};
+    return e ? std::max<int64_t>(0, std::atoll(e)) * 1000 : int64_t{0};
   }();
   return gap;
 }
 
-cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t s, int* launches) {
+cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t s, int* launches,
+                              const InlineOffsets* offs) {
   ++*launches;
-  delay_spin_kernel<<<1, kThreads, 0, s>>>(d, slot);
+  if (offs) {
+    if (d.k > static_cast<uint32_t>(kInlineOffsets)) return cudaErrorInvalidValue;
+    delay_spin_inline_kernel<<<1, kThreads, 0, s>>>(d, slot, *offs);
+  } else {
+    delay_spin_kernel<<<1, kThreads, 0, s>>>(d, slot);
+  }
   return cudaGetLastError();
 }
 

@@ -10,8 +10,10 @@
 namespace cemu_b200 {
 
 // Per-call record slot in device memory (int64 words):
-//   [0] t_start_ns  [1] t_end_ns  [2] device max floor (us)  [3] K
-//   [4..7] reserved
+//   [0] t_start_ns (the call's first kernel)  [1] t_end_ns  [2] device max
+//   floor (us)  [3] K  [4] schedule origin (= [0] unless queue-chained)
+//   [5] late_ns: max over steps of release - (origin + floor)
+//   [6] overshoot_ns: max(0, t_end - (origin + max floor))  [7] reserved
 //   [8 .. 8+kmax)            floors_us[j]
 //   [8+kmax .. 8+2kmax)      release_ns[j]   (%globaltimer at release)
 //   [8+2kmax .. 8+3kmax)     offsets_us[j]   (double bits)
@@ -43,7 +45,8 @@ struct DelayLaunch {
 // *chain = max(*chain, *other) in stream order (one 1-thread kernel).
 cudaError_t launch_chain_join(int64_t* chain, const int64_t* other, cudaStream_t stream, int* launches);
 
-// CEMU_QUEUE_GAP_US (default 10 us; 0 disables the back-to-back chaining)
+// CEMU_QUEUE_GAP_US: the communicators' default queue-chaining gap
+// (default 0 = off; cemuCommSetQueueChaining sets it per communicator)
 int64_t queue_gap_ns();
 
 // Synthesis cache (kernels.cu, "synthesis cache"): the emulated peers'
@@ -153,7 +156,13 @@ cudaError_t launch_stamp(int64_t* slot, cudaStream_t stream, int* launches);
 // chain: device int64 holding the previous spin's absolute deadline (or null)
 cudaError_t launch_spin_ns(int64_t ns, cudaStream_t stream, int* launches, int64_t* chain = nullptr,
                            bool resync = false);
+// A delay-model plugin's offsets passed by value in the launch (16 KB of
+// the 32 KB kernel-parameter space): up to kInlineOffsets steps.
+constexpr int kInlineOffsets = 2048;
+struct InlineOffsets {
+  double us[kInlineOffsets];
+};
 cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t stream,
-                              int* launches);
+                              int* launches, const InlineOffsets* offs = nullptr);
 
 }  // namespace cemu_b200

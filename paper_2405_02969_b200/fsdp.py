@@ -207,6 +207,10 @@ def whatif_table(world: int = 1024, iterations: int = 2, device: int = 0, units=
     for algo in ("ring", "tree", "hierarchical"):
         for scale in (1.0, 2.0):
             comm = Communicator(cost_config(world, algo, scale), 0, device)
+            # the trace issues every collective on one in-order comm stream:
+            # model that channel (a queued collective starts on the wire when
+            # the previous one leaves it; cemuCommSetQueueChaining)
+            comm.set_queue_chaining(10)
             lat_ag = [_latency(comm, 1, u["shard"] * 2) for u in plan]
             lat_rs = [_latency(comm, 2, u["shard"] * 2 * world) for u in plan]
             ideal = ideal_iteration_us(plan, lat_ag, lat_rs)

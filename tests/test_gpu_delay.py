@@ -99,6 +99,7 @@ def test_config1_alpha_beta_delay_within_tolerance(cuda):
     x = torch.randn(16 << 20, device="cuda")
     for _ in range(3):
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        torch.cuda._sleep(2_000_000)  # the stream is busy while the host enqueues: events time device work only
         e0.record()
         comm.all_reduce(x, x)
         e1.record()
@@ -107,7 +108,11 @@ def test_config1_alpha_beta_delay_within_tolerance(cuda):
         measured, model, err, tol = _delay_error(rec)
         assert model == 123453
         assert err <= tol, (measured, model)
-        assert e0.elapsed_time(e1) * 1e3 >= model  # the stream really waited
+        ev_us = e0.elapsed_time(e1) * 1e3
+        # event-timed stream occupancy: the stream really waited, and no more
+        # than the model plus the call's own kernel launches
+        assert model <= ev_us <= model + 50.0, (ev_us, model)
+        assert rec["overshoot_ns"] < 2000 and rec["t_origin_ns"] == rec["t_start_ns"]
     comm.close()
 
 
@@ -276,11 +281,14 @@ def test_plugin_failure_is_loud_and_none_restores_the_config(cuda):
 
 
 def test_back_to_back_calls_on_one_stream_chain_their_network_time(cuda):
-    """An in-order channel starts the next collective when the previous one
-    leaves the wire: a call enqueued behind another on the same stream starts
-    at the previous call's end, not after the kernel-dispatch gap.  The
-    per-call latency stays exactly the model's."""
+    """With queue chaining on (cemuCommSetQueueChaining; the training-loop
+    harness uses it for its own in-order comm stream): a call enqueued behind
+    another on the same stream starts its schedule at the previous call's
+    end, not after the kernel-dispatch gap.  The record keeps the real start
+    (t_start_ns) beside the schedule's origin (t_origin_ns); the latency from
+    the origin stays exactly the model's."""
     comm = pb.Communicator(delay_config(8, 2, fixed=200.0), 0, 0)
+    comm.set_queue_chaining(10)
     x = torch.zeros(1 << 20, device="cuda")
     for _ in range(6):
         comm.all_reduce(x, x)
@@ -288,15 +296,77 @@ def test_back_to_back_calls_on_one_stream_chain_their_network_time(cuda):
     last = comm.last_call_id
     recs = [comm.call_record(i) for i in range(last - 5, last + 1)]
     for a, b in zip(recs, recs[1:]):
-        assert b["t_start_ns"] == a["t_end_ns"]  # chained: zero gap between calls
+        assert b["t_origin_ns"] == a["t_end_ns"]  # chained: zero gap between calls
+        assert b["t_start_ns"] >= b["t_origin_ns"]  # the real start is kept
     for r in recs:
-        assert abs((r["t_end_ns"] - r["t_start_ns"]) / 1e3 - 200) <= 2.0
+        assert abs((r["t_end_ns"] - r["t_origin_ns"]) / 1e3 - 200) <= 2.0
     # a call issued after an idle stream is not chained
     torch.cuda._sleep(50_000_000)  # ~25 ms of GPU time on the current stream
     comm.all_reduce(x, x)
     torch.cuda.synchronize()
     r = comm.call_record()
+    assert r["t_origin_ns"] == r["t_start_ns"]
     assert r["t_start_ns"] - recs[-1]["t_end_ns"] > 1_000_000
+    comm.close()
+
+
+def test_no_queue_chaining_by_default(cuda):
+    """Off by default (the reference starts every op at its own creation
+    time, engine.cpp:36-41): two delayed calls separated by a ~5 us kernel
+    each take the full modelled latency from their own first kernel."""
+    comm = pb.Communicator(delay_config(8, 2, fixed=200.0), 0, 0)
+    x = torch.zeros(1 << 20, device="cuda")
+    comm.all_reduce(x, x)
+    torch.cuda._sleep(10_000)  # a few microseconds of other work on the stream
+    comm.all_reduce(x, x)
+    torch.cuda.synchronize()
+    last = comm.last_call_id
+    for i in (last - 1, last):
+        r = comm.call_record(i)
+        assert r["t_origin_ns"] == r["t_start_ns"]
+        assert abs((r["t_end_ns"] - r["t_start_ns"]) / 1e3 - 200) <= 2.0
+        assert r["overshoot_ns"] < 2000
+    comm.close()
+
+
+def test_overshoot_is_reported_as_late(cuda):
+    """A model shorter than the emulator's own work cannot be honoured: world
+    64, bf16, 1 GiB, a 64-rank NVLink-class ring (alpha 2 us, 2 x 770 GB/s)
+    models ~1.62 ms while uncached synthesis of 63 emulated ranks takes
+    ~2.2 ms.  The call record says so (late_ns ~ the overshoot; the event-
+    timed call length agrees); with the synthesis cache warm the fold takes
+    ~0.5 ms and the same call is on time."""
+    cfg = ("world_size = 64\nreal_ranks = 0\nbucket_bytes = 1\ndelay.kind = alpha_beta\n"
+           "link.alpha_us = 2\nlink.beta_us_per_byte = 0.000000649\n")
+    comm = pb.Communicator(cfg, 0, 0)
+    x = torch.zeros(1 << 29, dtype=torch.bfloat16, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def call():
+        torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
+        e0.record()
+        comm.all_reduce(x, x)
+        e1.record()
+        torch.cuda.synchronize()
+        return comm.call_record(), e0.elapsed_time(e1) * 1e3
+
+    comm.set_synth_cache(0, 16)  # synthesise every call
+    call()
+    rec, ev_us = call()
+    model = rec["model_latency_us"]
+    assert 1500 < model < 1700
+    dev_us = (rec["t_end_ns"] - rec["t_start_ns"]) / 1e3
+    assert rec["overshoot_ns"] / 1e3 > 200, rec  # reported, not silent
+    assert abs(dev_us - (model + rec["overshoot_ns"] / 1e3)) <= 1.0
+    assert rec["late_ns"] >= rec["overshoot_ns"]  # the early steps were later still
+    assert ev_us >= dev_us - 1.0
+    comm.set_synth_cache(4 << 30, 16)
+    call()  # fills the cache
+    rec, ev_us = call()
+    assert rec["overshoot_ns"] < 2000, rec
+    assert abs((rec["t_end_ns"] - rec["t_start_ns"]) / 1e3 - model) <= max(0.01 * model, 2.0)
+    assert ev_us <= model + 50.0  # event-timed stream occupancy: model + launch overhead
     comm.close()
 
 

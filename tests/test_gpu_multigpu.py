@@ -115,3 +115,30 @@ def test_two_streams_over_one_comm_stay_ordered():
         assert res["bad_allgather"] == 0 and res["bad_rs_ar"] == 0, res
         assert res["async_error"] is None, res
         assert res["launches"] >= 2000, res  # every call ran as a fused kernel
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_graph_capture_of_copy_engine_allreduce_with_plugin_delay():
+    """Nothing on the enqueue path blocks the host: a 512 MiB allreduce (the
+    copy-engine pipeline at two GPUs, the fused kernel at four) with a
+    delay-model plugin is captured into a CUDA graph; each replay equals the
+    eager call bit for bit (and the oracle on its first 1 Mi elements) and
+    releases on the plugin's floors (tests/graph_worker.py)."""
+    import json
+    import re
+    n = min(torch.cuda.device_count(), 4)
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "graph_worker.py")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()), worker],
+                       capture_output=True, text=True, timeout=420)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [json.loads(m) for m in re.findall(r"\{\"rank.*?\]\, \"async_error\": [^}]*\}", r.stdout)]
+    assert len(lines) == n, r.stdout
+    for res in lines:
+        assert res["async_error"] is None, res
+        if n == 2:
+            assert res["captured_launches"] >= 4, res  # barrier + fold chunks + barrier + delay: the CE pipeline
+        for rep in res["replays"]:
+            assert rep["equal_eager"] and rep["equal_oracle_1Mi"] and rep["floors_ok"], rep
+            assert abs(rep["delay_us"] - 3000) <= 30 and rep["overshoot_us"] < 2, rep
