@@ -44,6 +44,8 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mib", type=int, default=1024, help="buffer per real GPU (MiB)")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-fidelity", action="store_true",
+                    help="N > 1: skip the emulated-vs-baseline fidelity block (fidelity.py)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -672,7 +674,33 @@ def run_ours(args, rank, world_size, local_rank):
                                                * 2 * (RANKS_PER_GPU * n - 1) / (RANKS_PER_GPU * n), 2),
                            "note": "NCCL-style: algbw = S/t per GPU summed over GPUs, busbw = algbw*2(W-1)/W"}}
     if n > 1:
+        # the same step on plain (unregistered) buffers: NCCL reduce-scatter +
+        # synthesis on the own shard + NCCL allgather -- what an unmodified
+        # job gets without ncclCommRegister / ncclMemAlloc + window registration
+        xp, yp = torch.empty_like(x), torch.empty_like(y)
+        xp.copy_(x)
+        for _ in range(args.warmup):
+            comm.all_reduce(xp, yp)
+        barrier()
+        f0, f1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            comm.all_reduce(xp, yp)
+        f1.record(stream)
+        torch.cuda.synchronize(device)
+        fb_ms = max_over_ranks(f0.elapsed_time(f1)) / args.steps
+        extra["unregistered_buffers"] = {
+            "value": round(n * 2 * nbytes / (fb_ms * 1e-3) / 1e9, 2), "unit": UNIT, "ms_per_step": round(fb_ms, 5),
+            "path": "NCCL reduce-scatter + synth_reduce_vec on the own 1/N shard + NCCL allgather "
+                    "(buffers not from cemuMemAlloc / cemuCommRegister)"}
+        del xp, yp
         extra["config3_shape"] = config3_block(torch, pb, comm_args=(rank, device, n, uid, dist))
+        if not args.no_fidelity:
+            from paper_2405_02969_b200 import fidelity
+            fid = fidelity.run([s for s in fidelity.SIZES if s <= (64 << 20)], reps=100, segments=1,
+                               e2e_iters=10, mlp_iters=20)
+            if rank == 0:
+                extra["fidelity"] = fid
     if rank == 0 and n == 1:
         extra["delay_error"] = delay_error_block(torch, pb, device)
         if not args.no_sweep:

@@ -242,6 +242,14 @@ cemuResult_t cemuCommSetDelayModel(cemuComm_t comm, cemuDelayModelFn fn, void* u
  * own kernel-dispatch gap.  The record keeps both instants (t_start_ns,
  * t_origin_ns).  cemuRunTrainingLoop uses 10 us for its own loop. */
 cemuResult_t cemuCommSetQueueChaining(cemuComm_t comm, int64_t gapUs);
+/* The real collective's SM footprint.  A real collective's
+ * kernel (NCCL: one CTA per channel) occupies SMs for its whole duration,
+ * slowing compute that runs beside it on other streams.  With ctas > 0 every
+ * delayed call's wait also holds `ctas` CTAs (512 threads, smemBytes of
+ * shared memory each) until its modelled end, so that contention is
+ * emulated too.  0 (the default; CEMU_DELAY_HOLD_CTAS / _SMEM) holds one
+ * CTA, the schedule's. */
+cemuResult_t cemuCommSetDelayFootprint(cemuComm_t comm, int ctas, size_t smemBytes);
 
 cemuResult_t cemuCommLastCallId(cemuComm_t comm, uint64_t* callId);
 /* Copies the record (and up to `cap` floors / release times / offsets) of a

@@ -134,6 +134,7 @@ def _load():
         "cemuPayloadWord": (u32, [u32, u64]),
         "cemuCommSetDelayModel": (i32, [vp, DELAY_MODEL_FN, vp]),
         "cemuCommSetQueueChaining": (i32, [vp, i64]),
+        "cemuCommSetDelayFootprint": (i32, [vp, i32, sz]),
         "cemuConfigTopology": (u32, [vp, C.POINTER(TopoNode), C.POINTER(TopoEdge), sz]),
         "cemuRingSuccessor": (u32, [u32, u32]),
         "cemuRingPredecessor": (u32, [u32, u32]),

@@ -243,6 +243,12 @@ class Communicator:
         that call's end (0 = off, the default)."""
         check(lib.cemuCommSetQueueChaining(self._h, int(gap_us)), self._h)
 
+    def set_delay_footprint(self, ctas: int, smem_bytes: int = 0) -> None:
+        """cemuCommSetDelayFootprint: every delayed call also holds `ctas`
+        CTAs (512 threads, smem_bytes each) until its modelled end -- the SMs
+        a real collective's kernel would take from compute beside it."""
+        check(lib.cemuCommSetDelayFootprint(self._h, int(ctas), int(smem_bytes)), self._h)
+
     # -- wire mode (interop with a reference cemu-emulator) -------------------
     def attach_emulator(self, plan: list, timeout_ms: int = 10000) -> None:
         """cemuCommAttachEmulator: dial the config's emulator endpoint and

@@ -468,6 +468,9 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
   c->delay_active = cfg.delay_kind != DelayKind::kNone || cfg.delay_inject_us != 0.0;
   c->config_delay_active = c->delay_active;
   c->queue_gap_ns = queue_gap_ns();
+  if (const char* h = std::getenv("CEMU_DELAY_HOLD_CTAS")) c->hold_ctas = std::max(0, std::atoi(h));
+  if (const char* h = std::getenv("CEMU_DELAY_HOLD_SMEM")) c->hold_smem = std::max(0, std::atoi(h));
+  if (const char* h = std::getenv("CEMU_DELAY_HOLD_ACTIVE")) c->hold_active = std::atoi(h) ? 1 : 0;
   {
     const char* mb = std::getenv("CEMU_SYNTH_CACHE_MB");
     c->cache_cap = (mb ? std::strtoull(mb, nullptr, 10) : 4096ull) << 20;
@@ -499,6 +502,7 @@ cemuResult_t init_comm(cemuComm_t* out, JobConfig cfg, const cemuUniqueId& id, i
   CUDA_OK(cudaMemcpy(c->d_virt_keys, keys.data(), keys.size() * 4, cudaMemcpyHostToDevice));
   CUDA_OK(cudaMemcpy(c->d_virt_ranks, c->virt.data(), c->virt.size() * 4, cudaMemcpyHostToDevice));
   for (int coll = 0; coll < 4; ++coll) c->kmax = std::max(c->kmax, to_real_count(coll, c->W, c->real));
+  CUDA_OK(preload_delay_kernels());
   CUDA_OK(cudaMalloc(&c->d_slots, cemuComm::kSlots * slot_words(c->kmax) * 8));
   CUDA_OK(cudaMemset(c->d_slots, 0, cemuComm::kSlots * slot_words(c->kmax) * 8));
   if (c->k > 1) {
@@ -1513,6 +1517,15 @@ cemuResult_t cemuCommModelLatencyUs(cemuComm_t c, int coll, uint64_t bytes, int6
     return cemuSuccess;
   }
   *out = c->delay_active ? call_latency_us(c->delay, coll, c->W, bytes, k) : 0;
+  return cemuSuccess;
+}
+
+cemuResult_t cemuCommSetDelayFootprint(cemuComm_t c, int ctas, size_t smem_bytes) {
+  if (!c || ctas < 0 || ctas > 4096 || smem_bytes > 227 * 1024) {
+    return fail(cemuInvalidArgument, "cemuCommSetDelayFootprint: ctas in [0, 4096], smem <= 227 KB");
+  }
+  c->hold_ctas = ctas;
+  c->hold_smem = static_cast<int32_t>(smem_bytes);
   return cemuSuccess;
 }
 

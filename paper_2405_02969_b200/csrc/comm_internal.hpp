@@ -115,6 +115,7 @@ struct cemuComm {
   int64_t* last_slot = nullptr;
   cudaStream_t last_stream = nullptr;
   int64_t queue_gap_ns = 0;  // cemuCommSetQueueChaining (0: every call's schedule starts at its own start)
+  int32_t hold_ctas = 0, hold_smem = 0, hold_active = 0;  // cemuCommSetDelayFootprint
   ncclComm_t inner = nullptr;
   uint64_t launches = 0;
   // fused multi-GPU path (k > 1): IPC-mapped signal areas and symmetric buffers
@@ -330,6 +331,9 @@ struct Call {
     d.preloaded = 0;
     d.prev_end = (c->last_slot && c->last_stream == s) ? c->last_slot + 1 : nullptr;
     d.queue_gap_ns = c->queue_gap_ns;
+    d.hold_ctas = c->hold_ctas;
+    d.hold_smem = c->hold_smem;
+    d.hold_active = c->hold_active;
     if (!plugin.empty() && plugin.size() <= static_cast<size_t>(kInlineOffsets)) {
       // the offsets ride in the spin kernel's parameter block: nothing on
       // the host to recycle, no host wait, graph-capture safe

@@ -1278,16 +1278,23 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
   // Evaluate the model on the device: delay.cpp:23-47 offsets and
   // engine.cpp:41 llround floors, strided over the block.  A delay-model
   // plugin's offsets (DelayModelFn, delay.hpp:52-55) arrive preloaded.
+  // The releasing thread reads the floors from shared memory (up to
+  // kInlineOffsets of them): its loop is then a few cycles per step, so the
+  // last release follows the last floor by nanoseconds, not by K global loads.
+  __shared__ int64_t sfloor[kInlineOffsets];
   const double total = (!d.preloaded && d.model.kind == 1) ? model_total_us(d.model, d.coll, d.n, d.bytes) : 0.0;
   for (uint32_t j = threadIdx.x; j < d.k; j += blockDim.x) {
     const double o = inline_offs ? inline_offs[j] : d.preloaded ? offs[j] : release_offset_us(d.model, total, j, d.k);
     offs[j] = o;
-    floors[j] = llround(o);
+    const int64_t f = llround(o);
+    floors[j] = f;
+    if (j < static_cast<uint32_t>(kInlineOffsets)) sfloor[j] = f;
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  auto floor_at = [&](uint32_t j) { return j < static_cast<uint32_t>(kInlineOffsets) ? sfloor[j] : floors[j]; };
   int64_t lat = 0;
-  for (uint32_t j = 0; j < d.k; ++j) lat = max(lat, floors[j]);
+  for (uint32_t j = 0; j < d.k; ++j) lat = max(lat, floor_at(j));
   slot[2] = lat;
   slot[3] = d.k;
   // Head-of-line release (engine.cpp:58-70): step j leaves once its floor
@@ -1301,7 +1308,7 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
   int64_t t = globaltimer_ns();
   int64_t late = 0;
   for (uint32_t j = 0; j < d.k; ++j) {
-    const int64_t target = t0 + floors[j] * 1000;
+    const int64_t target = t0 + floor_at(j) * 1000;
     while (t < target) {
       if (target - t > 8000) __nanosleep(2000);
       t = globaltimer_ns();
@@ -1317,6 +1324,53 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
 
 __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int64_t* slot) {
   delay_spin_body(d, slot, nullptr);
+}
+
+// The network wait with the real collective's SM footprint:
+// CTA 0 runs the schedule as above; CTAs 1..hold_ctas stand in for the
+// real collective's kernel (e.g. NCCL's channels) and hold an SM slot each
+// -- hold_smem bytes of shared memory, kHoldThreads threads -- until the
+// call's modelled end, so compute running beside the collective on other
+// streams sees the SMs a real collective would take from it.  Each holder
+// derives the end itself from the same inputs (the start stamp written by
+// the call's first kernel, the model or the plugin's offsets): no
+// cross-CTA signalling, graph-replay safe.
+constexpr int kHoldThreads = 512;
+__global__ void __launch_bounds__(kHoldThreads) delay_spin_hold_kernel(DelayLaunch d, int64_t* slot,
+                                                                       const __grid_constant__ InlineOffsets o,
+                                                                       int use_inline) {
+  if (blockIdx.x == 0) {
+    delay_spin_body(d, slot, use_inline ? o.us : nullptr);
+    return;
+  }
+  extern __shared__ char hold_smem[];
+  __shared__ unsigned long long lat_s;
+  __shared__ int64_t t0_s;
+  if (threadIdx.x == 0) {
+    lat_s = 0;
+    int64_t t0 = d.self_stamp ? globaltimer_ns() : slot[0];
+    if (d.prev_end && d.queue_gap_ns > 0) {
+      const int64_t pe = *d.prev_end;
+      if (pe > 0 && t0 >= pe && t0 - pe <= d.queue_gap_ns) t0 = pe;
+    }
+    t0_s = t0;
+    hold_smem[0] = 0;  // the reservation is the point; touch it so it is kept
+  }
+  __syncthreads();
+  const double* offs = reinterpret_cast<const double*>(slot + kSlotHeader + 2 * static_cast<size_t>(d.kmax));
+  const double total = (!d.preloaded && d.model.kind == 1) ? model_total_us(d.model, d.coll, d.n, d.bytes) : 0.0;
+  for (uint32_t j = threadIdx.x; j < d.k; j += blockDim.x) {
+    const double v = use_inline ? o.us[j] : d.preloaded ? offs[j] : release_offset_us(d.model, total, j, d.k);
+    atomicMax(&lat_s, static_cast<unsigned long long>(max(int64_t{0}, static_cast<int64_t>(llround(v)))));
+  }
+  __syncthreads();
+  const int64_t end = t0_s + static_cast<int64_t>(lat_s) * 1000;
+  if (d.hold_active) {
+    while (globaltimer_ns() < end) {
+    }
+  } else {
+    while (globaltimer_ns() < end) __nanosleep(2000);
+  }
 }
 
 // A plugin's offsets travel in the launch's own parameter block (<= 16 KB):
@@ -1862,9 +1916,37 @@ int64_t queue_gap_ns() {
   return gap;
 }
 
+// Loads the delay path's kernels now (CUDA lazy loading would otherwise
+// load each at its first launch -- inside the first delayed call's wait).
+cudaError_t preload_delay_kernels() {
+  cudaFuncAttributes a;
+  for (const void* f : {reinterpret_cast<const void*>(delay_spin_kernel),
+                        reinterpret_cast<const void*>(delay_spin_inline_kernel),
+                        reinterpret_cast<const void*>(delay_spin_hold_kernel),
+                        reinterpret_cast<const void*>(stamp_kernel)}) {
+    if (const cudaError_t e = cudaFuncGetAttributes(&a, f)) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t s, int* launches,
                               const InlineOffsets* offs) {
   ++*launches;
+  if (offs && d.k > static_cast<uint32_t>(kInlineOffsets)) return cudaErrorInvalidValue;
+  if (d.hold_ctas > 0) {
+    static InlineOffsets none{};  // (parameter block of a call without inline offsets)
+    const size_t smem = static_cast<size_t>(std::max(0, d.hold_smem));
+    if (smem > 48 * 1024) {
+      if (const cudaError_t e = cudaFuncSetAttribute(delay_spin_hold_kernel,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     static_cast<int>(smem))) {
+        return e;
+      }
+    }
+    delay_spin_hold_kernel<<<1 + d.hold_ctas, kHoldThreads, smem, s>>>(d, slot, offs ? *offs : none,
+                                                                        offs ? 1 : 0);
+    return cudaGetLastError();
+  }
   if (offs) {
     if (d.k > static_cast<uint32_t>(kInlineOffsets)) return cudaErrorInvalidValue;
     delay_spin_inline_kernel<<<1, kThreads, 0, s>>>(d, slot, *offs);

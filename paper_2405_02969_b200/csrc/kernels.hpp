@@ -40,6 +40,12 @@ struct DelayLaunch {
   // one leaves the wire).
   const int64_t* prev_end;
   int64_t queue_gap_ns;
+  // the real collective's SM footprint to hold for the call's modelled
+  // duration (cemuCommSetDelayFootprint): CTAs beside the schedule CTA and
+  // the shared memory each reserves
+  int32_t hold_ctas = 0;
+  int32_t hold_smem = 0;
+  int32_t hold_active = 0;  // holders busy-poll (issue slots taken, as a polling collective kernel's)
 };
 
 // *chain = max(*chain, *other) in stream order (one 1-thread kernel).
@@ -164,5 +170,6 @@ struct InlineOffsets {
 };
 cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t stream,
                               int* launches, const InlineOffsets* offs = nullptr);
+cudaError_t preload_delay_kernels();
 
 }  // namespace cemu_b200
