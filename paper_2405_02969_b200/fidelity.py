@@ -339,8 +339,9 @@ def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=40, footprint=
         dist.barrier(group=host)
 
     res = {"k": k, "sizes": sizes, "reps": reps, "segments": segments}
-    # --- calibration: an idle sweep (alpha-beta fit + table) ---------------
-    calib = [u for u, _ in baseline_sweep(sizes, reps)]
+    # --- calibration: idle sweeps (alpha-beta fit + table); the per-size
+    # median of three keeps one noisy sweep out of the profile --------------
+    calib = [float(u) for u in np.median([[u for u, _ in baseline_sweep(sizes, reps)] for _ in range(3)], axis=0)]
     fit = fit_alpha_beta(sizes, calib, k)
     plugin = table_plugin(sizes, calib)
     res["fit"] = fit

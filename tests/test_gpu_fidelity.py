@@ -37,7 +37,7 @@ def test_emulated_matches_baseline():
     n = min(torch.cuda.device_count(), 4)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                         "--master-addr", "127.0.0.1", "--master-port", str(_port()), "-m",
-                        "paper_2405_02969_b200.fidelity", "--segments", "2", "--max-mib", "64",
+                        "paper_2405_02969_b200.fidelity", "--segments", "3", "--max-mib", "64",
                         "--e2e-iters", "12", "--mlp-iters", "12"],
                        capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
