@@ -395,9 +395,11 @@ cemuResult_t order_end(cemuComm* c, cudaStream_t s) {
 }
 
 // 20-bit signature of a fused call; every real rank must compute the same
-uint32_t op_sig(int coll, int dt, uint64_t count) {
+uint64_t buf_tag(const cemuComm::Region* r, uint64_t off) { return r ? (r->id << 40) ^ off : 0; }
+
+uint32_t op_sig(int coll, int dt, uint64_t count, uint64_t bufs) {
   uint64_t h = 1469598103934665603ull;
-  for (uint64_t v : {static_cast<uint64_t>(coll), static_cast<uint64_t>(dt), count}) {
+  for (uint64_t v : {static_cast<uint64_t>(coll), static_cast<uint64_t>(dt), count, bufs}) {
     h ^= v;
     h *= 1099511628211ull;
   }
@@ -582,11 +584,16 @@ void log_path(const cemuComm* c, const char* coll, uint64_t bytes, const char* p
 // ce_pipeline_probe.cu): start barrier; per chunk of this GPU's slice the
 // copy engine pulls the peer's chunk into staging, the fused kernel in
 // fold-only mode adds local + staged (ascending real rank, as the fused
-// path) and the emulated ranks into the local recv, and the copy engine
-// pushes the result into the peer's recv; done barrier after the pushes.
-// Bit-identical to the fused kernel (same fold code).  Chosen only where it
-// measured faster: two real GPUs, >= 512 MiB, no ragged tail, <= 16
-// emulated ranks (CEMU_CE=1 forces it, CEMU_CE=0 disables it).
+// path) and the emulated ranks into the local recv and a one-thread kernel
+// flags the chunk final; a second copy-engine stream fetches each of the
+// peer's flagged result chunks into the local recv; done barrier after the
+// fetches.  Only reads cross NVLink, so ranks that disagree on the call can
+// never write into each other's memory (the start barrier reports them).
+// Bit-identical to the fused kernel (same fold code).  Opt-in (CEMU_CE=2:
+// two real GPUs, >= 512 MiB, no ragged tail, <= 16 emulated ranks;
+// CEMU_CE=1 forces it): in this read-only form it measured 2-7% faster than
+// the fused kernel for bf16 / int32 but 2-5% slower for fp32 at 1 GiB
+// (profiles/r02_ce_pull_only.txt), so the fused kernel is the default.
 constexpr uint64_t kCeMinBytes = 512ull << 20;
 
 // Chunk of the slice: at most CEMU_CE_CHUNK_MIB (default 256; measured
@@ -625,26 +632,29 @@ bool ce_allreduce_fits(const cemuComm* c, const FusedArgs& a, uint64_t count, si
   return (sv + ce_chunk_vecs(sv) - 1) / ce_chunk_vecs(sv) <= 64;  // the event pool
 }
 
-cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs, cudaStream_t s, Call* call) {
+cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs, uint64_t nvec, cudaStream_t s,
+                          Call* call) {
   auto& p = c->cep;
   const uint64_t slice = stage_vecs * 16;
   if (!p.pull) CUDA_OK(cudaStreamCreateWithFlags(&p.pull, cudaStreamNonBlocking));
-  if (!p.push) CUDA_OK(cudaStreamCreateWithFlags(&p.push, cudaStreamNonBlocking));
+  if (!p.fetch) CUDA_OK(cudaStreamCreateWithFlags(&p.fetch, cudaStreamNonBlocking));
   for (cudaEvent_t& ev : p.ev) {
     if (!ev) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   if (auto r = grow_buffer(c, &p.stage, &p.stage_bytes, slice, "copy-engine staging")) return r;
   const int peer = 1 - a.me;
   const uint4* peer_send = a.src[peer];
-  uint4* peer_recv = a.dst[peer];
+  const uint4* peer_recv = a.dst[peer];
   uint4* my_recv = a.dst[a.me];
+  // the peer's slice of the vectors (k = 2: the other half)
+  const uint64_t pv_begin = a.me == 0 ? a.v_end : 0, pv_end = a.me == 0 ? nvec : a.v_begin;
   a.stamp = call->take_stamp();
   CUDA_OK(cache_fused(c, dt, a, s, &call->launches));  // the fold-only chunks inherit it
   CUDA_OK(launch_peer_barrier(a, 0, s, &call->launches));
-  cudaEvent_t started = p.ev[0], pushed = p.ev[1];
+  cudaEvent_t started = p.ev[0], fetched = p.ev[1];
   CUDA_OK(cudaEventRecord(started, s));
   CUDA_OK(cudaStreamWaitEvent(p.pull, started, 0));
-  CUDA_OK(cudaStreamWaitEvent(p.push, started, 0));
+  CUDA_OK(cudaStreamWaitEvent(p.fetch, started, 0));
   // the staging, indexed like the buffers: element vector v at stage[v - v_begin]
   const auto stage_at = reinterpret_cast<uintptr_t>(p.stage) - a.v_begin * 16;
   FusedArgs f = a;
@@ -658,7 +668,7 @@ cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs,
   for (uint64_t v0 = a.v_begin; v0 < a.v_end; v0 += cvec, ++ci) {
     const uint64_t v1 = std::min(a.v_end, v0 + cvec);
     const size_t n = (v1 - v0) * 16;
-    cudaEvent_t pulled = p.ev[2 + 2 * ci], folded = p.ev[3 + 2 * ci];
+    cudaEvent_t pulled = p.ev[2 + ci];
     CUDA_OK(cudaMemcpyAsync(reinterpret_cast<void*>(stage_at + v0 * 16), peer_send + v0, n,
                             cudaMemcpyDeviceToDevice, p.pull));
     CUDA_OK(cudaEventRecord(pulled, p.pull));
@@ -666,12 +676,21 @@ cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs,
     f.v_begin = v0;
     f.v_end = v1;
     CUDA_OK(launch_fused_allreduce(dt, f, s, &call->launches));
-    CUDA_OK(cudaEventRecord(folded, s));
-    CUDA_OK(cudaStreamWaitEvent(p.push, folded, 0));
-    CUDA_OK(cudaMemcpyAsync(peer_recv + v0, my_recv + v0, n, cudaMemcpyDeviceToDevice, p.push));
+    CUDA_OK(launch_chunk_signal(a, ci, s, &call->launches));  // "my chunk ci is final"
   }
-  CUDA_OK(cudaEventRecord(pushed, p.push));
-  CUDA_OK(cudaStreamWaitEvent(s, pushed, 0));
+  // the peer's result chunks, each once the peer has signalled it: a local
+  // write of data read over NVLink
+  const uint64_t pcvec = ce_chunk_vecs(pv_end - pv_begin);
+  int pi = 0;
+  for (uint64_t v0 = pv_begin; v0 < pv_end; v0 += pcvec, ++pi) {
+    const uint64_t v1 = std::min(pv_end, v0 + pcvec);
+    CUDA_OK(launch_chunk_wait(a, peer, pi, p.fetch, &call->launches));
+    CUDA_OK(cudaMemcpyAsync(my_recv + v0, peer_recv + v0, (v1 - v0) * 16, cudaMemcpyDeviceToDevice, p.fetch));
+  }
+  CUDA_OK(cudaEventRecord(fetched, p.fetch));
+  CUDA_OK(cudaStreamWaitEvent(s, fetched, 0));
+  // done: each side announces once its fetches completed, so neither frees
+  // or rewrites a buffer the other still reads
   CUDA_OK(launch_peer_barrier(a, 1, s, &call->launches));
   CUDA_OK(call->finish(kAllReduce));
   return cemuSuccess;
@@ -725,19 +744,20 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
       dp[g] = rr->peer[g] + roff;
     }
     FusedArgs a = fused_allreduce_args(c, dt, count, 0, sp, dp);
+    const uint64_t tags = buf_tag(rs, soff) * 31 + buf_tag(rr, roff);
     if ((soff | roff) % 16 == 0 && ce_allreduce_fits(c, a, count, es, s)) {
       log_path(c, "allreduce", count * es, "copy-engine pipeline");
       ph.push_back([=]() mutable -> cemuResult_t {
         set_barrier(c, a);
-        a.sig = op_sig(kAllReduce, dt, count);
-        return ce_allreduce(c, dt, a, ce_stage_vecs(count, es), s, call.get());
+        a.sig = op_sig(kAllReduce, dt, count, tags);
+        return ce_allreduce(c, dt, a, ce_stage_vecs(count, es), count / (16 / es), s, call.get());
       });
       return cemuSuccess;
     }
     if ((soff | roff) % 16 == 0) log_path(c, "allreduce", count * es, "fused");
     if ((soff | roff) % 16 == 0) ph.push_back([=]() mutable -> cemuResult_t {
       set_barrier(c, a);
-      a.sig = op_sig(kAllReduce, dt, count);
+      a.sig = op_sig(kAllReduce, dt, count, tags);
       a.ndst = a.k;
       a.stamp = call->take_stamp();
       CUDA_OK(cache_fused(c, dt, a, s, &call->launches));
@@ -825,7 +845,7 @@ cemuResult_t do_allgather(const void* send, void* recv, size_t sc, int dt, cemuC
       }
       FusedGatherArgs a;
       set_barrier(c, a);
-      a.sig = op_sig(kAllGather, dt, sc);
+      a.sig = op_sig(kAllGather, dt, sc, buf_tag(rr, roff));
       a.own = static_cast<const uint4*>(own_src);
       for (uint32_t g = 0; g < c->k; ++g) a.dst[g] = reinterpret_cast<uint4*>(rr->peer[g] + roff);
       a.own_block = c->rank;
@@ -917,7 +937,7 @@ cemuResult_t do_reducescatter(const void* send, void* recv, size_t rc, int dt, c
     }
     FusedArgs a;
     set_barrier(c, a);
-    a.sig = op_sig(kReduceScatter, dt, rc);
+    a.sig = op_sig(kReduceScatter, dt, rc, buf_tag(rs, sbase));
     const uint64_t epv = 16 / es;
     a.ndst = 1;
     a.word_base = (dt == cemuInt32 || dt == cemuUint32) ? mine : mine / 4;

@@ -200,10 +200,13 @@ struct cemuComm {
   size_t wire_buf_bytes = 0;
   // copy-engine allreduce (k = 2, large symmetric buffers):
   // the NVLink legs ride the copy engines, the fold + synthesis the SMs
-  int ce = 2;  // CEMU_CE: 0 off, 1 forced, 2 (default) auto -- see ce_allreduce_fits
+  int ce = 0;  // CEMU_CE: 0 (default) off, 1 forced, 2 auto -- see ce_allreduce_fits
   struct CePipe {
     static constexpr int kEvents = 2 * 64 + 2;
-    cudaStream_t pull = nullptr, push = nullptr;
+    // pull: the peer's send chunks into staging; fetch: the peer's finished
+    // result chunks into the local recv.  Both only READ peer memory: a rank
+    // never writes another GPU's buffers on this path.
+    cudaStream_t pull = nullptr, fetch = nullptr;
     cudaEvent_t ev[kEvents] = {};
     void* stage = nullptr;
     size_t stage_bytes = 0;
@@ -216,7 +219,7 @@ struct cemuComm {
     wire.reset();  // BYE to the emulator
     auto& p = pipe;
     // every internal stream drains before any mapping is closed or memory freed
-    for (cudaStream_t st : {p.h2d, p.comp, p.d2h, cep.pull, cep.push}) {
+    for (cudaStream_t st : {p.h2d, p.comp, p.d2h, cep.pull, cep.fetch}) {
       if (st) cudaStreamSynchronize(st);
     }
     if (order_ev) cudaEventSynchronize(order_ev);
@@ -236,7 +239,7 @@ struct cemuComm {
     for (auto& m : ipc_maps) {
       if (m.second.ptr) cudaIpcCloseMemHandle(m.second.ptr);
     }
-    for (cudaStream_t st : {cep.pull, cep.push}) {
+    for (cudaStream_t st : {cep.pull, cep.fetch}) {
       if (st) cudaStreamDestroy(st);
     }
     if (order_ev) cudaEventDestroy(order_ev);
@@ -408,7 +411,10 @@ cemuResult_t grow_buffer(cemuComm* c, void** buf, size_t* have, size_t bytes, co
 cemuResult_t order_begin(cemuComm* c, cudaStream_t s);
 cemuResult_t order_end(cemuComm* c, cudaStream_t s);
 // 20-bit signature of a fused call; every real rank must compute the same
-uint32_t op_sig(int coll, int dt, uint64_t count);
+// `bufs`: the symmetric buffers' identity (region id, offset) -- ranks that
+// pass different buffers disagree too, and must abort before any transfer
+uint32_t op_sig(int coll, int dt, uint64_t count, uint64_t bufs = 0);
+uint64_t buf_tag(const cemuComm::Region* r, uint64_t off);
 const cemuComm::Region* find_region(const cemuComm* c, const void* p, size_t bytes);
 cemuResult_t check_common(cemuComm* c, int dt, const char* what);
 cemuResult_t check_op(int op, const char* what);

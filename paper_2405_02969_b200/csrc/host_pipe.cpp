@@ -142,7 +142,7 @@ cemuResult_t host_allreduce(const void* send, void* recv, size_t count, int dt, 
       ch.work = [c, call, dt, n, e0](int b, void*, cudaStream_t st) {
         FusedArgs a = fused_allreduce_args(c, dt, n, e0, c->pipe.peer[b], c->pipe.peer[b]);  // in place
         set_barrier(c, a);
-        a.sig = op_sig(kAllReduce, dt, n);
+        a.sig = op_sig(kAllReduce, dt, n, static_cast<uint64_t>(b) + 1);
         if (const cudaError_t e = cache_fused(c, dt, a, st, &call->launches)) return e;
         return launch_fused_allreduce(dt, a, st, &call->launches);
       };

@@ -1022,6 +1022,23 @@ __global__ void peer_barrier_kernel(const __grid_constant__ FusedArgs a, int pha
   }
 }
 
+// Copy-engine pipeline chunk flags: word 64 + c of the signal area (bytes
+// 512 + 8c) holds flag_word(epoch, 0) once result chunk c of the call with
+// that epoch is final.  The fold kernel before the signal completed (stream
+// order); the system fence publishes its writes to the peer's copy engine.
+__global__ void chunk_signal_kernel(const __grid_constant__ FusedArgs a, int chunk) {
+  const uint64_t epoch = *a.epoch + 1;
+  __threadfence_system();
+  st_release_sys(a.flags + 64 + chunk, flag_word(epoch, 0));
+}
+
+__global__ void chunk_wait_kernel(const __grid_constant__ FusedArgs a, int peer, int chunk) {
+  const uint64_t epoch = *a.epoch + 1;
+  if (wait_flag(a.peer_flags[peer] + 64 + chunk, epoch, 0, false, globaltimer_ns(), a.timeout_ns)) {
+    atomicExch(a.error, 2u);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // fills
 // ---------------------------------------------------------------------------
@@ -1829,6 +1846,20 @@ cudaError_t launch_peer_barrier(const FusedArgs& a, int phase, cudaStream_t s, i
   if (a.k < 2 || a.k > 32) return cudaErrorInvalidValue;
   ++*launches;
   peer_barrier_kernel<<<1, 32, 0, s>>>(a, phase);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_signal(const FusedArgs& a, int chunk, cudaStream_t s, int* launches) {
+  if (chunk < 0 || chunk >= 64) return cudaErrorInvalidValue;
+  ++*launches;
+  chunk_signal_kernel<<<1, 1, 0, s>>>(a, chunk);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_wait(const FusedArgs& a, int peer, int chunk, cudaStream_t s, int* launches) {
+  if (chunk < 0 || chunk >= 64 || peer < 0 || peer >= a.k) return cudaErrorInvalidValue;
+  ++*launches;
+  chunk_wait_kernel<<<1, 1, 0, s>>>(a, peer, chunk);
   return cudaGetLastError();
 }
 
