@@ -466,6 +466,54 @@ def config3_block(torch, pb, comm_args):
     return out
 
 
+def cache_block(torch, pb, device):
+    """The synthesis cache at the many-peer shapes: 1 GiB
+    allreduces with the cache off (issue-bound synthesis), on the call that
+    fills it (synthesis + entry writes; allocation excluded) and warm (a
+    3-stream HBM fold).  HBM fraction = algorithmic 2S / time / peak; the
+    warm call's actual traffic also reads the entries."""
+    peak, _ = measured_peak()
+    out = {}
+    S = 1 << 30
+    for W, dname, dt in ((64, "fp32", torch.float32), (64, "bf16", torch.bfloat16), (128, "bf16", torch.bfloat16),
+                         (1024, "bf16", torch.bfloat16)):
+        comm = pb.Communicator(f"world_size = {W}\nreal_ranks = 0\nbucket_bytes = 1\n", 0, device)
+        es = torch.empty(0, dtype=dt).element_size()
+        x = torch.randn(S // es, device=device).to(dt)
+        y = torch.empty_like(x)
+
+        def ms(reps):
+            torch.cuda.synchronize(device)
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            for _ in range(reps):
+                comm.all_reduce(x, y)
+            e1.record()
+            torch.cuda.synchronize(device)
+            return e0.elapsed_time(e1) / reps
+        comm.set_synth_cache(0, 16)
+        comm.all_reduce(x, y)
+        off = ms(3 if W < 1024 else 1)
+        comm.set_synth_cache(4 << 30, 16)
+        comm.all_reduce(x, y)             # allocates + fills
+        comm.set_synth_cache(4 << 30, 16)  # drops the entries, keeps the buffer
+        fill = ms(1)
+        warm = ms(10)
+        entry = 2 if W - 1 <= 256 else 4
+        traffic = 2 * S + (S // es) * entry
+        out[f"world{W}_{dname}"] = {
+            "ms_uncached": round(off, 4), "ms_fill": round(fill, 4), "ms_cached": round(warm, 4),
+            "hbm_frac_uncached": round(2 * S / off / 1e6 / peak, 4), "hbm_frac_cached": round(2 * S / warm / 1e6 / peak, 4),
+            "cached_traffic_bytes": traffic, "cached_traffic_GBps": round(traffic / warm / 1e6, 1),
+            "stats": comm.synth_cache_stats()}
+        comm.close()
+        del x, y
+        torch.cuda.empty_cache()
+    out["note"] = ("1 GiB allreduce, 1 real + (world-1) emulated ranks; cached = the emulated ranks' per-element "
+                   "sums read from the communicator's synthesis cache (exact: same bits, tests/test_gpu_synth_cache.py)")
+    return out
+
+
 def sweep_block(torch, pb, device):
     """Config 2 shape (single B200 emulating a 64-rank ring): algorithmic HBM
     GB/s per collective, fp32 and bf16, 4 KiB .. 1 GiB (powers of 4)."""
@@ -532,7 +580,8 @@ def sweep_block(torch, pb, device):
             "reference_cpu_emulator_us_per_call": ref_pts,
             "note": "allgather: in place, (n-1)*block written; reduce-scatter: own chunk read + written; "
                     "each point = graph-captured back-to-back calls (device time); small sizes are "
-                    "kernel-launch bound and L2-resident", **res}
+                    "kernel-launch bound and L2-resident; allreduce / reduce-scatter >= 1 MiB fold from the "
+                    "synthesis cache the warm-up calls filled (see synthesis_cache)", **res}
 
 
 def run_ours(args, rank, world_size, local_rank):
@@ -704,6 +753,7 @@ def run_ours(args, rank, world_size, local_rank):
     if rank == 0 and n == 1:
         extra["delay_error"] = delay_error_block(torch, pb, device)
         if not args.no_sweep:
+            extra["synthesis_cache"] = cache_block(torch, pb, device)
             extra["sweep_config2"] = sweep_block(torch, pb, device)
             extra["whatif_config4"] = whatif_block(device, not args.no_cpu_baseline)
             from paper_2405_02969_b200 import fsdp

@@ -18,9 +18,12 @@ ap.add_argument("--world", type=int, default=8)
 ap.add_argument("--mib", type=int, default=1024)
 ap.add_argument("--dtype", default="fp32")
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--cache", type=int, default=1, help="0: synthesis cache off (every call synthesises)")
 a = ap.parse_args()
 dt = {"fp32": torch.float32, "bf16": torch.bfloat16}[a.dtype]
 comm = pb.Communicator(f"world_size = {a.world}\nreal_ranks = 0\nbucket_bytes = 1\n", 0, 0)
+if not a.cache:
+    comm.set_synth_cache(0, 16)
 n = (a.mib << 20) // torch.empty(0, dtype=dt).element_size()
 x = torch.randn(n, device="cuda").to(dt)
 y = torch.empty_like(x)
