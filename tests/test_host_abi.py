@@ -48,8 +48,26 @@ def test_nccl_interposer_exports_ncclapi():
     for name in ("ncclAllReduce", "ncclAllGather", "ncclReduceScatter", "ncclBroadcast", "ncclCommInitRank",
                  "ncclCommDestroy", "ncclCommCount", "ncclCommUserRank", "ncclGetUniqueId", "ncclGroupStart",
                  "ncclGroupEnd", "ncclGetErrorString", "ncclCommInitRankConfig", "ncclCommAbort",
-                 "ncclCommRegister", "ncclCommDeregister", "ncclCommSplit", "ncclReduce", "ncclSend", "ncclRecv"):
+                 "ncclCommRegister", "ncclCommDeregister", "ncclCommSplit", "ncclReduce", "ncclSend", "ncclRecv",
+                 "ncclCommWindowRegister", "ncclCommWindowDeregister", "ncclMemAlloc", "ncclMemFree",
+                 "ncclCommGetAsyncError", "ncclCommCuDevice"):
         assert name in exported, name
+
+
+def test_round2_entry_points_reject_bad_arguments_without_a_device():
+    """Registration, synthesis cache, queue chaining and delay footprint: a
+    null communicator or an out-of-range argument is an invalid argument (4)
+    before any device work."""
+    import ctypes as C
+    lib = _capi.lib
+    h = C.c_void_p(1)
+    assert lib.cemuCommRegister(None, None, 0, C.byref(h)) == 4
+    assert lib.cemuCommDeregister(None, None) == 4
+    assert lib.cemuCommSetSynthCache(None, 0, 16) == 4
+    f, hits, b = C.c_uint64(), C.c_uint64(), C.c_size_t()
+    assert lib.cemuCommSynthCacheStats(None, C.byref(f), C.byref(hits), C.byref(b)) == 4
+    assert lib.cemuCommSetQueueChaining(None, 10) == 4
+    assert lib.cemuCommSetDelayFootprint(None, 8, 0) == 4
 
 
 def test_library_is_sm100a_and_links_no_torch():
