@@ -84,3 +84,47 @@ def test_random_collectives_equal_the_oracle(cuda, block):
             assert_bit_equal(to_np(out), want, "broadcast " + what)
     for c in comms.values():
         c.close()
+
+
+@pytest.mark.parametrize("block", range(3))
+def test_random_calls_through_the_synthesis_cache(cuda, block):
+    """Random sequences of >= 1 MiB allreduces / reduce-scatters whose
+    element ranges overlap earlier ones -- fills, hits, partial coverage,
+    buffer growth, misaligned pointers (synthesised) -- with the cache on
+    for any emulated world (min peers 1): every result equals the oracle."""
+    rng = random.Random(7000 + block)
+    comms = {}
+    for _ in range(12):
+        W = rng.choice([5, 17, 64, 100, 257, 300])
+        rank = rng.randrange(W)
+        key = (W, rank)
+        if key not in comms:
+            comms[key] = pb.Communicator(config(W, (rank,), "hash", 1), rank, 0)
+            comms[key].set_synth_cache(1 << 30, 1)
+        comm = comms[key]
+        dt = rng.choice([0, 1, 2, 6, 7, 9])
+        es = torch.empty(0, dtype=TORCH[dt]).element_size()
+        shift = rng.choice([0, 0, 0, 1])
+        what = f"W={W} rank={rank} dt={dt} shift={shift}"
+        if rng.random() < 0.6:
+            count = rng.choice([1 << 20, (1 << 20) + 5, rng.randrange(1 << 18, 3 << 19)]) // max(1, es // 2)
+            count = max(count, (1 << 20) // es + 1)
+            h = host_input(dt, count, seed=rng.randrange(1 << 30))
+            want = P.allreduce(dt, P.PAYLOAD_HASH, W, [rank], rank, 1, [to_np(h)], count)
+            x = _on_device(h, shift)
+            y = _on_device(torch.zeros_like(h), 0)
+            comm.all_reduce(x, y)
+            torch.cuda.synchronize()
+            assert_bit_equal(to_np(y), want, f"cached allreduce n={count} " + what)
+        else:
+            rc = ((1 << 20) // es + rng.randrange(0, 4096)) // 4 * 4
+            h = host_input(dt, rc * W, seed=rng.randrange(1 << 30))
+            want = P.reducescatter(dt, P.PAYLOAD_HASH, W, [rank], rank, 1, [to_np(h)], rc)
+            out = _on_device(torch.zeros(rc, dtype=TORCH[dt]), shift)
+            comm.reduce_scatter(_on_device(h, 0), out)
+            torch.cuda.synchronize()
+            assert_bit_equal(to_np(out), want, f"cached reduce-scatter rc={rc} " + what)
+    stats = [c.synth_cache_stats() for c in comms.values()]
+    assert sum(s["fills"] for s in stats) > 0
+    for c in comms.values():
+        c.close()
