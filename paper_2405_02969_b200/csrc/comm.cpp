@@ -320,7 +320,11 @@ cudaError_t synth_reduce(cemuComm* c, int dt, const void* src, void* dst, uint64
   bool fill = false;
   const CacheRef cr = al ? cache_for(c, dt, e0, e0 + count, s, &fill) : CacheRef{};
   if (!cr.ptr) return launch_synth_reduce(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches);
-  if (fill) {
+  if (fill && (cr.kind == kCacheWide32) == (dt == cemuInt32 || dt == cemuUint32)) {
+    // one pass synthesises, folds and writes the entries (+ the tail's)
+    return launch_synth_reduce_filling(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, cr);
+  }
+  if (fill) {  // > 256 emulated ranks of a byte kind: fill, then the cached fold
     if (stamp) {  // the call starts with the fill
       if (const cudaError_t e = launch_stamp(stamp, s, launches)) return e;
       stamp = nullptr;

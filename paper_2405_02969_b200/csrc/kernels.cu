@@ -407,10 +407,10 @@ __device__ __forceinline__ void t32_to_lanes(const uint4& t, uint32_t n, uint32_
 // ctr[] holds the hoisted c1 values; nkeys >= 1 (launchers route 0 peers
 // elsewhere) and, for kSeed2, even.  Cached modes read the sums of words
 // j0 + u * kThreads * W + w from `cache` instead (ctr, skeys unused).
-template <int K, int U, int kMode>
+template <int K, int U, int kMode, bool kEnt = false>
 __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skeys, uint32_t nkeys,
                                           uint32_t one, uint32_t* r, const void* cache = nullptr,
-                                          uint64_t j0 = 0) {
+                                          uint64_t j0 = 0, uint32_t* ent = nullptr) {
   using T = VT<K>;
   constexpr int NW = U * T::WPV;
   if constexpr (cached(kMode)) {
@@ -460,6 +460,10 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
 #pragma unroll
       for (int i = 0; i < NW; ++i) r[i] = mad_add(payload_mix(key.x, key.y, ctr[i]), one, r[i]);
     }
+    if constexpr (kEnt) {  // synthesis-cache entries: the word sums themselves
+#pragma unroll
+      for (int i = 0; i < NW; ++i) ent[i] = r[i];
+    }
   } else {
     const uint32_t groups = kMulti ? (nkeys + 255) / 256 : 1;
     int32_t s[kMulti ? NW * 4 : 1];
@@ -504,6 +508,14 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
       if constexpr (!kMulti) {
 #pragma unroll
         for (int i = 0; i < NW; ++i) ah_to_lanes<K>(a[i], h[i], nkeys, r + 4 * i);
+        if constexpr (kEnt) {  // synthesis-cache entries: the packed uint16 lane sums
+#pragma unroll
+          for (int i = 0; i < NW; ++i) {
+            const uint32_t even = even_lanes(a[i], h[i]);
+            ent[2 * i] = __byte_perm(even, h[i], 0x5410);      // t0 | t1 << 16
+            ent[2 * i + 1] = __byte_perm(even, h[i], 0x7632);  // t2 | t3 << 16
+          }
+        }
       } else {
         // float kinds carry the -128 offset of the dyadic value; bytes wrap
         const int32_t bias = K == kU8 ? 0 : 128 * static_cast<int32_t>(q1 - q0);
@@ -589,7 +601,10 @@ __device__ __forceinline__ uint4 fold_vec(const uint4& x, const uint32_t* r) {
   return y;
 }
 
-template <int K, int DT, int U, int kMode>
+// kFill: also write the synthesis cache's entries of the tile's payload
+// words (single-group modes: <= 256 byte-kind peers, or the word kinds) --
+// the first call over a range fills the cache in its own synthesis pass.
+template <int K, int DT, int U, int kMode, bool kFill = false>
 __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     const uint4* __restrict__ src, uint4* dst, uint64_t nvec, uint64_t word_base,
     const uint32_t* __restrict__ keys, uint32_t nkeys, int64_t* stamp, const void* tail_src,
@@ -617,11 +632,27 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     // 2. the emulated peers' sums (registers only; or the cached sums),
     // 3. fold + stream out
     uint32_t r[T::kWords ? NW : NW * 4];
-    peer_sums<K, U, kMode>(ctr, skeys, nkeys, one, r, cache, j0);
+    uint32_t ent[kFill ? (T::kWords ? NW : 2 * NW) : 1];
+    peer_sums<K, U, kMode, kFill>(ctr, skeys, nkeys, one, r, cache, j0, ent);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
       if (v < nvec) st_stream(dst + v, fold_vec<K>(x[u], r + u * W * (T::kWords ? 1 : 4)));
+      if constexpr (kFill) {
+        if (v < nvec) {
+          const uint64_t jv = j0 + static_cast<uint64_t>(u) * kThreads * W;
+          if constexpr (T::kWords) {  // `cache` is the (writable) entry array in fill mode
+            st_stream(reinterpret_cast<uint4*>(const_cast<uint32_t*>(static_cast<const uint32_t*>(cache)) + jv),
+                      make_uint4(ent[u * 4], ent[u * 4 + 1], ent[u * 4 + 2], ent[u * 4 + 3]));
+          } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+              reinterpret_cast<uint2*>(const_cast<void*>(cache))[jv + w] =
+                  make_uint2(ent[2 * (u * W + w)], ent[2 * (u * W + w) + 1]);
+            }
+          }
+        }
+      }
     }
   }
   // ragged tail (< one vector): the last block's first threads
@@ -1468,7 +1499,8 @@ Shape pick_shape(int words_per_vec, uint32_t nkeys, uint64_t nvec) {
 
 template <int K, int DT, int U>
 cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_base,
-                      const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s, int bps_req) {
+                      const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s, int bps_req,
+                      void* fill = nullptr) {
   using T = VT<K>;
   const uint64_t nvec = count / T::EPV;
   const uint32_t ntail = static_cast<uint32_t>(count - nvec * T::EPV);
@@ -1478,6 +1510,10 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
   const int mode = peer_mode(T::kWords, nkeys);
   auto kern = mode == kGroups ? synth_reduce_vec<K, DT, U, kGroups>
               : mode == kSeed1 ? synth_reduce_vec<K, DT, U, kSeed1> : synth_reduce_vec<K, DT, U, kSeed2>;
+  if (fill) {  // the same pass also writes the synthesis cache's entries
+    if (mode == kGroups) return cudaErrorInvalidValue;
+    kern = mode == kSeed1 ? synth_reduce_vec<K, DT, U, kSeed1, true> : synth_reduce_vec<K, DT, U, kSeed2, true>;
+  }
   if (const cudaError_t e = fit_smem(kern, smem)) return e;
   const uint64_t tiles = (nvec + static_cast<uint64_t>(kThreads) * U - 1) / (static_cast<uint64_t>(kThreads) * U);
   // One tile per block over the whole buffer (not a persistent grid-stride
@@ -1498,7 +1534,7 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
   kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(
       static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, keys, nkeys,
       stamp, static_cast<const uint8_t*>(src) + nvec * T::EPV * es,
-      static_cast<uint8_t*>(dst) + nvec * T::EPV * es, ntail, elem_base + nvec * T::EPV, 1u, nullptr);
+      static_cast<uint8_t*>(dst) + nvec * T::EPV * es, ntail, elem_base + nvec * T::EPV, 1u, fill);
   return cudaGetLastError();
 }
 
@@ -1566,8 +1602,9 @@ cudaError_t run_split(const void* src, void* dst, uint64_t count, uint64_t elem_
 
 template <int K, int DT>
 cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_base,
-                    const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s) {
+                    const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s, void* fill = nullptr) {
   constexpr int W = VT<K>::WPV;
+  if (fill && split_ways(VT<K>::kWords, nkeys, count / VT<K>::EPV)) return cudaErrorInvalidValue;
   if (const int P = split_ways(VT<K>::kWords, nkeys, count / VT<K>::EPV)) {
     switch (P) {
       case 2: return run_split<K, DT, 2>(src, dst, count, elem_base, keys, nkeys, stamp, s);
@@ -1579,13 +1616,13 @@ cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_ba
   }
   const Shape sh = pick_shape(W, nkeys, count / VT<K>::EPV);
   if constexpr (8 / W >= 8) {
-    if (sh.u == 8) return run_vec_u<K, DT, 8>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
+    if (sh.u == 8 && !fill) return run_vec_u<K, DT, 8>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
   }
   if constexpr (8 / W >= 4) {
-    if (sh.u == 4) return run_vec_u<K, DT, 4>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
+    if (sh.u >= 4) return run_vec_u<K, DT, 4>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, fill);
   }
-  if (sh.u == 1) return run_vec_u<K, DT, 1>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
-  return run_vec_u<K, DT, 2>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
+  if (sh.u == 1) return run_vec_u<K, DT, 1>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, fill);
+  return run_vec_u<K, DT, 2>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, fill);
 }
 
 template <int DT>
@@ -1657,6 +1694,37 @@ cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t 
     case cemuFloat64: return run_scalar<cemuFloat64>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     default: --*launches; return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_synth_reduce_filling(int dtype, const void* src, void* dst, uint64_t count, uint64_t elem_base,
+                                        const uint32_t* d_keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s,
+                                        int* launches, CacheRef cache) {
+  const bool words = dtype == cemuInt32 || dtype == cemuUint32;
+  if (!cache.ptr || count == 0 || nkeys == 0 || !aligned16(src) || !aligned16(dst) || elem_base % 4 != 0 ||
+      (words ? cache.kind != kCacheWide32 : (cache.kind != kCacheLanes16 || nkeys > 256))) {
+    return cudaErrorInvalidValue;
+  }
+  ++*launches;
+  cudaError_t e = cudaErrorInvalidValue;
+  uint32_t epv = 4;
+  switch (dtype) {
+    case cemuFloat32: e = run_vec<kF32, cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 4; break;
+    case cemuBfloat16: e = run_vec<kBF16, cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 8; break;
+    case cemuFloat16: e = run_vec<kF16, cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 8; break;
+    case cemuUint8: e = run_vec<kU8, cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 16; break;
+    case cemuInt8: e = run_vec<kU8, cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 16; break;
+    case cemuInt32: e = run_vec<kI32, cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 4; break;
+    case cemuUint32: e = run_vec<kI32, cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 4; break;
+    default: break;
+  }
+  if (e != cudaSuccess) {
+    --*launches;
+    return e;
+  }
+  // the ragged tail's entries (elements after the last vector): a small fill
+  const uint64_t done = count / epv * epv;
+  if (done < count) return launch_synth_cache_fill(words, elem_base + done, count - done, d_keys, nkeys, cache, s, launches);
+  return cudaSuccess;
 }
 
 cudaError_t launch_synth_cache_fill(bool words, uint64_t elem_base, uint64_t count, const uint32_t* d_keys,
