@@ -116,6 +116,10 @@ struct cemuComm {
   cudaStream_t last_stream = nullptr;
   int64_t queue_gap_ns = 0;  // cemuCommSetQueueChaining (0: every call's schedule starts at its own start)
   int32_t hold_ctas = 0, hold_smem = 0, hold_active = 0;  // cemuCommSetDelayFootprint
+  // the footprint's side stream, forked from the call's stream at its start
+  // and joined back at its end
+  cudaStream_t hold_stream = nullptr;
+  cudaEvent_t hold_fork = nullptr, hold_join = nullptr;
   ncclComm_t inner = nullptr;
   uint64_t launches = 0;
   // fused multi-GPU path (k > 1): IPC-mapped signal areas and symmetric buffers
@@ -219,7 +223,7 @@ struct cemuComm {
     wire.reset();  // BYE to the emulator
     auto& p = pipe;
     // every internal stream drains before any mapping is closed or memory freed
-    for (cudaStream_t st : {p.h2d, p.comp, p.d2h, cep.pull, cep.fetch}) {
+    for (cudaStream_t st : {p.h2d, p.comp, p.d2h, cep.pull, cep.fetch, hold_stream}) {
       if (st) cudaStreamSynchronize(st);
     }
     if (order_ev) cudaEventSynchronize(order_ev);
@@ -243,6 +247,10 @@ struct cemuComm {
       if (st) cudaStreamDestroy(st);
     }
     if (order_ev) cudaEventDestroy(order_ev);
+    if (hold_stream) cudaStreamDestroy(hold_stream);
+    for (cudaEvent_t ev : {hold_fork, hold_join}) {
+      if (ev) cudaEventDestroy(ev);
+    }
     for (void* r : retired) cudaFree(r);
     cudaFree(cache_bytes.ptr);
     cudaFree(cache_words.ptr);
@@ -309,19 +317,58 @@ struct Call {
   int64_t* take_stamp() {
     if (!slot || stamped) return nullptr;
     stamped = true;
+    footprint_err = begin_footprint();
     return slot;
   }
   cudaError_t stamp_now() {
     if (!slot || stamped) return cudaSuccess;
     stamped = true;
+    if (const cudaError_t e = begin_footprint()) return e;
     return launch_stamp(slot, s, &launches);
   }
+  // The real collective's SM footprint (cemuCommSetDelayFootprint): forked
+  // from the call's stream as its first kernel is enqueued, joined at the end.
+  bool footprint = false;
+  cudaError_t footprint_err = cudaSuccess;
+  cudaError_t begin_footprint() {
+    if (footprint || !slot || c->hold_ctas <= 0 || c->meta[i].latency <= 0) return cudaSuccess;
+    if (!c->hold_stream) {
+      if (const cudaError_t e = cudaStreamCreateWithFlags(&c->hold_stream, cudaStreamNonBlocking)) return e;
+    }
+    for (cudaEvent_t* ev : {&c->hold_fork, &c->hold_join}) {
+      if (!*ev) {
+        if (const cudaError_t e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) return e;
+      }
+    }
+    if (const cudaError_t e = cudaEventRecord(c->hold_fork, s)) return e;
+    if (const cudaError_t e = cudaStreamWaitEvent(c->hold_stream, c->hold_fork, 0)) return e;
+    footprint = true;
+    return launch_footprint(reinterpret_cast<unsigned long long*>(slot + 7), c->meta[i].latency * 1000,
+                            c->hold_ctas, c->hold_smem, c->hold_active, c->hold_stream, &launches);
+  }
   cudaError_t finish(int coll) {
+    if (slot && !stamped) {
+      if (const cudaError_t e = begin_footprint()) return e;  // the spin kernel is the call's first
+    }
+    if (footprint_err) return footprint_err;
     c->launches += launches;
     if (!slot) {
       c->last_slot = nullptr;  // nothing to chain to / join with
       return cudaSuccess;
     }
+    if (footprint) {  // the call ends when its footprint does too
+      const cudaError_t e = launch_delay_and_join(coll);
+      return e;
+    }
+    return launch_delay(coll);
+  }
+  cudaError_t launch_delay_and_join(int coll) {
+    const cudaError_t e = launch_delay(coll);
+    if (e) return e;
+    if (const cudaError_t r = cudaEventRecord(c->hold_join, c->hold_stream)) return r;
+    return cudaStreamWaitEvent(s, c->hold_join, 0);
+  }
+  cudaError_t launch_delay(int coll) {
     const auto& m = c->meta[i];
     DelayLaunch d;
     d.model = c->delay;
@@ -334,9 +381,6 @@ struct Call {
     d.preloaded = 0;
     d.prev_end = (c->last_slot && c->last_stream == s) ? c->last_slot + 1 : nullptr;
     d.queue_gap_ns = c->queue_gap_ns;
-    d.hold_ctas = c->hold_ctas;
-    d.hold_smem = c->hold_smem;
-    d.hold_active = c->hold_active;
     if (!plugin.empty() && plugin.size() <= static_cast<size_t>(kInlineOffsets)) {
       // the offsets ride in the spin kernel's parameter block: nothing on
       // the host to recycle, no host wait, graph-capture safe

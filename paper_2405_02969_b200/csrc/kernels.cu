@@ -1374,46 +1374,29 @@ __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int
   delay_spin_body(d, slot, nullptr);
 }
 
-// The network wait with the real collective's SM footprint:
-// CTA 0 runs the schedule as above; CTAs 1..hold_ctas stand in for the
-// real collective's kernel (e.g. NCCL's channels) and hold an SM slot each
-// -- hold_smem bytes of shared memory, kHoldThreads threads -- until the
-// call's modelled end, so compute running beside the collective on other
-// streams sees the SMs a real collective would take from it.  Each holder
-// derives the end itself from the same inputs (the start stamp written by
-// the call's first kernel, the model or the plugin's offsets): no
-// cross-CTA signalling, graph-replay safe.
+// The real collective's SM footprint: `gridDim.x` CTAs stand in
+// for the real collective's kernel (e.g. NCCL's channels) and hold an SM
+// slot each -- kHoldThreads threads and the launch's shared-memory
+// reservation -- from the call's start until its modelled end, so compute
+// beside the collective on other streams loses the SMs a real collective
+// would take.  Launched on a side stream forked at the call's start (ahead
+// of the synthesis, as a real collective's kernel is dispatched), the first
+// holder to run publishes the start in *start (zeroed before the launch);
+// every holder leaves at start + lat_ns.
 constexpr int kHoldThreads = 512;
-__global__ void __launch_bounds__(kHoldThreads) delay_spin_hold_kernel(DelayLaunch d, int64_t* slot,
-                                                                       const __grid_constant__ InlineOffsets o,
-                                                                       int use_inline) {
-  if (blockIdx.x == 0) {
-    delay_spin_body(d, slot, use_inline ? o.us : nullptr);
-    return;
-  }
+__global__ void __launch_bounds__(kHoldThreads) footprint_kernel(unsigned long long* start, int64_t lat_ns,
+                                                                 int active) {
   extern __shared__ char hold_smem[];
-  __shared__ unsigned long long lat_s;
-  __shared__ int64_t t0_s;
+  __shared__ int64_t end_s;
   if (threadIdx.x == 0) {
-    lat_s = 0;
-    int64_t t0 = d.self_stamp ? globaltimer_ns() : slot[0];
-    if (d.prev_end && d.queue_gap_ns > 0) {
-      const int64_t pe = *d.prev_end;
-      if (pe > 0 && t0 >= pe && t0 - pe <= d.queue_gap_ns) t0 = pe;
-    }
-    t0_s = t0;
+    const unsigned long long now = static_cast<unsigned long long>(globaltimer_ns());
+    const unsigned long long first = atomicCAS(start, 0ull, now);
+    end_s = static_cast<int64_t>(first ? first : now) + lat_ns;
     hold_smem[0] = 0;  // the reservation is the point; touch it so it is kept
   }
   __syncthreads();
-  const double* offs = reinterpret_cast<const double*>(slot + kSlotHeader + 2 * static_cast<size_t>(d.kmax));
-  const double total = (!d.preloaded && d.model.kind == 1) ? model_total_us(d.model, d.coll, d.n, d.bytes) : 0.0;
-  for (uint32_t j = threadIdx.x; j < d.k; j += blockDim.x) {
-    const double v = use_inline ? o.us[j] : d.preloaded ? offs[j] : release_offset_us(d.model, total, j, d.k);
-    atomicMax(&lat_s, static_cast<unsigned long long>(max(int64_t{0}, static_cast<int64_t>(llround(v)))));
-  }
-  __syncthreads();
-  const int64_t end = t0_s + static_cast<int64_t>(lat_s) * 1000;
-  if (d.hold_active) {
+  const int64_t end = end_s;
+  if (active) {
     while (globaltimer_ns() < end) {
     }
   } else {
@@ -2015,13 +1998,28 @@ int64_t queue_gap_ns() {
   return gap;
 }
 
+cudaError_t launch_footprint(unsigned long long* start, int64_t lat_ns, int ctas, int smem, int active,
+                             cudaStream_t s, int* launches) {
+  if (ctas <= 0) return cudaSuccess;
+  if (smem > 48 * 1024) {
+    if (const cudaError_t e = cudaFuncSetAttribute(footprint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   smem)) {
+      return e;
+    }
+  }
+  if (const cudaError_t e = cudaMemsetAsync(start, 0, sizeof *start, s)) return e;
+  ++*launches;
+  footprint_kernel<<<ctas, kHoldThreads, static_cast<size_t>(std::max(0, smem)), s>>>(start, lat_ns, active);
+  return cudaGetLastError();
+}
+
 // Loads the delay path's kernels now (CUDA lazy loading would otherwise
 // load each at its first launch -- inside the first delayed call's wait).
 cudaError_t preload_delay_kernels() {
   cudaFuncAttributes a;
   for (const void* f : {reinterpret_cast<const void*>(delay_spin_kernel),
                         reinterpret_cast<const void*>(delay_spin_inline_kernel),
-                        reinterpret_cast<const void*>(delay_spin_hold_kernel),
+                        reinterpret_cast<const void*>(footprint_kernel),
                         reinterpret_cast<const void*>(stamp_kernel)}) {
     if (const cudaError_t e = cudaFuncGetAttributes(&a, f)) return e;
   }
@@ -2032,20 +2030,6 @@ cudaError_t launch_delay_spin(const DelayLaunch& d, int64_t* slot, cudaStream_t 
                               const InlineOffsets* offs) {
   ++*launches;
   if (offs && d.k > static_cast<uint32_t>(kInlineOffsets)) return cudaErrorInvalidValue;
-  if (d.hold_ctas > 0) {
-    static InlineOffsets none{};  // (parameter block of a call without inline offsets)
-    const size_t smem = static_cast<size_t>(std::max(0, d.hold_smem));
-    if (smem > 48 * 1024) {
-      if (const cudaError_t e = cudaFuncSetAttribute(delay_spin_hold_kernel,
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     static_cast<int>(smem))) {
-        return e;
-      }
-    }
-    delay_spin_hold_kernel<<<1 + d.hold_ctas, kHoldThreads, smem, s>>>(d, slot, offs ? *offs : none,
-                                                                        offs ? 1 : 0);
-    return cudaGetLastError();
-  }
   if (offs) {
     if (d.k > static_cast<uint32_t>(kInlineOffsets)) return cudaErrorInvalidValue;
     delay_spin_inline_kernel<<<1, kThreads, 0, s>>>(d, slot, *offs);

@@ -40,13 +40,13 @@ struct DelayLaunch {
   // one leaves the wire).
   const int64_t* prev_end;
   int64_t queue_gap_ns;
-  // the real collective's SM footprint to hold for the call's modelled
-  // duration (cemuCommSetDelayFootprint): CTAs beside the schedule CTA and
-  // the shared memory each reserves
-  int32_t hold_ctas = 0;
-  int32_t hold_smem = 0;
-  int32_t hold_active = 0;  // holders busy-poll (issue slots taken, as a polling collective kernel's)
 };
+// The real collective's SM footprint for one call (cemuCommSetDelayFootprint):
+// `ctas` CTAs of 512 threads with `smem` bytes each, from the first
+// holder's start for lat_ns; `active` = busy-poll instead of sleeping.
+// *start (a device word) is zeroed in stream order before the launch.
+cudaError_t launch_footprint(unsigned long long* start, int64_t lat_ns, int ctas, int smem, int active,
+                             cudaStream_t stream, int* launches);
 
 // *chain = max(*chain, *other) in stream order (one 1-thread kernel).
 cudaError_t launch_chain_join(int64_t* chain, const int64_t* other, cudaStream_t stream, int* launches);
