@@ -27,7 +27,10 @@ e2e          per-iteration time of the same training loop in both modes
 
 The emulated comm stream is an in-order channel, so queue chaining is on
 (cemuCommSetQueueChaining): a collective queued behind the previous one
-starts when that one leaves the wire, as NCCL's next kernel does.
+starts when that one leaves the wire, as NCCL's next kernel does.  Beside
+real compute the emulated collective also takes the SMs NCCL's kernel would
+(cemuCommSetDelayFootprint with NCCL's measured launch: 32 CTAs, ~101 KB
+shared memory each), from the call's start to its modelled end.
 
     python -m torch.distributed.run --nproc-per-node 2 -m paper_2405_02969_b200.fidelity
 """
@@ -330,7 +333,13 @@ def emulated_comm(k, fit=None, plugin=None, footprint=(0, 0)):
     return comm
 
 
-def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=40, footprint=(32, 100000)):
+# NCCL's allreduce-path kernel on these boxes (ncu launch attributes,
+# profiles/r02_ncu_nccl_kernel_launch.csv): 32 CTAs (its channels) of 544
+# threads, 82,240 B dynamic + 21,568 B static shared memory each.
+NCCL_FOOTPRINT = (32, 82240 + 21568)
+
+
+def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=40, footprint=NCCL_FOOTPRINT):
     sizes = sizes or SIZES
     rank, k = dist.get_rank(), dist.get_world_size()
     host = dist.new_group(backend="gloo")
@@ -406,7 +415,7 @@ def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=40, footprint=
         row["in_situ_service_us"] = {str(b): round(u, 2) for b, u in insitu_us.items()}
         row["footprint"] = {"ctas": footprint[0], "smem_bytes": footprint[1]}
         modes = (("table", {"plugin": plugin}, (0, 0)),
-                 ("loaded", {"plugin": table_plugin(sizes, loaded)}, (0, 0)),
+                 ("table_footprint", {"plugin": plugin}, footprint),
                  ("loaded_footprint", {"plugin": table_plugin(sizes, loaded)}, footprint),
                  ("in_situ_footprint", {"plugin": insitu}, footprint))
         for tag, kw, fp in modes:
@@ -437,8 +446,8 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=20)
     ap.add_argument("--mlp-iters", type=int, default=40)
     ap.add_argument("--max-mib", type=int, default=256)
-    ap.add_argument("--footprint-ctas", type=int, default=32, help="NCCL's channel count on this box")
-    ap.add_argument("--footprint-smem", type=int, default=100000)
+    ap.add_argument("--footprint-ctas", type=int, default=NCCL_FOOTPRINT[0], help="NCCL's channel count on this box")
+    ap.add_argument("--footprint-smem", type=int, default=NCCL_FOOTPRINT[1], help="shared memory per NCCL CTA")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)

@@ -9,7 +9,10 @@ wrapper on the GPU box first runs the profiled command once without ncu, so
 the unprofiled peers are respawned for every rank-0 process: rank 0 writes
 the unique id file, this launcher hands a copy to each peer.
 
-  python profiles/ncu_fused_launch.py N COUNT ITERS OUT.csv METRICS
+  python profiles/ncu_fused_launch.py N COUNT ITERS OUT.csv METRICS [MODE [KERNEL_REGEX]]
+
+MODE plain profiles the NCCL reduce-scatter / allgather path instead (the
+real NCCL kernels' launch footprint, e.g. with KERNEL_REGEX nccl).
 """
 import os
 import subprocess
@@ -22,6 +25,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def main():
     n, count, iters, out_csv, metrics = int(sys.argv[1]), sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5]
+    mode = sys.argv[6] if len(sys.argv) > 6 else "window"
+    kregex = sys.argv[7] if len(sys.argv) > 7 else "fused|synth|barrier|delay"
     d = tempfile.mkdtemp()
     cfg = os.path.join(d, "job.cfg")
     with open(cfg, "w") as f:
@@ -30,8 +35,8 @@ def main():
     app = os.path.join(ROOT, "tests", "apps", "nccl_mp_app")
     idf = os.path.join(d, "id")
     r0 = subprocess.Popen(["ncu", "--metrics", metrics, "--clock-control", "none", "--csv", "--log-file", out_csv,
-                           "-k", "regex:fused|synth|barrier|delay",
-                           app, str(8 * n), "0", "0", count, "window", idf, os.path.join(d, "o0"), iters], env=env)
+                           "-k", f"regex:{kregex}",
+                           app, str(8 * n), "0", "0", count, mode, idf, os.path.join(d, "o0"), iters], env=env)
     rounds = 0
     while r0.poll() is None and rounds < 4:
         if not os.path.exists(idf):
@@ -45,7 +50,7 @@ def main():
             pf = os.path.join(d, f"id_{rounds}_{r}")
             with open(pf, "wb") as f:
                 f.write(data)
-            peers.append(subprocess.Popen([app, str(8 * n), str(r), str(r), count, "window", pf,
+            peers.append(subprocess.Popen([app, str(8 * n), str(r), str(r), count, mode, pf,
                                            os.path.join(d, f"o{r}"), iters], env=env))
         for p in peers:
             p.wait(timeout=600)
