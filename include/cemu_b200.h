@@ -245,7 +245,7 @@ cemuResult_t cemuCommSetQueueChaining(cemuComm_t comm, int64_t gapUs);
 /* The real collective's SM footprint.  A real collective's
  * kernel (NCCL: one CTA per channel) occupies SMs for its whole duration,
  * slowing compute that runs beside it on other streams.  With ctas > 0 every
- * delayed call's wait also holds `ctas` CTAs (512 threads, smemBytes of
+ * delayed call's wait also holds `ctas` CTAs (544 threads, smemBytes of
  * shared memory each) until its modelled end, so that contention is
  * emulated too.  0 (the default; CEMU_DELAY_HOLD_CTAS / _SMEM) holds one
  * CTA, the schedule's. */

@@ -1383,7 +1383,7 @@ __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int
 // of the synthesis, as a real collective's kernel is dispatched), the first
 // holder to run publishes the start in *start (zeroed before the launch);
 // every holder leaves at start + lat_ns.
-constexpr int kHoldThreads = 512;
+constexpr int kHoldThreads = 544;  // NCCL's CTA width on these boxes
 __global__ void __launch_bounds__(kHoldThreads) footprint_kernel(unsigned long long* start, int64_t lat_ns,
                                                                  int active) {
   extern __shared__ char hold_smem[];

@@ -42,7 +42,7 @@ struct DelayLaunch {
   int64_t queue_gap_ns;
 };
 // The real collective's SM footprint for one call (cemuCommSetDelayFootprint):
-// `ctas` CTAs of 512 threads with `smem` bytes each, from the first
+// `ctas` CTAs of 544 threads with `smem` bytes each, from the first
 // holder's start for lat_ns; `active` = busy-poll instead of sleeping.
 // *start (a device word) is zeroed in stream order before the launch.
 cudaError_t launch_footprint(unsigned long long* start, int64_t lat_ns, int ctas, int smem, int active,

@@ -6,8 +6,9 @@ world of the same size, its peers emulated, the network delay calibrated
 from the baseline's own size sweep (paper_2405_02969_b200/fidelity.py).
 Checks: per-call latency emulated / baseline <= 1.05 at >= 2 MiB (the
 reference's rule, :281), and the reference's e2e training loops (bert-like,
-ResNet-50 with 25 MiB buckets) within 1% of the baseline iteration time.
-The real-compute MLP row is reported, not gated."""
+ResNet-50 with 25 MiB buckets) within 1% of the baseline iteration time;
+the real-compute MLP within 2% once calibrated under load with NCCL's SM
+footprint."""
 from __future__ import annotations
 
 import json
@@ -48,3 +49,8 @@ def test_emulated_matches_baseline():
     assert res["microbench_check"]["pass_table"], res["microbench"]
     for row in res["e2e"]:
         assert row["rel_err_table"] < 0.01, row
+    # the real-compute MLP: with the delay calibrated under compute load and
+    # NCCL's SM footprint emulated; 12 noisy iterations here, so
+    # the regression bound is looser than the < 1% the full runs show
+    mlp = res["mlp"]
+    assert min(mlp["rel_err_loaded_footprint"], mlp["rel_err_in_situ_footprint"]) < 0.02, mlp
