@@ -573,12 +573,16 @@ FusedArgs fused_allreduce_args(const cemuComm* c, int dt, uint64_t count, uint64
 // CEMU_DEBUG=INFO: one stderr line per call naming the path it took (the
 // NCCL_DEBUG analogue), so a job can see whether its buffers reach the
 // fused kernels.
-void log_path(const cemuComm* c, const char* coll, uint64_t bytes, const char* path) {
-  static const bool on = [] {
+int debug_level() {  // CEMU_DEBUG: INFO = 1, TRACE = 2
+  static const int level = [] {
     const char* e = std::getenv("CEMU_DEBUG");
-    return e && (std::string(e) == "INFO" || std::string(e) == "TRACE");
+    return !e ? 0 : std::string(e) == "TRACE" ? 2 : std::string(e) == "INFO" ? 1 : 0;
   }();
-  if (on) {
+  return level;
+}
+
+void log_path(const cemuComm* c, const char* coll, uint64_t bytes, const char* path) {
+  if (debug_level() >= 1) {
     std::fprintf(stderr, "cemu: rank %u %s %llu B -> %s\n", c->rank, coll, static_cast<unsigned long long>(bytes),
                  path);
   }
@@ -1055,7 +1059,7 @@ cemuResult_t run_or_defer(cemuComm* c, cudaStream_t s, F&& plan) {
       // unrelated runtime call left behind (e.g. a destroyed communicator's
       // IPC unmapping) so it cannot fail this call
       const cudaError_t pend = cudaGetLastError();
-      if (pend && std::getenv("CEMU_DEBUG_ERR")) {
+      if (pend && debug_level() >= 2) {
         std::fprintf(stderr, "cemu: stale error before phase %d: %s\n", idx, cudaGetErrorString(pend));
       }
       return f();
