@@ -79,8 +79,9 @@ def run():
         return out
 
     # all-gather (fp32, 64 Ki elements per block), reduce-scatter (bf16,
-    # 16 Ki elements per chunk), allreduce (int32, 256 Ki elements)
-    blk, rc, ar = 1 << 16, 1 << 14, 1 << 18
+    # 512 Ki elements per chunk), allreduce (int32, 256 Ki elements): the
+    # last two are >= 1 MiB, so the synthesis cache serves them when on
+    blk, rc, ar = 1 << 16, 1 << 19, 1 << 18
     ag_send, ag_want, rs_send, rs_want, ar_send, ar_want = [], [], [], [], [], []
     for tag in range(2):
         s = inputs(7, blk, tag)

@@ -97,7 +97,8 @@ def test_single_process_init_all(tmp_path):
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
-def test_two_streams_over_one_comm_stay_ordered():
+@pytest.mark.parametrize("cache", ["default", "forced"])
+def test_two_streams_over_one_comm_stay_ordered(cache):
     """1,000 fused all-gathers on stream A interleaved with fused
     reduce-scatters and allreduces on stream B over ONE communicator (the
     FSDP all-gather / reduce-scatter stream pattern): the communicator
@@ -107,9 +108,12 @@ def test_two_streams_over_one_comm_stay_ordered():
     import json
     n = min(torch.cuda.device_count(), 4)
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "interleave_worker.py")
+    # "forced": the synthesis cache on for every call (the fused kernels read
+    # their slices' entries; fills and hits interleave across the streams)
+    env = dict(os.environ, **({"CEMU_SYNTH_CACHE_MIN_PEERS": "1"} if cache == "forced" else {}))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                         "--master-addr", "127.0.0.1", "--master-port", str(_port()), worker],
-                       capture_output=True, text=True, timeout=420)
+                       capture_output=True, text=True, timeout=420, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     import re
     lines = [json.loads(m) for m in re.findall(r"\{[^{}]*\}", r.stdout)]  # ranks' lines may interleave
@@ -118,7 +122,7 @@ def test_two_streams_over_one_comm_stay_ordered():
         assert res["iters"] == 1000
         assert res["bad_allgather"] == 0 and res["bad_rs_ar"] == 0, res
         assert res["async_error"] is None, res
-        assert res["launches"] >= 2000, res  # every call ran as a fused kernel
+        assert res["launches"] >= 2000, res  # every call ran as a fused kernel (+ cache fills)
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
