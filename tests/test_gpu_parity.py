@@ -444,3 +444,25 @@ def test_cuda_graph_capture_and_replay(cuda):
         rec = comm.call_record()
         assert abs((rec["t_end_ns"] - rec["t_start_ns"]) / 1e3 - 40) <= 2
     comm.close()
+
+
+def test_registration_on_one_real_gpu(comms):
+    """cemuCommRegister / Deregister with one real GPU: bookkeeping only --
+    calls on a registered tensor are unchanged, a handle can be dropped once,
+    an unknown handle is an invalid argument, a null buffer registers nothing."""
+    import ctypes as C
+    from paper_2405_02969_b200._capi import lib
+    comm = comms(8)
+    x = host_input(7, 100003, seed=5)
+    d = x.cuda()
+    h = comm.register(d)
+    assert h
+    y = torch.empty_like(d)
+    comm.all_reduce(d, y)
+    torch.cuda.synchronize()
+    assert_bit_equal(to_np(y), P.allreduce(7, P.PAYLOAD_HASH, 8, [0], 0, 1, [to_np(x)], 100003), "registered")
+    comm.deregister(h)
+    with pytest.raises(pb.CemuError, match="not returned by cemuCommRegister"):
+        comm.deregister(h)
+    out = C.c_void_p(1)
+    assert lib.cemuCommRegister(comm._h, None, 0, C.byref(out)) == 0 and not out.value
