@@ -173,7 +173,8 @@ cemuResult_t cemuCommDeregister(cemuComm_t comm, void* handle);
 /* Synthesis cache.  The emulated ranks' payloads depend only on
  * (seed, rank, element index), so their per-element sums are the same in
  * every call over the same element range.  A call over a range of >= 1 MiB
- * with >= minPeers emulated ranks writes those sums into a per-communicator
+ * (or >= 64 KiB when elements x emulated ranks >= 2^27) with >= minPeers
+ * emulated ranks writes those sums into a per-communicator
  * cache (2 bytes per element for the byte kinds up to 256 emulated ranks,
  * else 4) and later calls over the range fold from it -- a memory-bound pass
  * instead of issue-bound synthesis, with identical bits.  capBytes bounds

@@ -278,8 +278,12 @@ CacheRef cache_for(cemuComm* c, int dt, uint64_t b, uint64_t e, cudaStream_t s, 
       !cacheable_dtype(dt) || b % 4 != 0 || e <= b) {
     return {};
   }
-  // small calls are launch-bound either way: not worth an entry
-  if ((e - b) * dtype_size(dt) < (1u << 20)) return {};
+  // small calls are launch-bound either way: not worth an entry -- unless
+  // the world makes even a small range's synthesis long (>= 2^27 peer-
+  // elements: e.g. a 1024-rank FSDP reduce-scatter chunk of ~0.4 MB)
+  const uint64_t bytes = (e - b) * dtype_size(dt);
+  const bool heavy = (e - b) * static_cast<uint64_t>(c->virt.size()) >= (1ull << 27) && bytes >= (64u << 10);
+  if (bytes < (1u << 20) && !heavy) return {};
   const bool words = dt == cemuInt32 || dt == cemuUint32;
   auto& sc = words ? c->cache_words : c->cache_bytes;
   if (sc.kind == kNoCache) sc.kind = (words || c->virt.size() > 256) ? kCacheWide32 : kCacheLanes16;
