@@ -93,6 +93,11 @@ const char* cemuGetLastError(cemuComm_t comm);
 /* ------------------------------------------------------------------ */
 /* Collectives (NCCL signatures)                                        */
 /* ------------------------------------------------------------------ */
+/* Ordering (NCCL's semantics; the reference's one-op-in-flight engine,
+ * collective.cpp:357-404): a communicator's calls take effect in the order
+ * they are issued, also across streams -- a call on another stream than the
+ * previous call waits for it on the device (the host never blocks).  As with
+ * NCCL, one communicator is driven by one host thread at a time. */
 /* replaces WorkerSession::allreduce_async (collective.cpp:213-216) */
 cemuResult_t cemuAllReduce(const void* sendbuff, void* recvbuff, size_t count,
                            cemuDataType_t datatype, cemuRedOp_t op, cemuComm_t comm,
