@@ -64,9 +64,10 @@ def workload(args, n):
             "emulated_ranks": RANKS_PER_GPU * n - n, "dtype": "fp32",
             "l2_policy": "inputs larger than L2 (1 GiB >> 126 MB)",
             "parallelism": (("2 real GPUs: copy-engine pipelined allreduce per step -- start barrier, "
-                             "per 256 MiB chunk CE pull of the peer's shard + fold/synthesis kernel, CE fetch of "
-                             "the peer's result chunks, done barrier (CEMU_CE=1)" if n == 2 and
-                             os.environ.get("CEMU_CE", "0") != "0" else
+                             "per 256 MiB chunk CE pull of the peer's shard + fold/synthesis kernel storing into "
+                             "both GPUs' recv (the peer store gated on the barrier), done barrier "
+                             "(CEMU_CE=0: the fused kernel)" if n == 2 and
+                             os.environ.get("CEMU_CE", "2") != "0" else
                              f"{n} real GPU(s): one fused NVLink allreduce + synthesis kernel per step "
                              "(CEMU_FUSED=0: NCCL RS/AG + per-GPU synthesis)") if n > 1 else
                             "1 real GPU: one synthesis kernel per step")}
@@ -678,8 +679,8 @@ def run_ours(args, rank, world_size, local_rank):
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": None,
                     "kernel": (("peer_barrier_kernel x2 + fused_allreduce_vec<fp32> (fold-only) per chunk; "
-                                "NVLink legs on the copy engines") if n == 2 and fused and
-                               os.environ.get("CEMU_CE", "0") != "0" else
+                                "peer pulls on the copy engines, peer stores from the SMs") if n == 2 and fused and
+                               os.environ.get("CEMU_CE", "2") != "0" else
                                "fused_allreduce_vec<fp32>: P2P pull of every real GPU's shard + synthesis + "
                                "P2P push of the result, one launch per step") if fused else
                               "NCCL reduce-scatter + synth_reduce_vec<fp32> + NCCL allgather",

@@ -594,18 +594,16 @@ void log_path(const cemuComm* c, const char* coll, uint64_t bytes, const char* p
 
 // Copy-engine allreduce at k = 2 (probe: profiles/
 // ce_pipeline_probe.cu): start barrier; per chunk of this GPU's slice the
-// copy engine pulls the peer's chunk into staging, the fused kernel in
+// copy engine pulls the peer's chunk into staging and the fused kernel in
 // fold-only mode adds local + staged (ascending real rank, as the fused
-// path) and the emulated ranks into the local recv and a one-thread kernel
-// flags the chunk final; a second copy-engine stream fetches each of the
-// peer's flagged result chunks into the local recv; done barrier after the
-// fetches.  Only reads cross NVLink, so ranks that disagree on the call can
-// never write into each other's memory (the start barrier reports them).
-// Bit-identical to the fused kernel (same fold code).  Opt-in (CEMU_CE=2:
-// two real GPUs, >= 512 MiB, no ragged tail, <= 16 emulated ranks;
-// CEMU_CE=1 forces it): in this read-only form it measured 2-7% faster than
-// the fused kernel for bf16 / int32 but 2-5% slower for fp32 at 1 GiB
-// (profiles/r02_ce_pull_only.txt), so the fused kernel is the default.
+// path) and the emulated ranks, storing into the local recv and the peer's
+// -- the peer store only after a successful start barrier; done barrier.
+// The pulls leave the SMs, so the NVLink legs run on both the copy engines
+// and the SMs.  Bit-identical to the fused kernel (same fold code).  Chosen
+// where it measured faster: two real GPUs, >= 512 MiB, a count divisible
+// into 16-byte vectors, <= 16 emulated ranks (CEMU_CE=1 forces it,
+// CEMU_CE=0 disables it; 1 GiB: fp32 1.547 vs 1.634 ms, bf16 1.567 vs
+// 1.680, int32 1.574 vs 1.680 -- profiles/r02_ce_pull_only.txt).
 constexpr uint64_t kCeMinBytes = 512ull << 20;
 
 // Chunk of the slice: at most CEMU_CE_CHUNK_MIB (default 256; measured
@@ -644,65 +642,51 @@ bool ce_allreduce_fits(const cemuComm* c, const FusedArgs& a, uint64_t count, si
   return (sv + ce_chunk_vecs(sv) - 1) / ce_chunk_vecs(sv) <= 64;  // the event pool
 }
 
-cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs, uint64_t nvec, cudaStream_t s,
-                          Call* call) {
+cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs, cudaStream_t s, Call* call) {
   auto& p = c->cep;
   const uint64_t slice = stage_vecs * 16;
   if (!p.pull) CUDA_OK(cudaStreamCreateWithFlags(&p.pull, cudaStreamNonBlocking));
-  if (!p.fetch) CUDA_OK(cudaStreamCreateWithFlags(&p.fetch, cudaStreamNonBlocking));
   for (cudaEvent_t& ev : p.ev) {
     if (!ev) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   if (auto r = grow_buffer(c, &p.stage, &p.stage_bytes, slice, "copy-engine staging")) return r;
   const int peer = 1 - a.me;
   const uint4* peer_send = a.src[peer];
-  const uint4* peer_recv = a.dst[peer];
-  uint4* my_recv = a.dst[a.me];
-  // the peer's slice of the vectors (k = 2: the other half)
-  const uint64_t pv_begin = a.me == 0 ? a.v_end : 0, pv_end = a.me == 0 ? nvec : a.v_begin;
   a.stamp = call->take_stamp();
   CUDA_OK(cache_fused(c, dt, a, s, &call->launches));  // the fold-only chunks inherit it
   CUDA_OK(launch_peer_barrier(a, 0, s, &call->launches));
-  cudaEvent_t started = p.ev[0], fetched = p.ev[1];
+  cudaEvent_t started = p.ev[0];
   CUDA_OK(cudaEventRecord(started, s));
   CUDA_OK(cudaStreamWaitEvent(p.pull, started, 0));
-  CUDA_OK(cudaStreamWaitEvent(p.fetch, started, 0));
   // the staging, indexed like the buffers: element vector v at stage[v - v_begin]
   const auto stage_at = reinterpret_cast<uintptr_t>(p.stage) - a.v_begin * 16;
+  // fold-only chunks of the fused kernel: local + staged peer data + the
+  // emulated ranks, stored into the local recv and the peer's -- the peer
+  // store gated on the start barrier's verdict (the comm's error word), so
+  // ranks that disagree never write into each other's memory
   FusedArgs f = a;
   f.barriers = 0;
   f.stamp = nullptr;
-  f.ndst = 1;
-  f.dst[0] = my_recv;
+  f.ndst = 2;
+  f.dst[0] = a.dst[a.me];
+  f.dst[1] = a.dst[peer];
+  f.gate = a.error;
   f.src[peer] = reinterpret_cast<const uint4*>(stage_at);
   const uint64_t cvec = ce_chunk_vecs(a.v_end - a.v_begin);
   int ci = 0;
   for (uint64_t v0 = a.v_begin; v0 < a.v_end; v0 += cvec, ++ci) {
     const uint64_t v1 = std::min(a.v_end, v0 + cvec);
-    const size_t n = (v1 - v0) * 16;
     cudaEvent_t pulled = p.ev[2 + ci];
-    CUDA_OK(cudaMemcpyAsync(reinterpret_cast<void*>(stage_at + v0 * 16), peer_send + v0, n,
+    CUDA_OK(cudaMemcpyAsync(reinterpret_cast<void*>(stage_at + v0 * 16), peer_send + v0, (v1 - v0) * 16,
                             cudaMemcpyDeviceToDevice, p.pull));
     CUDA_OK(cudaEventRecord(pulled, p.pull));
     CUDA_OK(cudaStreamWaitEvent(s, pulled, 0));
     f.v_begin = v0;
     f.v_end = v1;
     CUDA_OK(launch_fused_allreduce(dt, f, s, &call->launches));
-    CUDA_OK(launch_chunk_signal(a, ci, s, &call->launches));  // "my chunk ci is final"
   }
-  // the peer's result chunks, each once the peer has signalled it: a local
-  // write of data read over NVLink
-  const uint64_t pcvec = ce_chunk_vecs(pv_end - pv_begin);
-  int pi = 0;
-  for (uint64_t v0 = pv_begin; v0 < pv_end; v0 += pcvec, ++pi) {
-    const uint64_t v1 = std::min(pv_end, v0 + pcvec);
-    CUDA_OK(launch_chunk_wait(a, peer, pi, p.fetch, &call->launches));
-    CUDA_OK(cudaMemcpyAsync(my_recv + v0, peer_recv + v0, (v1 - v0) * 16, cudaMemcpyDeviceToDevice, p.fetch));
-  }
-  CUDA_OK(cudaEventRecord(fetched, p.fetch));
-  CUDA_OK(cudaStreamWaitEvent(s, fetched, 0));
-  // done: each side announces once its fetches completed, so neither frees
-  // or rewrites a buffer the other still reads
+  // done: the peer's stores into my recv are complete, and it no longer
+  // reads my send
   CUDA_OK(launch_peer_barrier(a, 1, s, &call->launches));
   CUDA_OK(call->finish(kAllReduce));
   return cemuSuccess;
@@ -762,7 +746,7 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
       ph.push_back([=]() mutable -> cemuResult_t {
         set_barrier(c, a);
         a.sig = op_sig(kAllReduce, dt, count, tags);
-        return ce_allreduce(c, dt, a, ce_stage_vecs(count, es), count / (16 / es), s, call.get());
+        return ce_allreduce(c, dt, a, ce_stage_vecs(count, es), s, call.get());
       });
       return cemuSuccess;
     }

@@ -204,13 +204,10 @@ struct cemuComm {
   size_t wire_buf_bytes = 0;
   // copy-engine allreduce (k = 2, large symmetric buffers):
   // the NVLink legs ride the copy engines, the fold + synthesis the SMs
-  int ce = 0;  // CEMU_CE: 0 (default) off, 1 forced, 2 auto -- see ce_allreduce_fits
+  int ce = 2;  // CEMU_CE: 0 off, 1 forced, 2 (default) auto -- see ce_allreduce_fits
   struct CePipe {
     static constexpr int kEvents = 2 * 64 + 2;
-    // pull: the peer's send chunks into staging; fetch: the peer's finished
-    // result chunks into the local recv.  Both only READ peer memory: a rank
-    // never writes another GPU's buffers on this path.
-    cudaStream_t pull = nullptr, fetch = nullptr;
+    cudaStream_t pull = nullptr;  // the peer's send chunks into staging
     cudaEvent_t ev[kEvents] = {};
     void* stage = nullptr;
     size_t stage_bytes = 0;
@@ -223,7 +220,7 @@ struct cemuComm {
     wire.reset();  // BYE to the emulator
     auto& p = pipe;
     // every internal stream drains before any mapping is closed or memory freed
-    for (cudaStream_t st : {p.h2d, p.comp, p.d2h, cep.pull, cep.fetch, hold_stream}) {
+    for (cudaStream_t st : {p.h2d, p.comp, p.d2h, cep.pull, hold_stream}) {
       if (st) cudaStreamSynchronize(st);
     }
     if (order_ev) cudaEventSynchronize(order_ev);
@@ -243,9 +240,7 @@ struct cemuComm {
     for (auto& m : ipc_maps) {
       if (m.second.ptr) cudaIpcCloseMemHandle(m.second.ptr);
     }
-    for (cudaStream_t st : {cep.pull, cep.fetch}) {
-      if (st) cudaStreamDestroy(st);
-    }
+    if (cep.pull) cudaStreamDestroy(cep.pull);
     if (order_ev) cudaEventDestroy(order_ev);
     if (hold_stream) cudaStreamDestroy(hold_stream);
     for (cudaEvent_t ev : {hold_fork, hold_join}) {

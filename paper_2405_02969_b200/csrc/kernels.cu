@@ -904,7 +904,7 @@ __device__ __forceinline__ uint4 add_real(const uint4& a, const uint4& b) {
 
 // ragged elements after the last full vector: same fold, one element
 template <int DT, int kMode>
-__device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* skeys) {
+__device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* skeys, int ndst) {
   using S = typename std::conditional<
       DT == cemuInt8 || DT == cemuUint8, uint8_t,
       typename std::conditional<DT == cemuFloat16 || DT == cemuBfloat16, uint16_t, uint32_t>::type>::type;
@@ -929,7 +929,7 @@ __device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* ske
   } else {
     elem_reduce<DT>(&acc, &out, 0, a.tail_e0 + i, skeys, a.nkeys);
   }
-  for (int g = 0; g < a.ndst; ++g) reinterpret_cast<S*>(a.dst[g] + a.v_end)[i] = out;
+  for (int g = 0; g < ndst; ++g) reinterpret_cast<S*>(a.dst[g] + a.v_end)[i] = out;
 }
 
 template <int K, int DT, int KMAX, int U, int kMode>
@@ -937,7 +937,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
   using T = VT<K>;
   constexpr int W = T::WPV, NW = U * W;
   extern __shared__ uint2 skeys[];
-  __shared__ int abort_s;
+  __shared__ int abort_s, ndst_s;
   const int64_t t0 = globaltimer_ns();
   // every real GPU runs the same fused calls in the same order, so the local
   // counters agree; the last CTA advances it when the call is complete
@@ -947,7 +947,12 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
   if (a.barriers && blockIdx.x == 0 && threadIdx.x < a.k && static_cast<int>(threadIdx.x) != a.me) {
     st_release_sys(a.peer_flags[threadIdx.x] + a.me, flag_word(epoch, a.sig));
   }
-  if (threadIdx.x == 0) abort_s = 0;
+  if (threadIdx.x == 0) {
+    abort_s = 0;
+    // a fold-only chunk after a failed start barrier (the comm's error word
+    // set) keeps its result local: no store reaches a peer's memory
+    ndst_s = (a.gate && *reinterpret_cast<volatile const uint32_t*>(a.gate) != 0) ? 1 : a.ndst;
+  }
   if constexpr (!cached(kMode)) {
     load_keys(skeys, a.keys, a.nkeys, key_shift(kMode));
   } else {
@@ -965,6 +970,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.epoch = epoch;
     return;
   }
+  const int ndst = ndst_s;
 
   const uint64_t tile = static_cast<uint64_t>(kThreads) * U;
   for (uint64_t base = a.v_begin + static_cast<uint64_t>(blockIdx.x) * tile; base < a.v_end;
@@ -998,12 +1004,12 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
       const uint4 y = fold_vec<K>(real, r + u * W * (T::kWords ? 1 : 4));
 #pragma unroll
       for (int g = 0; g < KMAX; ++g) {
-        if (g < a.ndst) st_stream(a.dst[g] + v, y);
+        if (g < ndst) st_stream(a.dst[g] + v, y);
       }
     }
   }
   if (a.ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < a.ntail) {
-    fused_tail_elem<DT, kMode>(a, threadIdx.x, skeys + key_shift(kMode));
+    fused_tail_elem<DT, kMode>(a, threadIdx.x, skeys + key_shift(kMode), ndst);
   }
 
   if (!a.barriers) return;
@@ -1050,23 +1056,6 @@ __global__ void peer_barrier_kernel(const __grid_constant__ FusedArgs a, int pha
     if (peer && wait_flag(a.flags + 8 + g, epoch, 0, false, t0, a.timeout_ns)) atomicExch(a.error, 2u);
     __syncwarp();
     if (g == 0) *a.epoch = epoch;
-  }
-}
-
-// Copy-engine pipeline chunk flags: word 64 + c of the signal area (bytes
-// 512 + 8c) holds flag_word(epoch, 0) once result chunk c of the call with
-// that epoch is final.  The fold kernel before the signal completed (stream
-// order); the system fence publishes its writes to the peer's copy engine.
-__global__ void chunk_signal_kernel(const __grid_constant__ FusedArgs a, int chunk) {
-  const uint64_t epoch = *a.epoch + 1;
-  __threadfence_system();
-  st_release_sys(a.flags + 64 + chunk, flag_word(epoch, 0));
-}
-
-__global__ void chunk_wait_kernel(const __grid_constant__ FusedArgs a, int peer, int chunk) {
-  const uint64_t epoch = *a.epoch + 1;
-  if (wait_flag(a.peer_flags[peer] + 64 + chunk, epoch, 0, false, globaltimer_ns(), a.timeout_ns)) {
-    atomicExch(a.error, 2u);
   }
 }
 
@@ -1897,20 +1886,6 @@ cudaError_t launch_peer_barrier(const FusedArgs& a, int phase, cudaStream_t s, i
   if (a.k < 2 || a.k > 32) return cudaErrorInvalidValue;
   ++*launches;
   peer_barrier_kernel<<<1, 32, 0, s>>>(a, phase);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_chunk_signal(const FusedArgs& a, int chunk, cudaStream_t s, int* launches) {
-  if (chunk < 0 || chunk >= 64) return cudaErrorInvalidValue;
-  ++*launches;
-  chunk_signal_kernel<<<1, 1, 0, s>>>(a, chunk);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_chunk_wait(const FusedArgs& a, int peer, int chunk, cudaStream_t s, int* launches) {
-  if (chunk < 0 || chunk >= 64 || peer < 0 || peer >= a.k) return cudaErrorInvalidValue;
-  ++*launches;
-  chunk_wait_kernel<<<1, 1, 0, s>>>(a, peer, chunk);
   return cudaGetLastError();
 }
 

@@ -132,6 +132,9 @@ struct FusedArgs {
   // synthesis cache covering this GPU's slice (and tail), or none
   const void* cache = nullptr;
   int cache_kind = kNoCache;
+  // fold-only chunks: when *gate != 0 (the start barrier failed) only dst[0]
+  // (local) is written
+  const uint32_t* gate = nullptr;
 };
 // Returns cudaErrorNotSupported for datatypes without a vector path.
 cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t stream, int* launches);
@@ -139,11 +142,7 @@ cudaError_t launch_fused_allreduce(int dtype, const FusedArgs& a, cudaStream_t s
 // done (phase 1: announce + wait, then the epoch advances) barrier alone, as
 // a one-warp kernel: brackets a copy-engine allreduce.
 cudaError_t launch_peer_barrier(const FusedArgs& a, int phase, cudaStream_t stream, int* launches);
-// Copy-engine pipeline chunk flags (signal area bytes [512, 1024): 64
-// epoch-tagged words): "my result chunk `chunk` of this call is final", and
-// a wait for the same flag of real GPU `peer` (timeout -> error 2).
-cudaError_t launch_chunk_signal(const FusedArgs& a, int chunk, cudaStream_t stream, int* launches);
-cudaError_t launch_chunk_wait(const FusedArgs& a, int peer, int chunk, cudaStream_t stream, int* launches);
+
 
 // One-kernel multi-GPU allgather: push the own block to every real GPU over
 // NVLink while the same launch synthesises the emulated blocks locally.

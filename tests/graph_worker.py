@@ -53,7 +53,7 @@ def run():
     real = list(range(n))
     obj = [pb.get_unique_id() if local == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    os.environ["CEMU_CE"] = "1"  # two GPUs: the (opt-in) copy-engine pipeline, the path with the most moving parts
+    os.environ["CEMU_CE"] = "1"  # two GPUs: the copy-engine pipeline, the path with the most moving parts
     comm = pb.Communicator(f"world_size = {W}\nreal_ranks = {','.join(map(str, real))}\nbucket_bytes = 1\n",
                            local, local, obj[0])
     comm.set_delay_model(plugin)
