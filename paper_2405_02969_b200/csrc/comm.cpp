@@ -244,27 +244,6 @@ bool capturing(cudaStream_t s) {
 
 // ---- synthesis cache ----------------------------------------------------
 namespace {
-bool covered(const cemuComm::SynthCache& sc, uint64_t b, uint64_t e) {
-  for (const auto& r : sc.covered) {
-    if (r.first <= b && e <= r.second) return true;
-  }
-  return false;
-}
-
-void cover(cemuComm::SynthCache& sc, uint64_t b, uint64_t e) {
-  sc.covered.emplace_back(b, e);
-  std::sort(sc.covered.begin(), sc.covered.end());
-  std::vector<std::pair<uint64_t, uint64_t>> m;
-  for (const auto& r : sc.covered) {
-    if (!m.empty() && r.first <= m.back().second) {
-      m.back().second = std::max(m.back().second, r.second);
-    } else {
-      m.push_back(r);
-    }
-  }
-  sc.covered.swap(m);
-}
-
 bool cacheable_dtype(int dt) {
   return dt == cemuFloat32 || dt == cemuBfloat16 || dt == cemuFloat16 || dt == cemuUint8 || dt == cemuInt8 ||
          dt == cemuInt32 || dt == cemuUint32;
@@ -287,33 +266,45 @@ CacheRef cache_for(cemuComm* c, int dt, uint64_t b, uint64_t e, cudaStream_t s, 
   const bool words = dt == cemuInt32 || dt == cemuUint32;
   auto& sc = words ? c->cache_words : c->cache_bytes;
   if (sc.kind == kNoCache) sc.kind = (words || c->virt.size() > 256) ? kCacheWide32 : kCacheLanes16;
+  const size_t entry = cache_entry_bytes(sc.kind);
   const uint64_t end = words ? e : (e + 3) / 4 * 4;  // the fill writes whole payload words
-  const size_t need = end * cache_entry_bytes(sc.kind);
-  if (need > c->cache_cap) return {};
+  // entry 0 of the returned pointer is element 0's: a segment's base moved
+  // back by its first element (only indices inside the segment are read)
+  auto ref = [&](const cemuComm::SynthCache::Segment& g) {
+    return CacheRef{reinterpret_cast<void*>(reinterpret_cast<uintptr_t>(g.ptr) - g.b * entry), sc.kind};
+  };
   const bool cap = capturing(s);
-  if (covered(sc, b, e) && sc.bytes >= need) {
-    ++c->cache_hits;
-    return CacheRef{sc.ptr, sc.kind};
-  }
-  if (cap) return {};  // no allocation and no fill inside a capture: synthesise
-  if (sc.bytes < need) {
-    // grow (64 MiB steps, within the cap); the old entries are dropped
-    const size_t step = 64ull << 20;
-    const size_t want = std::min(c->cache_cap, (need + step - 1) / step * step);
-    void* p = nullptr;
-    if (cudaMalloc(&p, want) != cudaSuccess) {
-      cudaGetLastError();
-      return {};
+  for (auto& g : sc.segs) {
+    if (g.b <= b && end <= g.e) {  // written by an earlier call, which every later call is ordered after
+      g.captured |= cap;
+      ++c->cache_hits;
+      return ref(g);
     }
-    if (sc.ptr) c->retired.push_back(sc.ptr);  // an enqueued or captured call may still read it
-    sc.ptr = p;
-    sc.bytes = want;
-    sc.covered.clear();
   }
-  cover(sc, b, e);  // every later call of this comm is ordered after this one's fill
+  // a new segment holding exactly this range's entries
+  const size_t need = (end - b) * entry;
+  if (cap || sc.bytes + need > c->cache_cap) return {};  // no allocation / fill in a capture
+  void* p = nullptr;
+  size_t have = need;
+  // a dropped segment no captured graph reads is free once the calls before
+  // this one are done -- and this call is ordered after all of them
+  auto best = sc.spare.end();
+  for (auto it = sc.spare.begin(); it != sc.spare.end(); ++it) {
+    if (it->second >= need && (best == sc.spare.end() || it->second < best->second)) best = it;
+  }
+  if (best != sc.spare.end()) {
+    p = best->first;
+    have = best->second;
+    sc.spare.erase(best);
+  } else if (cudaMalloc(&p, need) != cudaSuccess) {
+    cudaGetLastError();
+    return {};
+  }
+  sc.segs.push_back({b, end, p, have, false});
+  sc.bytes += have;
   ++c->cache_fills;
   *fill = true;
-  return CacheRef{sc.ptr, sc.kind};
+  return ref(sc.segs.back());
 }
 }  // namespace
 
@@ -1485,11 +1476,19 @@ cemuResult_t cemuCommSetSynthCache(cemuComm_t c, size_t cap, uint32_t min_peers)
   c->cache_cap = cap;
   c->cache_min_peers = min_peers;
   for (auto* sc : {&c->cache_bytes, &c->cache_words}) {
-    sc->covered.clear();  // buffers stay (an enqueued call may read them); entries are refilled
-    if (sc->bytes > cap && sc->ptr) {
-      c->retired.push_back(sc->ptr);
-      sc->ptr = nullptr;
-      sc->bytes = 0;
+    for (const auto& g : sc->segs) {
+      if (g.captured) {
+        c->retired.push_back(g.ptr);  // a captured graph may still read it
+      } else {
+        sc->spare.emplace_back(g.ptr, g.bytes);  // reusable by a later fill (calls are ordered)
+      }
+    }
+    sc->segs.clear();
+    sc->bytes = 0;
+    if (cap == 0) {  // caching off: give the memory back once the calls that may read it are done
+      if (c->order_ev) cudaEventSynchronize(c->order_ev);
+      for (const auto& g : sc->spare) cudaFree(g.first);
+      sc->spare.clear();
     }
   }
   return cemuSuccess;

@@ -162,17 +162,24 @@ struct cemuComm {
   // first waits for it.  Fused multi-GPU kernels spin on peer flags, so two
   // of them in flight at once would share the signal area's epoch and CTA
   // counter -- and could deadlock on SM occupancy -- without this.
-  // Synthesis cache (kernels.hpp CacheRef; DESIGN §4): the emulated
+  // Synthesis cache (kernels.hpp CacheRef; DESIGN §4b): the emulated
   // peers' per-element sums, written by the first call over an element
-  // range and folded from by every later call over it.  One cache for the
+  // range and folded from by every later call within it.  One cache for the
   // byte kinds (u8/i8/fp16/bf16/fp32 share byte_r(e)), one for the 32-bit
-  // integer kinds.  Buffers only grow (the old one is retired, its coverage
-  // dropped); nothing is filled inside a stream capture.
+  // integer kinds; each a list of segments sized to exactly the ranges seen
+  // (a reduce-scatter chunk at a high rank costs its own size, not its
+  // offset).  Nothing is allocated or filled inside a stream capture.
   struct SynthCache {
-    void* ptr = nullptr;
+    struct Segment {
+      uint64_t b, e;  // element range [b, e) whose entries it holds
+      void* ptr;
+      size_t bytes;
+      bool captured;  // a captured graph reads it: never reused, only retired
+    };
+    std::vector<Segment> segs;
+    std::vector<std::pair<void*, size_t>> spare;  // dropped, never-captured segments: reusable
     size_t bytes = 0;
     int kind = kNoCache;
-    std::vector<std::pair<uint64_t, uint64_t>> covered;  // element ranges with entries: sorted, disjoint
   };
   SynthCache cache_bytes, cache_words;
   size_t cache_cap = 0;           // bytes per cache (CEMU_SYNTH_CACHE_MB; 0 = off)
@@ -247,8 +254,10 @@ struct cemuComm {
       if (ev) cudaEventDestroy(ev);
     }
     for (void* r : retired) cudaFree(r);
-    cudaFree(cache_bytes.ptr);
-    cudaFree(cache_words.ptr);
+    for (const auto* sc : {&cache_bytes, &cache_words}) {
+      for (const auto& g : sc->segs) cudaFree(g.ptr);
+      for (const auto& g : sc->spare) cudaFree(g.first);
+    }
     for (cudaEvent_t ev : cep.ev) {
       if (ev) cudaEventDestroy(ev);
     }
