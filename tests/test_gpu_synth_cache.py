@@ -44,7 +44,8 @@ def test_cached_allreduce_equals_oracle_on_fill_and_hits(cuda, W, dt):
     st = comm.synth_cache_stats()
     assert st["fills"] == 1 and st["hits"] == 2, st
     entry = 4 if (dt == 2 or W > 257) else 2
-    assert st["bytes"] >= ((count + 3) // 4 * 4) * entry
+    entries = count if dt == 2 else (count + 3) // 4 * 4  # byte kinds: whole payload words
+    assert st["bytes"] == entries * entry  # one segment, exactly the range's entries
     comm.close()
 
 
