@@ -626,7 +626,14 @@ uint64_t ce_stage_vecs(uint64_t count, size_t es) { return (count / (16 / es) + 
 bool ce_allreduce_fits(const cemuComm* c, const FusedArgs& a, uint64_t count, size_t es, cudaStream_t s) {
   const uint64_t bytes = count * es;
   if (!c->ce || c->k != 2 || bytes < kCeMinBytes || count % (16 / es) != 0) return false;
-  if (c->ce == 2 && c->virt.size() > kCeMaxAutoPeers) return false;
+  // many emulated ranks: only while the synthesis cache serves the folds
+  // (synthesised folds are issue-bound and the pipeline serialises around
+  // them; cached ones are memory-bound: 1 GiB at worlds 32-128, 1.53 vs
+  // 1.63 ms fused -- profiles/r02_ce_pull_only.txt)
+  if (c->ce == 2 && c->virt.size() > kCeMaxAutoPeers &&
+      !(c->cache_cap > 0 && c->virt.size() >= c->cache_min_peers)) {
+    return false;
+  }
   const uint64_t sv = ce_stage_vecs(count, es);
   if (c->cep.stage_bytes < sv * 16 && capturing(s)) return false;
   (void)a;
