@@ -112,7 +112,7 @@ def safety(cfg, rank):
         comm.close()
     res["offset_ce_equals_fused"] = bool(torch.equal(outs[("1", count)][0], outs[("0", count)][0]))
     res["offset_ce_took_pipeline"] = outs[("1", count)][1] > 2
-    res["ragged_took_fused_kernel"] = outs[("1", count + 3)][1] == 1
+    res["ragged_took_fused_kernel"] = outs[("1", count + 3)][1] <= 2  # (+ a synthesis-cache fill)
     res["ragged_equals_fused"] = bool(torch.equal(outs[("1", count + 3)][0], outs[("0", count + 3)][0]))
     res["guards_intact"] = all(v[2] for v in outs.values())
     res["no_async_errors"] = all(v[3] is None for v in outs.values())

@@ -42,16 +42,20 @@ def test_multi_gpu_collectives_match_oracle(kmax):
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
-def test_copy_engine_allreduce_equals_the_fused_kernel():
+@pytest.mark.parametrize("cache", ["default", "forced"])
+def test_copy_engine_allreduce_equals_the_fused_kernel(cache):
     """Two real GPUs, >= 512 MiB: the copy-engine pipeline (default there)
     is bit-identical to the fused kernel (CEMU_CE=0) -- itself pinned to the
     oracle by mgpu_worker.py -- on arbitrary fp32 / bf16 / int32, out of
     place and in place (tests/ce_check.py)."""
     import json
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ce_check.py")
+    # "forced": both paths fold from the synthesis cache (the pipeline's
+    # default at many emulated ranks)
+    env = dict(os.environ, **({"CEMU_SYNTH_CACHE_MIN_PEERS": "1"} if cache == "forced" else {}))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                         "--master-addr", "127.0.0.1", "--master-port", str(_port()), worker],
-                       capture_output=True, text=True, timeout=420)
+                       capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     import re
     lines = [json.loads(m) for m in re.findall(r"\{\"k\".*?\"safety\": \{[^}]*\}\}", r.stdout)]
@@ -59,7 +63,7 @@ def test_copy_engine_allreduce_equals_the_fused_kernel():
     for res in lines:
         for case in res["cases"]:
             assert case["equal"] and case["equal_in_place"], case
-            assert case["ce_launches"] > case["fused_launches"] == 1  # the pipeline really ran
+            assert case["ce_launches"] > case["fused_launches"] >= 1  # the pipeline really ran
             assert case["errors"] == [None, None], case
         # offsets / ragged counts / guard bands, and disagreeing ranks:
         # reported on both, neither writes the other's memory
