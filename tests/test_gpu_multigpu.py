@@ -154,3 +154,28 @@ def test_graph_capture_of_copy_engine_allreduce_with_plugin_delay():
         for rep in res["replays"]:
             assert rep["equal_eager"] and rep["equal_oracle_1Mi"] and rep["floors_ok"], rep
             assert abs(rep["delay_us"] - 3000) <= 30 and rep["overshoot_us"] < 2, rep
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_random_mixed_collectives_on_two_streams():
+    """tests/soak_worker.py: a random mix of registered / cemuMemAlloc /
+    plain-buffer allreduces (fused, copy-engine and NCCL paths),
+    reduce-scatters, all-gathers and emulated-root broadcasts over one
+    communicator, each on one of two streams, the synthesis cache on: every
+    result equals its oracle result bit for bit."""
+    import json
+    import re
+    n = min(torch.cuda.device_count(), 4)
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "soak_worker.py")
+    env = dict(os.environ, SOAK_ITERS="400")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()), worker],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [json.loads(m) for m in re.findall(r"SOAK (\{.*?\"cache\": \{[^}]*\}\})", r.stdout)]
+    assert len(lines) == n, r.stdout[-2000:]
+    for res in lines:
+        assert all(v == 0 for v in res["bad"].values()), res
+        assert res["async_error"] is None, res
+        assert sum(res["calls"].values()) == 400 and res["cache"]["hits"] > 0, res
