@@ -617,7 +617,13 @@ constexpr size_t kCeMaxAutoPeers = 16;
 
 // The larger of the two slices: every rank sizes its staging alike, so the
 // capture-time check below agrees across ranks.
-uint64_t ce_stage_vecs(uint64_t count, size_t es) { return (count / (16 / es) + 1) / 2; }
+// The largest rank's slice (the last rank's: the ragged remainder) in
+// 16-byte vectors: every rank sizes its per-peer staging alike, so the
+// capture-time check below agrees across ranks.
+uint64_t ce_stage_vecs(uint64_t count, size_t es, uint32_t k) {
+  const uint64_t nvec = count / (16 / es);
+  return nvec - nvec / k * (k - 1);
+}
 
 // Every real rank must take the same decision (they meet in the barriers),
 // so it only looks at symmetric quantities: the count's ragged tail, not
@@ -625,7 +631,8 @@ uint64_t ce_stage_vecs(uint64_t count, size_t es) { return (count / (16 / es) + 
 // grow (no allocation there), so such a call stays on the fused kernel.
 bool ce_allreduce_fits(const cemuComm* c, const FusedArgs& a, uint64_t count, size_t es, cudaStream_t s) {
   const uint64_t bytes = count * es;
-  if (!c->ce || c->k != 2 || bytes < kCeMinBytes || count % (16 / es) != 0) return false;
+  if (!c->ce || c->k < 2 || bytes < kCeMinBytes || count % (16 / es) != 0) return false;
+  if (c->ce == 2 && c->k != 2) return false;  // measured faster at two GPUs; CEMU_CE=1 forces it at k > 2
   // many emulated ranks: only while the synthesis cache serves the folds
   // (synthesised folds are issue-bound and the pipeline serialises around
   // them; cached ones are memory-bound: 1 GiB at worlds 32-128, 1.53 vs
@@ -634,57 +641,64 @@ bool ce_allreduce_fits(const cemuComm* c, const FusedArgs& a, uint64_t count, si
       !(c->cache_cap > 0 && c->virt.size() >= c->cache_min_peers)) {
     return false;
   }
-  const uint64_t sv = ce_stage_vecs(count, es);
-  if (c->cep.stage_bytes < sv * 16 && capturing(s)) return false;
+  const uint64_t sv = ce_stage_vecs(count, es, c->k);
+  if (c->cep.stage_bytes < (c->k - 1) * sv * 16 && capturing(s)) return false;
   (void)a;
-  return (sv + ce_chunk_vecs(sv) - 1) / ce_chunk_vecs(sv) <= 64;  // the event pool
+  const uint64_t chunks = (sv + ce_chunk_vecs(sv) - 1) / ce_chunk_vecs(sv);
+  return chunks * (c->k - 1) <= cemuComm::CePipe::kEvents - 2;  // the event pool
 }
 
 cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs, cudaStream_t s, Call* call) {
   auto& p = c->cep;
-  const uint64_t slice = stage_vecs * 16;
-  if (!p.pull) CUDA_OK(cudaStreamCreateWithFlags(&p.pull, cudaStreamNonBlocking));
+  const uint32_t k = c->k;
+  const uint64_t slice = stage_vecs * 16;  // per peer
+  for (uint32_t g = 0; g < k; ++g) {
+    if (g != c->li && !p.pull[g]) CUDA_OK(cudaStreamCreateWithFlags(&p.pull[g], cudaStreamNonBlocking));
+  }
   for (cudaEvent_t& ev : p.ev) {
     if (!ev) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
-  if (auto r = grow_buffer(c, &p.stage, &p.stage_bytes, slice, "copy-engine staging")) return r;
-  const int peer = 1 - a.me;
-  const uint4* peer_send = a.src[peer];
+  if (auto r = grow_buffer(c, &p.stage, &p.stage_bytes, (k - 1) * slice, "copy-engine staging")) return r;
   a.stamp = call->take_stamp();
   CUDA_OK(cache_fused(c, dt, a, s, &call->launches));  // the fold-only chunks inherit it
   CUDA_OK(launch_peer_barrier(a, 0, s, &call->launches));
   cudaEvent_t started = p.ev[0];
   CUDA_OK(cudaEventRecord(started, s));
-  CUDA_OK(cudaStreamWaitEvent(p.pull, started, 0));
-  // the staging, indexed like the buffers: element vector v at stage[v - v_begin]
-  const auto stage_at = reinterpret_cast<uintptr_t>(p.stage) - a.v_begin * 16;
-  // fold-only chunks of the fused kernel: local + staged peer data + the
-  // emulated ranks, stored into the local recv and the peer's -- the peer
-  // store gated on the start barrier's verdict (the comm's error word), so
+  // fold-only chunks of the fused kernel: local + every peer's staged data
+  // + the emulated ranks, stored into every real GPU's recv -- the peer
+  // stores gated on the start barrier's verdict (the comm's error word), so
   // ranks that disagree never write into each other's memory
   FusedArgs f = a;
   f.barriers = 0;
   f.stamp = nullptr;
-  f.ndst = 2;
-  f.dst[0] = a.dst[a.me];
-  f.dst[1] = a.dst[peer];
+  f.ndst = static_cast<int>(k);
   f.gate = a.error;
-  f.src[peer] = reinterpret_cast<const uint4*>(stage_at);
+  uintptr_t stage_at[kMaxReal] = {};
+  for (uint32_t g = 0, slot = 0; g < k; ++g) {
+    if (g == c->li) continue;
+    CUDA_OK(cudaStreamWaitEvent(p.pull[g], started, 0));
+    // peer g's staging, indexed like the buffers: vector v at stage[v - v_begin]
+    stage_at[g] = reinterpret_cast<uintptr_t>(p.stage) + slot++ * slice - a.v_begin * 16;
+    f.src[g] = reinterpret_cast<const uint4*>(stage_at[g]);
+  }
   const uint64_t cvec = ce_chunk_vecs(a.v_end - a.v_begin);
-  int ci = 0;
-  for (uint64_t v0 = a.v_begin; v0 < a.v_end; v0 += cvec, ++ci) {
+  int ev = 2;
+  for (uint64_t v0 = a.v_begin; v0 < a.v_end; v0 += cvec) {
     const uint64_t v1 = std::min(a.v_end, v0 + cvec);
-    cudaEvent_t pulled = p.ev[2 + ci];
-    CUDA_OK(cudaMemcpyAsync(reinterpret_cast<void*>(stage_at + v0 * 16), peer_send + v0, (v1 - v0) * 16,
-                            cudaMemcpyDeviceToDevice, p.pull));
-    CUDA_OK(cudaEventRecord(pulled, p.pull));
-    CUDA_OK(cudaStreamWaitEvent(s, pulled, 0));
+    for (uint32_t g = 0; g < k; ++g) {  // every peer's chunk on its own copy stream
+      if (g == c->li) continue;
+      cudaEvent_t pulled = p.ev[ev++];
+      CUDA_OK(cudaMemcpyAsync(reinterpret_cast<void*>(stage_at[g] + v0 * 16), a.src[g] + v0, (v1 - v0) * 16,
+                              cudaMemcpyDeviceToDevice, p.pull[g]));
+      CUDA_OK(cudaEventRecord(pulled, p.pull[g]));
+      CUDA_OK(cudaStreamWaitEvent(s, pulled, 0));
+    }
     f.v_begin = v0;
     f.v_end = v1;
     CUDA_OK(launch_fused_allreduce(dt, f, s, &call->launches));
   }
-  // done: the peer's stores into my recv are complete, and it no longer
-  // reads my send
+  // done: the peers' stores into my recv are complete, and they no longer
+  // read my send
   CUDA_OK(launch_peer_barrier(a, 1, s, &call->launches));
   CUDA_OK(call->finish(kAllReduce));
   return cemuSuccess;
@@ -744,7 +758,7 @@ cemuResult_t do_allreduce(const void* send, void* recv, size_t count, int dt, ce
       ph.push_back([=]() mutable -> cemuResult_t {
         set_barrier(c, a);
         a.sig = op_sig(kAllReduce, dt, count, tags);
-        return ce_allreduce(c, dt, a, ce_stage_vecs(count, es), s, call.get());
+        return ce_allreduce(c, dt, a, ce_stage_vecs(count, es, c->k), s, call.get());
       });
       return cemuSuccess;
     }

@@ -214,7 +214,7 @@ struct cemuComm {
   int ce = 2;  // CEMU_CE: 0 off, 1 forced, 2 (default) auto -- see ce_allreduce_fits
   struct CePipe {
     static constexpr int kEvents = 2 * 64 + 2;
-    cudaStream_t pull = nullptr;  // the peer's send chunks into staging
+    cudaStream_t pull[kMaxReal] = {};  // per peer: its send chunks into this GPU's staging
     cudaEvent_t ev[kEvents] = {};
     void* stage = nullptr;
     size_t stage_bytes = 0;
@@ -227,7 +227,10 @@ struct cemuComm {
     wire.reset();  // BYE to the emulator
     auto& p = pipe;
     // every internal stream drains before any mapping is closed or memory freed
-    for (cudaStream_t st : {p.h2d, p.comp, p.d2h, cep.pull, hold_stream}) {
+    for (cudaStream_t st : {p.h2d, p.comp, p.d2h, hold_stream}) {
+      if (st) cudaStreamSynchronize(st);
+    }
+    for (cudaStream_t st : cep.pull) {
       if (st) cudaStreamSynchronize(st);
     }
     if (order_ev) cudaEventSynchronize(order_ev);
@@ -247,7 +250,9 @@ struct cemuComm {
     for (auto& m : ipc_maps) {
       if (m.second.ptr) cudaIpcCloseMemHandle(m.second.ptr);
     }
-    if (cep.pull) cudaStreamDestroy(cep.pull);
+    for (cudaStream_t st : cep.pull) {
+      if (st) cudaStreamDestroy(st);
+    }
     if (order_ev) cudaEventDestroy(order_ev);
     if (hold_stream) cudaStreamDestroy(hold_stream);
     for (cudaEvent_t ev : {hold_fork, hold_join}) {
