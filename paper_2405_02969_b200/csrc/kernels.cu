@@ -929,6 +929,10 @@ __device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* ske
   } else {
     elem_reduce<DT>(&acc, &out, 0, a.tail_e0 + i, skeys, a.nkeys);
   }
+  if (ndst == 0) {  // gated: the local copy only
+    reinterpret_cast<S*>(a.dst[a.me] + a.v_end)[i] = out;
+    return;
+  }
   for (int g = 0; g < ndst; ++g) reinterpret_cast<S*>(a.dst[g] + a.v_end)[i] = out;
 }
 
@@ -950,8 +954,8 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
   if (threadIdx.x == 0) {
     abort_s = 0;
     // a fold-only chunk after a failed start barrier (the comm's error word
-    // set) keeps its result local: no store reaches a peer's memory
-    ndst_s = (a.gate && *reinterpret_cast<volatile const uint32_t*>(a.gate) != 0) ? 1 : a.ndst;
+    // set) keeps its result local (dst[me]): no store reaches a peer's memory
+    ndst_s = (a.gate && *reinterpret_cast<volatile const uint32_t*>(a.gate) != 0) ? 0 : a.ndst;
   }
   if constexpr (!cached(kMode)) {
     load_keys(skeys, a.keys, a.nkeys, key_shift(kMode));
@@ -1002,6 +1006,10 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
         if (g < a.k) real = add_real<K>(real, x[g][u]);
       }
       const uint4 y = fold_vec<K>(real, r + u * W * (T::kWords ? 1 : 4));
+      if (ndst == 0) {  // gated: the local copy only
+        st_stream(a.dst[a.me] + v, y);
+        continue;
+      }
 #pragma unroll
       for (int g = 0; g < KMAX; ++g) {
         if (g < ndst) st_stream(a.dst[g] + v, y);

@@ -132,8 +132,8 @@ struct FusedArgs {
   // synthesis cache covering this GPU's slice (and tail), or none
   const void* cache = nullptr;
   int cache_kind = kNoCache;
-  // fold-only chunks: when *gate != 0 (the start barrier failed) only dst[0]
-  // (local) is written
+  // fold-only chunks: when *gate != 0 (the start barrier failed) only
+  // dst[me] (local) is written
   const uint32_t* gate = nullptr;
 };
 // Returns cudaErrorNotSupported for datatypes without a vector path.
