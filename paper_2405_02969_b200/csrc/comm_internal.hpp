@@ -1,6 +1,8 @@
 // comm_internal.hpp -- what the communicator's translation units share
-// (comm.cpp: lifecycle, collective bodies, the C-ABI; host_pipe.cpp: the
-// host-buffer pipeline; comm_wire.cpp: wire mode).  Not part of the C-ABI.
+// (comm.cpp: lifecycle, collective bodies, the C-ABI; symmetric.cpp:
+// symmetric memory and registration; synth_cache.cpp: the synthesis cache;
+// host_pipe.cpp: the host-buffer pipeline; comm_wire.cpp: wire mode).  Not
+// part of the C-ABI.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -457,6 +459,11 @@ cemuResult_t map_peers(cemuComm* c, void* local, size_t bytes, uint8_t** peers, 
 // still maps this GPU's memory when the call returns).
 void unmap_region(cemuComm* c, cemuComm::Region& r);
 cemuResult_t ensure_scratch(cemuComm* c, size_t bytes);
+// True while `s` is being captured into a CUDA graph.
+bool capturing(cudaStream_t s);
+// All-gather `rec` (bytes each) among the k real GPUs over the inner NCCL
+// comm; synchronous -- setup and registration only (symmetric.cpp).
+cudaError_t exchange_records(cemuComm* c, const void* rec, size_t bytes, std::vector<uint8_t>* all, ncclResult_t* nr);
 // Grows *buf to >= bytes; the superseded buffer goes to c->retired.
 cemuResult_t grow_buffer(cemuComm* c, void** buf, size_t* have, size_t bytes, const char* what);
 // Call order across streams (see cemuComm::order_ev): before the call's
