@@ -482,7 +482,7 @@ def cache_block(torch, pb, device):
     out = {}
     S = 1 << 30
     for W, dname, dt in ((64, "fp32", torch.float32), (64, "bf16", torch.bfloat16), (128, "bf16", torch.bfloat16),
-                         (1024, "bf16", torch.bfloat16)):
+                         (1024, "bf16", torch.bfloat16), (1024, "fp32", torch.float32)):
         comm = pb.Communicator(f"world_size = {W}\nreal_ranks = 0\nbucket_bytes = 1\n", 0, device)
         es = torch.empty(0, dtype=dt).element_size()
         x = torch.randn(S // es, device=device).to(dt)
@@ -505,7 +505,7 @@ def cache_block(torch, pb, device):
         comm.set_synth_cache(4 << 30, 16)  # drops the entries, keeps the buffer
         fill = ms(1)
         warm = ms(10)
-        entry = 2 if W - 1 <= 256 else 4
+        entry = 2  # uint16 byte sums (<= 256 emulated ranks) or centred uint16 entries (<= 8192)
         traffic = 2 * S + (S // es) * entry
         out[f"world{W}_{dname}"] = {
             "ms_uncached": round(off, 4), "ms_fill": round(fill, 4), "ms_cached": round(warm, 4),

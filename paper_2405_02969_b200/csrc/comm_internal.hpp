@@ -177,6 +177,13 @@ struct cemuComm {
       void* ptr;
       size_t bytes;
       bool captured;  // a captured graph reads it: never reused, only retired
+      // centred entries (kCacheCentered16): the fill's escape count (mapped
+      // host memory), the event after the fill, and once that event has
+      // completed whether the range holds escapes (-1 = not known yet)
+      uint32_t* esc_h = nullptr;
+      uint32_t* esc_d = nullptr;
+      cudaEvent_t filled = nullptr;
+      int esc_state = -1;
     };
     std::vector<Segment> segs;
     std::vector<std::pair<void*, size_t>> spare;  // dropped, never-captured segments: reusable
@@ -184,6 +191,11 @@ struct cemuComm {
     int kind = kNoCache;
   };
   SynthCache cache_bytes, cache_words;
+  // escape counters of the centred segments: blocks of 1024 mapped pinned
+  // words, one word per segment ever created; and the segments' fill events
+  std::vector<uint32_t*> esc_blocks;
+  size_t esc_used = 0;
+  std::vector<cudaEvent_t> seg_events;
   size_t cache_cap = 0;           // bytes per cache (CEMU_SYNTH_CACHE_MB; 0 = off)
   uint32_t cache_min_peers = 16;  // CEMU_SYNTH_CACHE_MIN_PEERS
   uint64_t cache_fills = 0, cache_hits = 0;
@@ -261,6 +273,8 @@ struct cemuComm {
       if (ev) cudaEventDestroy(ev);
     }
     for (void* r : retired) cudaFree(r);
+    for (cudaEvent_t ev : seg_events) cudaEventDestroy(ev);
+    for (uint32_t* b : esc_blocks) cudaFreeHost(b);
     for (const auto* sc : {&cache_bytes, &cache_words}) {
       for (const auto& g : sc->segs) cudaFree(g.ptr);
       for (const auto& g : sc->spare) cudaFree(g.first);

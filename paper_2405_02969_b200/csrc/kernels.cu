@@ -160,17 +160,49 @@ __device__ void elem_reduce(const void* src, void* dst, uint64_t i, uint64_t e,
   }
 }
 
+// Exact byte sums t_b = sum over the peers of byte b of payload word j, from
+// the raw keys in global memory: a centred cache entry's escape (kernels.hpp
+// kCacheCentered16) -- rare by construction, so it stays out of line.
+__device__ __noinline__ uint4 exact_byte_sums(const uint32_t* __restrict__ keys, uint32_t nkeys, uint64_t j) {
+  const uint32_t c1 = payload_c1(j);
+  uint4 t = make_uint4(0, 0, 0, 0);
+  for (uint32_t q = 0; q < nkeys; ++q) {
+    const uint32_t key = keys[q];
+    const uint32_t w = payload_mix(payload_k1(key), payload_km(key), c1);
+    t.x += w & 0xFFu;
+    t.y += (w >> 8) & 0xFFu;
+    t.z += (w >> 16) & 0xFFu;
+    t.w += w >> 24;
+  }
+  return t;
+}
+
 // elem_reduce from the synthesis cache: t = the peers' byte sum (or word
 // sum) of element e, so s = t - 128 n is elem_reduce's dyadic sum exactly.
+// `kind` is the cache's CacheKind; `keys` (global) serve centred escapes.
 template <int DT>
-__device__ void elem_fold_cached(const void* src, void* dst, uint64_t i, uint64_t e, const void* cache, bool wide,
-                                 uint32_t nkeys) {
+__device__ void elem_fold_cached(const void* src, void* dst, uint64_t i, uint64_t e, const void* cache, int kind,
+                                 uint32_t nkeys, const uint32_t* keys) {
   if constexpr (DT == cemuInt32 || DT == cemuUint32) {
     static_cast<uint32_t*>(dst)[i] = static_cast<const uint32_t*>(src)[i] + static_cast<const uint32_t*>(cache)[e];
   } else if constexpr (DT == cemuInt64 || DT == cemuUint64 || DT == cemuFloat64) {
     __trap();  // never cached (scalar path only)
   } else {
-    const uint32_t t = wide ? static_cast<const uint32_t*>(cache)[e] : static_cast<const uint16_t*>(cache)[e];
+    uint32_t t;
+    if (kind == kCacheWide32) {
+      t = static_cast<const uint32_t*>(cache)[e];
+    } else {
+      t = static_cast<const uint16_t*>(cache)[e];
+      if (kind == kCacheCentered16) {
+        if (t == 0) {
+          const uint4 x = exact_byte_sums(keys, nkeys, e >> 2);
+          const uint32_t b = static_cast<uint32_t>(e & 3);
+          t = b == 0 ? x.x : (b == 1 ? x.y : (b == 2 ? x.z : x.w));
+        } else {
+          t += c16_offset(nkeys);
+        }
+      }
+    }
     if constexpr (DT == cemuInt8 || DT == cemuUint8) {
       static_cast<uint8_t*>(dst)[i] = static_cast<uint8_t>(static_cast<const uint8_t*>(src)[i] + t);
     } else {
@@ -230,9 +262,16 @@ __device__ __forceinline__ void load_keys(uint2* skeys, const uint32_t* keys, ui
 //            cache (synth_cache_fill wrote them; see "synthesis cache" below)
 //   kCache32 the same with uint32 entries: byte sums of > 256 peers, or the
 //            wrapping word sums of the 32-bit integer kinds
-enum PeerMode { kSeed1 = 0, kSeed2 = 1, kGroups = 2, kCache16 = 3, kCache32 = 4 };
+//   kCacheC16 the same with centred uint16 entries (257..8192 peers; an
+//            entry 0 is an escape recomputed from the keys, kernels.hpp)
+//   kCacheC16F centred entries of a range known to hold no escape (its fill
+//            counted none): the kCache16 fold with the centred constants
+enum PeerMode { kSeed1 = 0, kSeed2 = 1, kGroups = 2, kCache16 = 3, kCache32 = 4, kCacheC16 = 5, kCacheC16F = 6 };
 __host__ __device__ constexpr uint32_t key_shift(int mode) { return mode == kSeed1 ? 1u : 0u; }
 __host__ __device__ constexpr bool cached(int mode) { return mode >= kCache16; }
+__host__ __device__ constexpr int cache_kind_of(int mode) {
+  return mode == kCache16 ? kCacheLanes16 : (mode == kCacheC16 || mode == kCacheC16F ? kCacheCentered16 : kCacheWide32);
+}
 inline int peer_mode(bool words, uint32_t nkeys) {
   if (!words && nkeys > 256) return kGroups;  // 16-bit lanes hold <= 257 bytes
   return (nkeys & 1) ? kSeed1 : kSeed2;
@@ -368,12 +407,18 @@ __device__ __forceinline__ void ah_to_lanes(uint32_t a, uint32_t h, uint32_t n, 
 // The same lanes from cached byte sums: t16 = the word's four uint16 lane
 // sums packed as (t0 | t1 << 16, t2 | t3 << 16) -- exactly the values
 // ah_to_lanes decodes from (A, H), so the result is bit-identical.
-template <int K>
+// kC: centred entries u = t - c16_offset(n): t - 128 n = u - (32768 +
+// ceil(n / 2)), so the magic's constant moves by (32768 + ceil(n/2)) * 2^-7
+// -- still exact (<= 98560 + 112 in the same binade); bytes add the offset's
+// low byte back.
+template <int K, bool kC = false>
 __device__ __forceinline__ void t16_to_lanes(uint32_t w01, uint32_t w23, uint32_t n, uint32_t* r) {
   if constexpr (K == kU8) {
     r[0] = __byte_perm(w01, w23, 0x6420);  // low byte of each lane sum
+    if constexpr (kC) r[0] = add_bytes(r[0], (c16_offset(n) & 0xFFu) * 0x01010101u);
   } else {
-    const float c = -(98304.0f + static_cast<float>(n));
+    const float c = kC ? -(98560.0f + static_cast<float>((n + 1) / 2) * kDyadicScale)
+                       : -(98304.0f + static_cast<float>(n));
     const float2 d01 = add_f32x2(lane_float(w01, 0x7610), lane_float(w01, 0x7632), c, c);
     const float2 d23 = add_f32x2(lane_float(w23, 0x7610), lane_float(w23, 0x7632), c, c);
     r[0] = __float_as_uint(d01.x);
@@ -382,6 +427,9 @@ __device__ __forceinline__ void t16_to_lanes(uint32_t w01, uint32_t w23, uint32_
     r[3] = __float_as_uint(d23.y);
   }
 }
+
+// nonzero iff some 16-bit lane of x is 0 (a centred entry's escape)
+__device__ __forceinline__ uint32_t zero_lane16(uint32_t x) { return (x - 0x00010001u) & ~x & 0x80008000u; }
 
 // ... and from uint32 byte sums T_e (> 256 peers): the kGroups flush below
 // computes the same integers (sum over groups of t - 128 * group size).
@@ -410,9 +458,39 @@ __device__ __forceinline__ void t32_to_lanes(const uint4& t, uint32_t n, uint32_
 template <int K, int U, int kMode, bool kEnt = false>
 __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skeys, uint32_t nkeys,
                                           uint32_t one, uint32_t* r, const void* cache = nullptr,
-                                          uint64_t j0 = 0, uint32_t* ent = nullptr) {
+                                          uint64_t j0 = 0, uint32_t* ent = nullptr,
+                                          const uint32_t* gkeys = nullptr) {
   using T = VT<K>;
   constexpr int NW = U * T::WPV;
+  if constexpr (kMode == kCacheC16) {
+    // centred entries: every load of the tile first (an escape test between
+    // two loads would serialise them), then decode; escapes out of line
+    constexpr int W = T::WPV;
+    uint2 c[U * W];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const uint64_t j = j0 + static_cast<uint64_t>(u) * kThreads * W + w;
+        c[u * W + w] = ld_stream64(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(cache) + 4 * j));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < U * W; ++i) t16_to_lanes<K, true>(c[i].x, c[i].y, nkeys, r + 4 * i);
+    uint32_t esc = 0;
+#pragma unroll
+    for (int i = 0; i < U * W; ++i) esc |= zero_lane16(c[i].x) | zero_lane16(c[i].y);
+    if (esc) {  // (unrolled: r stays in registers)
+#pragma unroll
+      for (int i = 0; i < U * W; ++i) {
+        if (zero_lane16(c[i].x) | zero_lane16(c[i].y)) {
+          const uint64_t j = j0 + static_cast<uint64_t>(i / W) * kThreads * W + (i % W);
+          t32_to_lanes<K>(exact_byte_sums(gkeys, nkeys, j), nkeys, r + 4 * i);
+        }
+      }
+    }
+    return;
+  }
   if constexpr (cached(kMode)) {
     constexpr int W = T::WPV;
 #pragma unroll
@@ -424,11 +502,11 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
         r[u * 4 + 1] = c.y;
         r[u * 4 + 2] = c.z;
         r[u * 4 + 3] = c.w;
-      } else if constexpr (kMode == kCache16) {
+      } else if constexpr (kMode == kCache16 || kMode == kCacheC16F) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {
           const uint2 c = ld_stream64(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(cache) + 4 * (jv + w)));
-          t16_to_lanes<K>(c.x, c.y, nkeys, r + 4 * (u * W + w));
+          t16_to_lanes<K, kMode == kCacheC16F>(c.x, c.y, nkeys, r + 4 * (u * W + w));
         }
       } else {
 #pragma unroll
@@ -633,7 +711,7 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     // 3. fold + stream out
     uint32_t r[T::kWords ? NW : NW * 4];
     uint32_t ent[kFill ? (T::kWords ? NW : 2 * NW) : 1];
-    peer_sums<K, U, kMode, kFill>(ctr, skeys, nkeys, one, r, cache, j0, ent);
+    peer_sums<K, U, kMode, kFill>(ctr, skeys, nkeys, one, r, cache, j0, ent, keys);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
@@ -658,7 +736,8 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
   // ragged tail (< one vector): the last block's first threads
   if (ntail && blockIdx.x == gridDim.x - 1 && threadIdx.x < ntail) {
     if constexpr (cached(kMode)) {
-      elem_fold_cached<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, cache, kMode == kCache32, nkeys);
+      elem_fold_cached<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, cache, cache_kind_of(kMode),
+                           nkeys, keys);
     } else {
       elem_reduce<DT>(tail_src, tail_dst, threadIdx.x, tail_e0 + threadIdx.x, skeys + key_shift(kMode), nkeys);
     }
@@ -744,10 +823,12 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_split(
 //   kEntry 0: uint16 lane sums t0..t3 of each word, packed (t0|t1<<16, t2|t3<<16)
 //          1: uint32 byte sums (> 256 peers: 256-peer groups, summed exactly)
 //          2: uint32 wrapping word sums (32-bit integer kinds; word = element)
+//          3: centred uint16 byte sums, packed as 0 (257..8192 peers: t as in
+//             1, then u = t - c16_offset(n) or the escape 0, kernels.hpp)
 template <int U, int kEntry>
 __global__ void __launch_bounds__(kThreads) synth_cache_fill(uint64_t word_begin, uint64_t word_end,
                                                              const uint32_t* __restrict__ keys, uint32_t nkeys,
-                                                             void* cache, uint32_t one) {
+                                                             void* cache, uint32_t one, uint32_t* esc) {
   constexpr int W = 4, NW = U * W;
   extern __shared__ uint2 skeys[];
   load_keys(skeys, keys, nkeys);
@@ -771,7 +852,7 @@ __global__ void __launch_bounds__(kThreads) synth_cache_fill(uint64_t word_begin
       if (word_of(i) < word_end) out[word_of(i)] = sum[i];
     }
   } else {
-    constexpr bool kWide = kEntry == 1;
+    constexpr bool kWide = kEntry == 1 || kEntry == 3;
     uint32_t tw[kWide ? NW * 4 : NW * 2];
     if constexpr (kWide) {
 #pragma unroll
@@ -807,16 +888,30 @@ __global__ void __launch_bounds__(kThreads) synth_cache_fill(uint64_t word_begin
         }
       }
     }
+    uint32_t nesc = 0;
 #pragma unroll
     for (int i = 0; i < NW; ++i) {
       const uint64_t j = word_of(i);
       if (j >= word_end) continue;
-      if constexpr (kWide) {
+      if constexpr (kEntry == 3) {
+        const uint32_t off = c16_offset(nkeys);
+        uint32_t u[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          u[e] = tw[4 * i + e] - off;
+          if (u[e] - 1u >= 0xFFFFu) {  // outside [1, 65535]: escape
+            u[e] = 0;
+            ++nesc;
+          }
+        }
+        reinterpret_cast<uint2*>(cache)[j] = make_uint2(u[0] | (u[1] << 16), u[2] | (u[3] << 16));
+      } else if constexpr (kWide) {
         reinterpret_cast<uint4*>(cache)[j] = make_uint4(tw[4 * i], tw[4 * i + 1], tw[4 * i + 2], tw[4 * i + 3]);
       } else {
         reinterpret_cast<uint2*>(cache)[j] = make_uint2(tw[2 * i], tw[2 * i + 1]);
       }
     }
+    if (kEntry == 3 && nesc && esc) atomicAdd_system(esc, nesc);  // rare: mapped host memory
   }
 }
 
@@ -925,7 +1020,7 @@ __device__ void fused_tail_elem(const FusedArgs& a, uint32_t i, const uint2* ske
   }
   S out;
   if constexpr (cached(kMode)) {
-    elem_fold_cached<DT>(&acc, &out, 0, a.tail_e0 + i, a.cache, kMode == kCache32, a.nkeys);
+    elem_fold_cached<DT>(&acc, &out, 0, a.tail_e0 + i, a.cache, cache_kind_of(kMode), a.nkeys, a.keys);
   } else {
     elem_reduce<DT>(&acc, &out, 0, a.tail_e0 + i, skeys, a.nkeys);
   }
@@ -995,7 +1090,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
     uint32_t ctr[NW];
     if constexpr (!cached(kMode)) tile_ctrs<W, U>(j0, ctr);
     uint32_t r[T::kWords ? NW : NW * 4];
-    peer_sums<K, U, kMode>(ctr, skeys, a.nkeys, 1u, r, a.cache, j0);
+    peer_sums<K, U, kMode>(ctr, skeys, a.nkeys, 1u, r, a.cache, j0, nullptr, a.keys);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
@@ -1521,8 +1616,8 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
 // The fold of a cached call: the hot kernel in a cached mode, one tile of
 // U = 2 vectors per thread per block (the memory-bound shape).
 template <int K, int DT>
-cudaError_t run_vec_cached(const void* src, void* dst, uint64_t count, uint64_t elem_base, uint32_t nkeys,
-                           int64_t* stamp, cudaStream_t s, CacheRef cache) {
+cudaError_t run_vec_cached(const void* src, void* dst, uint64_t count, uint64_t elem_base, const uint32_t* keys,
+                           uint32_t nkeys, int64_t* stamp, cudaStream_t s, CacheRef cache) {
   using T = VT<K>;
   constexpr int U = 2;
   const uint64_t nvec = count / T::EPV;
@@ -1534,9 +1629,12 @@ cudaError_t run_vec_cached(const void* src, void* dst, uint64_t count, uint64_t 
   auto kern = synth_reduce_vec<K, DT, U, kCache32>;
   if constexpr (!T::kWords) {
     if (cache.kind == kCacheLanes16) kern = synth_reduce_vec<K, DT, U, kCache16>;
+    if (cache.kind == kCacheCentered16) {
+      kern = cache.clean ? synth_reduce_vec<K, DT, U, kCacheC16F> : synth_reduce_vec<K, DT, U, kCacheC16>;
+    }
   }
   kern<<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
-      static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, nullptr, nkeys, stamp,
+      static_cast<const uint4*>(src), static_cast<uint4*>(dst), nvec, word_base, keys, nkeys, stamp,
       static_cast<const uint8_t*>(src) + nvec * T::EPV * es, static_cast<uint8_t*>(dst) + nvec * T::EPV * es, ntail,
       elem_base + nvec * T::EPV, 1u, cache.ptr);
   return cudaGetLastError();
@@ -1632,13 +1730,13 @@ cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t 
     if (words && cache.kind != kCacheWide32) return cudaErrorInvalidValue;
     ++*launches;
     switch (dtype) {
-      case cemuFloat32: return run_vec_cached<kF32, cemuFloat32>(src, dst, count, elem_base, nkeys, stamp, s, cache);
-      case cemuBfloat16: return run_vec_cached<kBF16, cemuBfloat16>(src, dst, count, elem_base, nkeys, stamp, s, cache);
-      case cemuFloat16: return run_vec_cached<kF16, cemuFloat16>(src, dst, count, elem_base, nkeys, stamp, s, cache);
-      case cemuUint8: return run_vec_cached<kU8, cemuUint8>(src, dst, count, elem_base, nkeys, stamp, s, cache);
-      case cemuInt8: return run_vec_cached<kU8, cemuInt8>(src, dst, count, elem_base, nkeys, stamp, s, cache);
-      case cemuInt32: return run_vec_cached<kI32, cemuInt32>(src, dst, count, elem_base, nkeys, stamp, s, cache);
-      case cemuUint32: return run_vec_cached<kI32, cemuUint32>(src, dst, count, elem_base, nkeys, stamp, s, cache);
+      case cemuFloat32: return run_vec_cached<kF32, cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
+      case cemuBfloat16: return run_vec_cached<kBF16, cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
+      case cemuFloat16: return run_vec_cached<kF16, cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
+      case cemuUint8: return run_vec_cached<kU8, cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
+      case cemuInt8: return run_vec_cached<kU8, cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
+      case cemuInt32: return run_vec_cached<kI32, cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
+      case cemuUint32: return run_vec_cached<kI32, cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
       default: --*launches; return cudaErrorInvalidValue;
     }
   }
@@ -1721,10 +1819,12 @@ cudaError_t launch_synth_cache_fill(bool words, uint64_t elem_base, uint64_t cou
   if (grid > 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const size_t smem = static_cast<size_t>(nkeys) * 8;
   auto kern = words ? synth_cache_fill<U, 2>
-                    : (cache.kind == kCacheLanes16 ? synth_cache_fill<U, 0> : synth_cache_fill<U, 1>);
+                    : (cache.kind == kCacheLanes16      ? synth_cache_fill<U, 0>
+                       : cache.kind == kCacheCentered16 ? synth_cache_fill<U, 3>
+                                                        : synth_cache_fill<U, 1>);
   if (const cudaError_t e = fit_smem(kern, smem)) return e;
   ++*launches;
-  kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(wb, we, d_keys, nkeys, cache.ptr, 1u);
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(wb, we, d_keys, nkeys, cache.ptr, 1u, cache.esc);
   return cudaGetLastError();
 }
 
@@ -1840,6 +1940,10 @@ cudaError_t fused_ku(const FusedArgs& a, cudaStream_t s) {
   if constexpr (!VT<K>::kWords) {
     if (a.cache && a.cache_kind == kCacheLanes16) {
       kern = fused_allreduce_vec<K, DT, KMAX, U, kCache16>;
+      smem = 0;
+    }
+    if (a.cache && a.cache_kind == kCacheCentered16) {
+      kern = a.cache_clean ? fused_allreduce_vec<K, DT, KMAX, U, kCacheC16F> : fused_allreduce_vec<K, DT, KMAX, U, kCacheC16>;
       smem = 0;
     }
   }

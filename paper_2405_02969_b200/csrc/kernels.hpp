@@ -61,15 +61,28 @@ int64_t queue_gap_ns();
 // from it.  Entries, indexed by absolute payload element e:
 //   kCacheLanes16  byte kinds (u8/i8/fp16/bf16/fp32), <= 256 peers: uint16
 //                  t_e = sum over peers of byte_r(e)
-//   kCacheWide32   byte kinds, > 256 peers: uint32 t_e;  32-bit integer
-//                  kinds: uint32 wrapping sum of word_r(e)
-enum CacheKind { kNoCache = 0, kCacheLanes16 = 1, kCacheWide32 = 2 };
+//   kCacheWide32   byte kinds, > CEMU_SYNTH_CACHE_C16_MAX peers: uint32 t_e;
+//                  32-bit integer kinds: uint32 wrapping sum of word_r(e)
+//   kCacheCentered16  byte kinds, 257..CEMU_SYNTH_CACHE_C16_MAX (8192) peers:
+//                  uint16 u_e = t_e - c16_offset(n) (mod 2^32) when it lies in
+//                  [1, 65535], else 0 -- an escape: the fold recomputes t_e
+//                  exactly from the keys.  t_e has mean 127.5 n and standard
+//                  deviation 73.9 sqrt(n), so u_e is centred on 32768 and an
+//                  escape needs a 6.9-sigma sum at n = 4096 (4.8 at 8192)
+enum CacheKind { kNoCache = 0, kCacheLanes16 = 1, kCacheWide32 = 2, kCacheCentered16 = 3 };
+// floor(127.5 n) - 32768 (mod 2^32): the centred entries' offset
+inline constexpr uint32_t c16_offset(uint32_t n) { return n * 255u / 2u - 32768u; }
 struct CacheRef {
   void* ptr = nullptr;  // entry 0 = payload element 0
   int kind = kNoCache;
+  // centred entries: `clean` = the range is known to hold no escape (its
+  // fill has completed and counted none), so the fold may skip the escape
+  // test; `esc` = where a fill counts its escapes (mapped host memory)
+  bool clean = false;
+  uint32_t* esc = nullptr;
 };
 // Cache entries of one element range need this many bytes per element.
-inline size_t cache_entry_bytes(int kind) { return kind == kCacheLanes16 ? 2 : 4; }
+inline size_t cache_entry_bytes(int kind) { return kind == kCacheWide32 ? 4 : 2; }
 
 // dst[i] = src[i] (+) sum over `nkeys` emulated peers of their payload at
 // element elem_base + i.  src may equal dst.  Returns the number of kernel
@@ -132,6 +145,7 @@ struct FusedArgs {
   // synthesis cache covering this GPU's slice (and tail), or none
   const void* cache = nullptr;
   int cache_kind = kNoCache;
+  bool cache_clean = false;  // centred entries without escapes (CacheRef::clean)
   // fold-only chunks: when *gate != 0 (the start barrier failed) only
   // dst[me] (local) is written
   const uint32_t* gate = nullptr;

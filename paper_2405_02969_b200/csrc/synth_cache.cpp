@@ -7,9 +7,60 @@ namespace cemu_b200 {
 
 // ---- synthesis cache ----------------------------------------------------
 namespace {
+// The largest emulated world cached with centred 16-bit entries
+// (CEMU_SYNTH_CACHE_C16_MAX, default 8192: escapes need a 4.8-sigma byte sum
+// there; beyond it uint32 entries).
+uint32_t c16_max_peers() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("CEMU_SYNTH_CACHE_C16_MAX");
+    return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 8192u;
+  }();
+  return v;
+}
+
 bool cacheable_dtype(int dt) {
   return dt == cemuFloat32 || dt == cemuBfloat16 || dt == cemuFloat16 || dt == cemuUint8 || dt == cemuInt8 ||
          dt == cemuInt32 || dt == cemuUint32;
+}
+
+// A centred segment's escape counter (zeroed) and fill event.
+bool esc_slot(cemuComm* c, cemuComm::SynthCache::Segment* g) {
+  constexpr size_t kBlock = 1024;
+  if (c->esc_used % kBlock == 0) {
+    void* blk = nullptr;
+    if (cudaHostAlloc(&blk, kBlock * sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    c->esc_blocks.push_back(static_cast<uint32_t*>(blk));
+  }
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  c->seg_events.push_back(ev);
+  g->esc_h = c->esc_blocks.back() + c->esc_used++ % kBlock;
+  *g->esc_h = 0;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, g->esc_h, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  g->esc_d = static_cast<uint32_t*>(d);
+  g->filled = ev;
+  return true;
+}
+
+// The fill event of the segment a fill just wrote (centred entries only).
+void note_filled(cemuComm* c, const CacheRef& cr, cudaStream_t s) {
+  if (cr.kind != kCacheCentered16) return;
+  for (const auto& g : c->cache_bytes.segs) {
+    if (g.esc_d == cr.esc && g.filled) {
+      cudaEventRecord(g.filled, s);
+      return;
+    }
+  }
 }
 
 // The cache to use for elements [b, e) of dtype dt, or none.  *fill: the
@@ -28,19 +79,28 @@ CacheRef cache_for(cemuComm* c, int dt, uint64_t b, uint64_t e, cudaStream_t s, 
   if (bytes < (1u << 20) && !heavy) return {};
   const bool words = dt == cemuInt32 || dt == cemuUint32;
   auto& sc = words ? c->cache_words : c->cache_bytes;
-  if (sc.kind == kNoCache) sc.kind = (words || c->virt.size() > 256) ? kCacheWide32 : kCacheLanes16;
+  if (sc.kind == kNoCache) {
+    const size_t n = c->virt.size();
+    sc.kind = words ? kCacheWide32 : n <= 256 ? kCacheLanes16 : n <= c16_max_peers() ? kCacheCentered16 : kCacheWide32;
+  }
   const size_t entry = cache_entry_bytes(sc.kind);
   const uint64_t end = words ? e : (e + 3) / 4 * 4;  // the fill writes whole payload words
   // entry 0 of the returned pointer is element 0's: a segment's base moved
   // back by its first element (only indices inside the segment are read)
   auto ref = [&](const cemuComm::SynthCache::Segment& g) {
-    return CacheRef{reinterpret_cast<void*>(reinterpret_cast<uintptr_t>(g.ptr) - g.b * entry), sc.kind};
+    return CacheRef{reinterpret_cast<void*>(reinterpret_cast<uintptr_t>(g.ptr) - g.b * entry), sc.kind,
+                    g.esc_state == 0, g.esc_d};
   };
   const bool cap = capturing(s);
   for (auto& g : sc.segs) {
     if (g.b <= b && end <= g.e) {  // written by an earlier call, which every later call is ordered after
       g.captured |= cap;
       ++c->cache_hits;
+      // a centred range's escape count is known once its fill has run (no
+      // wait: until then, and inside a capture, the fold tests for escapes)
+      if (g.esc_state < 0 && g.filled && !cap && cudaEventQuery(g.filled) == cudaSuccess) {
+        g.esc_state = *reinterpret_cast<volatile uint32_t*>(g.esc_h) != 0 ? 1 : 0;
+      }
       return ref(g);
     }
   }
@@ -63,7 +123,12 @@ CacheRef cache_for(cemuComm* c, int dt, uint64_t b, uint64_t e, cudaStream_t s, 
     cudaGetLastError();
     return {};
   }
-  sc.segs.push_back({b, end, p, have, false});
+  cemuComm::SynthCache::Segment g{b, end, p, have, false};
+  if (sc.kind == kCacheCentered16 && !esc_slot(c, &g)) {
+    sc.spare.emplace_back(p, have);
+    return {};
+  }
+  sc.segs.push_back(g);
   sc.bytes += have;
   ++c->cache_fills;
   *fill = true;
@@ -78,17 +143,18 @@ cudaError_t synth_reduce(cemuComm* c, int dt, const void* src, void* dst, uint64
   bool fill = false;
   const CacheRef cr = al ? cache_for(c, dt, e0, e0 + count, s, &fill) : CacheRef{};
   if (!cr.ptr) return launch_synth_reduce(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches);
-  if (fill && (cr.kind == kCacheWide32) == (dt == cemuInt32 || dt == cemuUint32)) {
+  if (fill && cr.kind == ((dt == cemuInt32 || dt == cemuUint32) ? kCacheWide32 : kCacheLanes16)) {
     // one pass synthesises, folds and writes the entries (+ the tail's)
     return launch_synth_reduce_filling(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, cr);
   }
-  if (fill) {  // > 256 emulated ranks of a byte kind: fill, then the cached fold
+  if (fill) {  // > 256 emulated ranks of a byte kind: fill, then the cached fold (centred or wide entries)
     if (stamp) {  // the call starts with the fill
       if (const cudaError_t e = launch_stamp(stamp, s, launches)) return e;
       stamp = nullptr;
     }
     const bool words = dt == cemuInt32 || dt == cemuUint32;
     if (const cudaError_t e = launch_synth_cache_fill(words, e0, count, c->d_virt_keys, nk, cr, s, launches)) return e;
+    note_filled(c, cr, s);
   }
   return launch_synth_reduce(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, cr);
 }
@@ -107,9 +173,11 @@ cudaError_t cache_fused(cemuComm* c, int dt, FusedArgs& a, cudaStream_t s, int* 
       a.stamp = nullptr;
     }
     if (const cudaError_t r = launch_synth_cache_fill(words, b, e - b, a.keys, a.nkeys, cr, s, launches)) return r;
+    note_filled(c, cr, s);
   }
   a.cache = cr.ptr;
   a.cache_kind = cr.kind;
+  a.cache_clean = cr.clean;
   return cudaSuccess;
 }
 

@@ -3,7 +3,7 @@ at the many-peer shapes (config 2: world 64 fp32 / bf16 / int32; config 3
 at k = 1: world 128 bf16; world 1024 bf16), with the cache off, on its
 filling call and on warm calls.  Prints one JSON line per shape.
 
-  python profiles/cache_probe.py [--mib 1024] [--reps 10]
+  python profiles/cache_probe.py [--mib 1024] [--reps 10] [--shapes 1024:bf16,1024:fp32]
 """
 import argparse
 import json
@@ -33,11 +33,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mib", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--shapes", default="", help="W:dtype,... (fp32, bf16, int32); default: the six below")
     args = ap.parse_args()
+    names = {"fp32": torch.float32, "bf16": torch.bfloat16, "int32": torch.int32}
+    shapes = [(int(w), names[d]) for w, d in (x.split(":") for x in args.shapes.split(",") if x)] or \
+        [(64, torch.float32), (64, torch.bfloat16), (64, torch.int32), (128, torch.bfloat16),
+         (16, torch.float32), (1024, torch.bfloat16)]
     torch.cuda.set_device(0)
     S = args.mib << 20
-    for W, dtype in ((64, torch.float32), (64, torch.bfloat16), (64, torch.int32), (128, torch.bfloat16),
-                     (16, torch.float32), (1024, torch.bfloat16)):
+    for W, dtype in shapes:
         comm = pb.Communicator(f"world_size = {W}\nreal_ranks = 0\nbucket_bytes = 1\n", 0, 0)
         n = S // torch.empty(0, dtype=dtype).element_size()
         x = torch.ones(n, dtype=dtype, device="cuda") if dtype != torch.int32 else \

@@ -72,6 +72,30 @@ def test_copy_engine_allreduce_equals_the_fused_kernel(cache):
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
+def test_fused_kernel_reads_centred_cache_entries():
+    """k real GPUs in worlds of 1,024 (config 5's) and 20,001 ranks: the fused
+    kernel folds its slice from centred 16-bit cache entries, escapes
+    included (window raised to 28,672 ranks), bit-exact against the oracle
+    on every byte kind (tests/c16_worker.py)."""
+    import json
+    n = min(torch.cuda.device_count(), 4)
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "c16_worker.py")
+    env = dict(os.environ, CEMU_SYNTH_CACHE_C16_MAX="28672")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()), worker, "1024", "20001"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    import re
+    lines = [json.loads(m) for m in re.findall(r'\{"rank".*\]\}', r.stdout)]
+    assert len(lines) == n, r.stdout[-2000:]
+    for res in lines:
+        if res["rank"] == 0:
+            esc = {c["world"]: c["escapes"] for c in res["cases"]}
+            assert esc[1024] == 0 and esc[20001] > 100, esc
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
 def test_single_process_init_all(tmp_path):
     """ncclCommInitAll shape: one process drives every GPU (grouped calls)."""
     import numpy as np

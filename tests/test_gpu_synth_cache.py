@@ -3,8 +3,8 @@
 The emulated ranks' contribution depends only on (seed, rank, element), so
 a communicator folds repeat calls over an element range from a cache of the
 per-element sums.  Every call here -- the one that fills the cache and the
-ones that read it, every datatype, both entry widths (<= 256 and > 256
-emulated ranks), ragged tails, offsets, both streams, graph replay -- is
+ones that read it, every datatype, every entry form (uint16 at <= 256
+emulated ranks, centred uint16 with escapes beyond, uint32 word sums), ragged tails, offsets, both streams, graph replay -- is
 compared bit for bit with the CPU oracle, which never caches.
 """
 from __future__ import annotations
@@ -43,10 +43,31 @@ def test_cached_allreduce_equals_oracle_on_fill_and_hits(cuda, W, dt):
         assert_bit_equal(_ar(comm, h), want, f"cached allreduce W={W} dt={dt} call {i}")
     st = comm.synth_cache_stats()
     assert st["fills"] == 1 and st["hits"] == 2, st
-    entry = 4 if (dt == 2 or W > 257) else 2
+    entry = 4 if dt == 2 else 2  # W = 300: centred 16-bit entries
     entries = count if dt == 2 else (count + 3) // 4 * 4  # byte kinds: whole payload words
     assert st["bytes"] == entries * entry  # one segment, exactly the range's entries
     comm.close()
+
+
+def test_centred_entries_and_their_escapes():
+    """257..8192 emulated ranks keep 16-bit entries centred on the byte sums'
+    mean (kernels.hpp kCacheCentered16); a sum outside the 16-bit window is an
+    escape the fold recomputes from the keys.  With the window's bound raised
+    to 28,672 ranks, worlds of 20,001 / 20,002 ranks (even and odd peer
+    counts: the u8 offset byte differs) make ~1.5% of the entries escapes --
+    every result still equals the oracle (tests/c16_worker.py)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "c16_worker.py")
+    env = dict(os.environ, CEMU_SYNTH_CACHE_C16_MAX="28672")
+    r = subprocess.run([sys.executable, worker, "1024", "20001", "20002"], capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    esc = {c["world"]: c["escapes"] for c in res["cases"]}
+    assert esc[1024] == 0 and esc[20001] > 100 and esc[20002] > 100, esc
 
 
 def test_one_byte_cache_serves_every_byte_kind(cuda):
