@@ -228,9 +228,11 @@ def sweep(model: str, delays_us, world: int = 2, bucket_bytes: int = 65536, devi
               "samples": int(len(xs)), "ideal_us": ideal,
               "rel_err": float(abs(np.mean(xs) - ideal) / ideal)}
         if reference_fn is not None:
-            ri = np.asarray(reference_fn(spec.render(), world, bucket_bytes, float(d)))[info["warmup"]:]
-            pt["reference_mean_us"] = float(np.mean(ri))
-            pt["reference_rel_err"] = float(abs(np.mean(ri) - ideal) / ideal)
+            ref_iters = reference_fn(spec.render(), world, bucket_bytes, float(d))
+            if ref_iters is not None:  # None: the comparison emulator gave no result for this point
+                ri = np.asarray(ref_iters)[info["warmup"]:]
+                pt["reference_mean_us"] = float(np.mean(ri))
+                pt["reference_rel_err"] = float(abs(np.mean(ri) - ideal) / ideal)
         points.append(pt)
     tail = [(p["inject_us"], p["mean_us"]) for p in points if p["inject_us"] > knee]
     marg = [(p["inject_us"], p["mean_us"]) for p in points if p["inject_us"] < knee]
@@ -238,8 +240,8 @@ def sweep(model: str, delays_us, world: int = 2, bucket_bytes: int = 65536, devi
            "tail_slope": ols_slope(*zip(*tail)) if len(tail) >= 2 else None,
            "marginal_slope": ols_slope(*zip(*marg)) if len(marg) >= 2 else None,
            "max_rel_err": max(p["rel_err"] for p in points), "points": points}
-    if reference_fn is not None:
-        res["reference_max_rel_err"] = max(p["reference_rel_err"] for p in points)
+    if any("reference_rel_err" in p for p in points):
+        res["reference_max_rel_err"] = max(p["reference_rel_err"] for p in points if "reference_rel_err" in p)
     ok = True
     if res["tail_slope"] is not None:
         ok &= 0.9 * nb <= res["tail_slope"] <= 1.1 * nb

@@ -32,7 +32,7 @@ def _ar(comm, h, stream=None):
     return to_np(r)
 
 
-@pytest.mark.parametrize("W", [64, 300])
+@pytest.mark.parametrize("W", [64, 258, 300])
 @pytest.mark.parametrize("dt", [7, 9, 6, 1, 0, 2])
 def test_cached_allreduce_equals_oracle_on_fill_and_hits(cuda, W, dt):
     comm = _comm(W)
