@@ -339,7 +339,7 @@ def emulated_comm(k, fit=None, plugin=None, footprint=(0, 0)):
 NCCL_FOOTPRINT = (32, 82240 + 21568)
 
 
-def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=40, footprint=NCCL_FOOTPRINT):
+def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=100, footprint=NCCL_FOOTPRINT):
     sizes = sizes or SIZES
     rank, k = dist.get_rank(), dist.get_world_size()
     host = dist.new_group(backend="gloo")
@@ -404,12 +404,14 @@ def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=40, footprint=
     loaded = loaded_sweep(sizes, 20)
     service = []
     barrier()
+    # the baseline runs twice -- before and after the emulated runs -- so a
+    # drift of the box (clocks, power) over the measurement cannot pose as
+    # an emulation error; both halves feed the in-situ calibration
     base = mlp_loop(NcclAllReduce(), mlp_iters, 3, service=service)
     barrier()
     row = {"model": "mlp_bf16_8x4096_25MiB"}
+    modes = ()
     if rank == 0:
-        row["baseline_mean_us"] = float(np.mean(base))
-        row["baseline_stddev_us"] = float(np.std(base, ddof=1))
         insitu, insitu_us = size_plugin(service)
         row["loaded_calibration_us"] = [round(u, 2) for u in loaded]
         row["in_situ_service_us"] = {str(b): round(u, 2) for b, u in insitu_us.items()}
@@ -418,15 +420,30 @@ def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=40, footprint=
                  ("table_footprint", {"plugin": plugin}, footprint),
                  ("loaded_footprint", {"plugin": table_plugin(sizes, loaded)}, footprint),
                  ("in_situ_footprint", {"plugin": insitu}, footprint))
+        emus = {}
         for tag, kw, fp in modes:
             comm = emulated_comm(k, footprint=fp, **kw)
-            emu = mlp_loop(comm, mlp_iters, 3)
+            emus[tag] = mlp_loop(comm, mlp_iters, 3)
             comm.close()
-            row[f"emulated_{tag}_mean_us"] = float(np.mean(emu))
-            row[f"rel_err_{tag}"] = float(abs(np.mean(emu) - np.mean(base)) / np.mean(base))
         comp = mlp_loop(type("ComputeOnly", (), {"all_reduce": lambda self, t, recv=None, stream=None: t})(),
                         mlp_iters, 3)
         row["compute_only_mean_us"] = float(np.mean(comp))
+    barrier()
+    base2 = mlp_loop(NcclAllReduce(), mlp_iters, 3)
+    barrier()
+    if rank == 0:
+        pooled = list(base) + list(base2)
+        bm = float(np.mean(pooled))
+        row["baseline_mean_us"] = bm
+        row["baseline_halves_mean_us"] = [float(np.mean(base)), float(np.mean(base2))]
+        row["baseline_stddev_us"] = float(np.std(pooled, ddof=1))
+        # the baseline mean's own uncertainty: two standard errors, relative
+        # (iterations with real GEMMs beside NCCL vary by a few percent)
+        row["baseline_noise_2sem_rel"] = float(2 * np.std(pooled, ddof=1) / np.sqrt(len(pooled)) / bm)
+        row["iterations"] = {"baseline": len(pooled), "emulated": mlp_iters}
+        for tag, *_ in modes:
+            row[f"emulated_{tag}_mean_us"] = float(np.mean(emus[tag]))
+            row[f"rel_err_{tag}"] = float(abs(np.mean(emus[tag]) - bm) / bm)
     barrier()
     res["mlp"] = row
     if rank == 0:
@@ -444,7 +461,7 @@ def main():
     ap.add_argument("--reps", type=int, default=100)
     ap.add_argument("--segments", type=int, default=3)
     ap.add_argument("--e2e-iters", type=int, default=20)
-    ap.add_argument("--mlp-iters", type=int, default=40)
+    ap.add_argument("--mlp-iters", type=int, default=100)
     ap.add_argument("--max-mib", type=int, default=256)
     ap.add_argument("--footprint-ctas", type=int, default=NCCL_FOOTPRINT[0], help="NCCL's channel count on this box")
     ap.add_argument("--footprint-smem", type=int, default=NCCL_FOOTPRINT[1], help="shared memory per NCCL CTA")
