@@ -180,8 +180,9 @@ cemuResult_t cemuCommDeregister(cemuComm_t comm, void* handle);
  * every call over the same element range.  A call over a range of >= 1 MiB
  * (or >= 64 KiB when elements x emulated ranks >= 2^27) with >= minPeers
  * emulated ranks writes those sums into a per-communicator
- * cache (2 bytes per element for the byte kinds up to 256 emulated ranks,
- * else 4) and later calls over the range fold from it -- a memory-bound pass
+ * cache (2 bytes per element for the byte kinds up to
+ * CEMU_SYNTH_CACHE_C16_MAX = 8192 emulated ranks, else 4) and later calls
+ * over the range fold from it -- a memory-bound pass
  * instead of issue-bound synthesis, with identical bits.  capBytes bounds
  * each of the two caches (byte kinds / 32-bit integer kinds; default
  * CEMU_SYNTH_CACHE_MB = 4096 MiB, minPeers CEMU_SYNTH_CACHE_MIN_PEERS = 16);
