@@ -1395,6 +1395,12 @@ __global__ void chain_join_kernel(int64_t* chain, const int64_t* other) {
   if (o > *chain) *chain = o;
 }
 
+// The last gate (= the largest floor, the call's modelled latency).
+__device__ __forceinline__ int64_t run_max_floor(uint32_t k, const int64_t* sgate, const int64_t* gates_beyond) {
+  if (k == 0) return 0;
+  return k - 1 < static_cast<uint32_t>(kInlineOffsets) ? sgate[k - 1] : gates_beyond[k - 1];
+}
+
 __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* slot, const double* inline_offs) {
   int64_t* floors = slot + kSlotHeader;
   int64_t* release = floors + d.kmax;
@@ -1418,10 +1424,9 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
   // Evaluate the model on the device: delay.cpp:23-47 offsets and
   // engine.cpp:41 llround floors, strided over the block.  A delay-model
   // plugin's offsets (DelayModelFn, delay.hpp:52-55) arrive preloaded.
-  // The releasing thread reads the floors from shared memory (up to
-  // kInlineOffsets of them): its loop is then a few cycles per step, so the
-  // last release follows the last floor by nanoseconds, not by K global loads.
   __shared__ int64_t sfloor[kInlineOffsets];
+  __shared__ int64_t sgate[kInlineOffsets];
+  __shared__ int64_t wmax[kThreads / 32];
   const double total = (!d.preloaded && d.model.kind == 1) ? model_total_us(d.model, d.coll, d.n, d.bytes) : 0.0;
   for (uint32_t j = threadIdx.x; j < d.k; j += blockDim.x) {
     const double o = inline_offs ? inline_offs[j] : d.preloaded ? offs[j] : release_offset_us(d.model, total, j, d.k);
@@ -1431,35 +1436,105 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
     if (j < static_cast<uint32_t>(kInlineOffsets)) sfloor[j] = f;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  auto floor_at = [&](uint32_t j) { return j < static_cast<uint32_t>(kInlineOffsets) ? sfloor[j] : floors[j]; };
-  int64_t lat = 0;
-  for (uint32_t j = 0; j < d.k; ++j) lat = max(lat, floor_at(j));
-  slot[2] = lat;
-  slot[3] = d.k;
   // Head-of-line release (engine.cpp:58-70): step j leaves once its floor
-  // has passed and step j-1 has left.
+  // has passed and step j-1 has left -- at the first poll at or after its
+  // gate, the running maximum of the floors up to j.  The gates are a
+  // block-wide prefix maximum (each thread a contiguous segment), kept in
+  // shared memory (first kInlineOffsets steps) or, beyond, in the release
+  // array the times later overwrite.
+  auto floor_at = [&](uint32_t j) { return j < static_cast<uint32_t>(kInlineOffsets) ? sfloor[j] : floors[j]; };
+  auto gate_ref = [&](uint32_t j) -> int64_t& { return j < static_cast<uint32_t>(kInlineOffsets) ? sgate[j] : release[j]; };
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t seg = (d.k + blockDim.x - 1) / blockDim.x;
+  const uint32_t sb = min(d.k, threadIdx.x * seg), se = min(d.k, sb + seg);
+  int64_t m = 0;  // floors are >= 0
+  for (uint32_t j = sb; j < se; ++j) m = max(m, floor_at(j));
+  int64_t incl = m;  // inclusive scan of the segment maxima over the block
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl = max(incl, v);
+  }
+  if (lane == 31) wmax[warp] = incl;
+  __syncthreads();
+  int64_t run = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) run = 0;
+  for (uint32_t w = 0; w < warp; ++w) run = max(run, wmax[w]);
+  for (uint32_t j = sb; j < se; ++j) {
+    run = max(run, floor_at(j));
+    gate_ref(j) = run;
+  }
+  __syncthreads();
+  // The release loop: thread 0 waits for the next gate; warp 0 finds how far
+  // the gates have passed at that instant (32 probes per round, O(log32 K));
+  // the whole block records that run of steps.  So many steps on one floor
+  // (a fixed or injected delay gives every step the same floor) leave
+  // together, not through a serial K-step loop that would lengthen the call
+  // (126 steps at world 64 cost 8.8 us that way).
+  const int64_t lat = run_max_floor(d.k, sgate, release);  // the last gate
+  if (threadIdx.x == 0) {
+    slot[2] = lat;
+    slot[3] = d.k;
+  }
   // A step released after its floor is late: the emulator's own work (the
   // synthesis kernels before this one) outlasted that step's floor, or the
   // spin overshot.  The largest lateness is recorded (slot[5]), and how far
   // the whole call overran its modelled latency (slot[6]), so such a call
   // is visible, never silently longer.
+  __shared__ int64_t t_s;
+  __shared__ uint32_t e_s;
   const int64_t t0 = t0_s;
-  int64_t t = globaltimer_ns();
   int64_t late = 0;
-  for (uint32_t j = 0; j < d.k; ++j) {
-    const int64_t target = t0 + floor_at(j) * 1000;
-    while (t < target) {
-      if (target - t > 8000) __nanosleep(2000);
-      t = globaltimer_ns();
+  uint32_t pos = 0;
+  while (pos < d.k) {
+    if (threadIdx.x == 0) {
+      const int64_t next = t0 + gate_ref(pos) * 1000;
+      int64_t t = globaltimer_ns();
+      while (t < next) {
+        if (next - t > 8000) __nanosleep(2000);
+        t = globaltimer_ns();
+      }
+      t_s = t;
     }
-    release[j] = t;
-    late = max(late, t - target);
+    __syncthreads();
+    const int64_t t = t_s;
+    if (warp == 0) {
+      // e = the first step in [pos, k) whose gate is still ahead of t
+      // (gates are non-decreasing); its gate at pos has passed
+      uint32_t lo = pos + 1, hi = d.k;  // the answer lies in [lo, hi]
+      while (lo < hi) {
+        const uint32_t stride = (hi - lo + 31) / 32;
+        const uint32_t j = lo + lane * stride;  // probes lo, lo + stride, ...
+        const bool passed = j < hi && t0 + gate_ref(j) * 1000 <= t;
+        const uint32_t np = __popc(__ballot_sync(0xffffffffu, passed));  // the passed probes lead
+        if (np == 0) break;                                              // probe lo is ahead: e = lo
+        const uint32_t nhi = min(hi, lo + np * stride);  // the first probe still ahead (or hi)
+        lo = lo + (np - 1) * stride + 1;                 // just after the last passed probe
+        hi = nhi;
+      }
+      if (lane == 0) e_s = lo;
+    }
+    __syncthreads();
+    const uint32_t e = e_s;
+    for (uint32_t j = pos + threadIdx.x; j < e; j += blockDim.x) {
+      late = max(late, t - (t0 + floor_at(j) * 1000));
+      release[j] = t;  // (beyond kInlineOffsets this overwrites the gate, already passed)
+    }
+    pos = e;
+    __syncthreads();  // e_s / t_s / the gates read above are done with
   }
-  slot[5] = late;
-  const int64_t end = globaltimer_ns();
-  slot[6] = max(int64_t{0}, end - (t0 + lat * 1000));  // the call itself ran long by this much
-  slot[1] = end;
+  // the block's largest lateness
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) late = max(late, __shfl_xor_sync(0xffffffffu, late, o));
+  if (lane == 0) wmax[warp] = late;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < blockDim.x / 32; ++w) late = max(late, wmax[w]);
+    slot[5] = late;
+    const int64_t end = globaltimer_ns();
+    slot[6] = max(int64_t{0}, end - (t0 + lat * 1000));  // the call itself ran long by this much
+    slot[1] = end;
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int64_t* slot) {
@@ -1575,7 +1650,7 @@ Shape pick_shape(int words_per_vec, uint32_t nkeys, uint64_t nvec) {
 template <int K, int DT, int U>
 cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_base,
                       const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s, int bps_req,
-                      void* fill = nullptr) {
+                      void* fill = nullptr, uint32_t grid_cap = 0) {
   using T = VT<K>;
   const uint64_t nvec = count / T::EPV;
   const uint32_t ntail = static_cast<uint32_t>(count - nvec * T::EPV);
@@ -1600,7 +1675,7 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
     const char* e = std::getenv("CEMU_SYNTH_GRID");
     return (e && std::string(e) == "persistent") || std::getenv("CEMU_SYNTH_BPS");
   }();
-  uint64_t cap = 0x7FFFFFFFull;
+  uint64_t cap = grid_cap ? grid_cap : 0x7FFFFFFFull;
   if (persistent) {
     const int occ = blocks_per_sm(kern, smem);
     cap = static_cast<uint64_t>(sm_count()) * (bps_req > 0 ? std::min(bps_req, occ) : std::min(occ, 4));
@@ -1617,7 +1692,7 @@ cudaError_t run_vec_u(const void* src, void* dst, uint64_t count, uint64_t elem_
 // U = 2 vectors per thread per block (the memory-bound shape).
 template <int K, int DT>
 cudaError_t run_vec_cached(const void* src, void* dst, uint64_t count, uint64_t elem_base, const uint32_t* keys,
-                           uint32_t nkeys, int64_t* stamp, cudaStream_t s, CacheRef cache) {
+                           uint32_t nkeys, int64_t* stamp, cudaStream_t s, CacheRef cache, uint32_t grid_cap = 0) {
   using T = VT<K>;
   constexpr int U = 2;
   const uint64_t nvec = count / T::EPV;
@@ -1625,7 +1700,7 @@ cudaError_t run_vec_cached(const void* src, void* dst, uint64_t count, uint64_t 
   const size_t es = T::kWords ? 4 : (K == kF32 ? 4 : (K == kU8 ? 1 : 2));
   const uint64_t word_base = T::kWords ? elem_base : elem_base / 4;
   const uint64_t tiles = (nvec + static_cast<uint64_t>(kThreads) * U - 1) / (static_cast<uint64_t>(kThreads) * U);
-  const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, 0x7FFFFFFFull));
+  const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(tiles, grid_cap ? grid_cap : 0x7FFFFFFFull));
   auto kern = synth_reduce_vec<K, DT, U, kCache32>;
   if constexpr (!T::kWords) {
     if (cache.kind == kCacheLanes16) kern = synth_reduce_vec<K, DT, U, kCache16>;
@@ -1680,7 +1755,8 @@ cudaError_t run_split(const void* src, void* dst, uint64_t count, uint64_t elem_
 
 template <int K, int DT>
 cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_base,
-                    const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s, void* fill = nullptr) {
+                    const uint32_t* keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s, void* fill = nullptr,
+                    uint32_t grid_cap = 0) {
   constexpr int W = VT<K>::WPV;
   if (fill && split_ways(VT<K>::kWords, nkeys, count / VT<K>::EPV)) return cudaErrorInvalidValue;
   if (const int P = split_ways(VT<K>::kWords, nkeys, count / VT<K>::EPV)) {
@@ -1694,13 +1770,13 @@ cudaError_t run_vec(const void* src, void* dst, uint64_t count, uint64_t elem_ba
   }
   const Shape sh = pick_shape(W, nkeys, count / VT<K>::EPV);
   if constexpr (8 / W >= 8) {
-    if (sh.u == 8 && !fill) return run_vec_u<K, DT, 8>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps);
+    if (sh.u == 8 && !fill) return run_vec_u<K, DT, 8>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, nullptr, grid_cap);
   }
   if constexpr (8 / W >= 4) {
-    if (sh.u >= 4) return run_vec_u<K, DT, 4>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, fill);
+    if (sh.u >= 4) return run_vec_u<K, DT, 4>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, fill, grid_cap);
   }
-  if (sh.u == 1) return run_vec_u<K, DT, 1>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, fill);
-  return run_vec_u<K, DT, 2>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, fill);
+  if (sh.u == 1) return run_vec_u<K, DT, 1>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, fill, grid_cap);
+  return run_vec_u<K, DT, 2>(src, dst, count, elem_base, keys, nkeys, stamp, s, sh.bps, fill, grid_cap);
 }
 
 template <int DT>
@@ -1720,7 +1796,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t count,
                                 uint64_t elem_base, const uint32_t* d_keys, uint32_t nkeys,
-                                int64_t* stamp, cudaStream_t s, int* launches, CacheRef cache) {
+                                int64_t* stamp, cudaStream_t s, int* launches, CacheRef cache, uint32_t grid_cap) {
   if (nkeys > kMaxKeys) return cudaErrorInvalidValue;
   if (count == 0) return cudaSuccess;
   if (cache.ptr) {
@@ -1730,13 +1806,13 @@ cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t 
     if (words && cache.kind != kCacheWide32) return cudaErrorInvalidValue;
     ++*launches;
     switch (dtype) {
-      case cemuFloat32: return run_vec_cached<kF32, cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
-      case cemuBfloat16: return run_vec_cached<kBF16, cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
-      case cemuFloat16: return run_vec_cached<kF16, cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
-      case cemuUint8: return run_vec_cached<kU8, cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
-      case cemuInt8: return run_vec_cached<kU8, cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
-      case cemuInt32: return run_vec_cached<kI32, cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
-      case cemuUint32: return run_vec_cached<kI32, cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache);
+      case cemuFloat32: return run_vec_cached<kF32, cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache, grid_cap);
+      case cemuBfloat16: return run_vec_cached<kBF16, cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache, grid_cap);
+      case cemuFloat16: return run_vec_cached<kF16, cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache, grid_cap);
+      case cemuUint8: return run_vec_cached<kU8, cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache, grid_cap);
+      case cemuInt8: return run_vec_cached<kU8, cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache, grid_cap);
+      case cemuInt32: return run_vec_cached<kI32, cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache, grid_cap);
+      case cemuUint32: return run_vec_cached<kI32, cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache, grid_cap);
       default: --*launches; return cudaErrorInvalidValue;
     }
   }
@@ -1747,25 +1823,25 @@ cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t 
   const bool word_al = (elem_base % 4) == 0;
   switch (dtype) {
     case cemuFloat32:
-      if (al && word_al) return run_vec<kF32, cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      if (al && word_al) return run_vec<kF32, cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, nullptr, grid_cap);
       return run_scalar<cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     case cemuBfloat16:
-      if (al && word_al) return run_vec<kBF16, cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      if (al && word_al) return run_vec<kBF16, cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, nullptr, grid_cap);
       return run_scalar<cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     case cemuFloat16:
-      if (al && word_al) return run_vec<kF16, cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      if (al && word_al) return run_vec<kF16, cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, nullptr, grid_cap);
       return run_scalar<cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     case cemuUint8:
-      if (al && word_al) return run_vec<kU8, cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      if (al && word_al) return run_vec<kU8, cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, nullptr, grid_cap);
       return run_scalar<cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     case cemuInt8:
-      if (al && word_al) return run_vec<kU8, cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      if (al && word_al) return run_vec<kU8, cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, nullptr, grid_cap);
       return run_scalar<cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     case cemuInt32:
-      if (al) return run_vec<kI32, cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      if (al) return run_vec<kI32, cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, nullptr, grid_cap);
       return run_scalar<cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     case cemuUint32:
-      if (al) return run_vec<kI32, cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
+      if (al) return run_vec<kI32, cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, nullptr, grid_cap);
       return run_scalar<cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     case cemuInt64: return run_scalar<cemuInt64>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
     case cemuUint64: return run_scalar<cemuUint64>(src, dst, count, elem_base, d_keys, nkeys, stamp, s);
@@ -1776,7 +1852,7 @@ cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t 
 
 cudaError_t launch_synth_reduce_filling(int dtype, const void* src, void* dst, uint64_t count, uint64_t elem_base,
                                         const uint32_t* d_keys, uint32_t nkeys, int64_t* stamp, cudaStream_t s,
-                                        int* launches, CacheRef cache) {
+                                        int* launches, CacheRef cache, uint32_t grid_cap) {
   const bool words = dtype == cemuInt32 || dtype == cemuUint32;
   if (!cache.ptr || count == 0 || nkeys == 0 || !aligned16(src) || !aligned16(dst) || elem_base % 4 != 0 ||
       (words ? cache.kind != kCacheWide32 : (cache.kind != kCacheLanes16 || nkeys > 256))) {
@@ -1786,13 +1862,13 @@ cudaError_t launch_synth_reduce_filling(int dtype, const void* src, void* dst, u
   cudaError_t e = cudaErrorInvalidValue;
   uint32_t epv = 4;
   switch (dtype) {
-    case cemuFloat32: e = run_vec<kF32, cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 4; break;
-    case cemuBfloat16: e = run_vec<kBF16, cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 8; break;
-    case cemuFloat16: e = run_vec<kF16, cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 8; break;
-    case cemuUint8: e = run_vec<kU8, cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 16; break;
-    case cemuInt8: e = run_vec<kU8, cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 16; break;
-    case cemuInt32: e = run_vec<kI32, cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 4; break;
-    case cemuUint32: e = run_vec<kI32, cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr); epv = 4; break;
+    case cemuFloat32: e = run_vec<kF32, cemuFloat32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr, grid_cap); epv = 4; break;
+    case cemuBfloat16: e = run_vec<kBF16, cemuBfloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr, grid_cap); epv = 8; break;
+    case cemuFloat16: e = run_vec<kF16, cemuFloat16>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr, grid_cap); epv = 8; break;
+    case cemuUint8: e = run_vec<kU8, cemuUint8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr, grid_cap); epv = 16; break;
+    case cemuInt8: e = run_vec<kU8, cemuInt8>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr, grid_cap); epv = 16; break;
+    case cemuInt32: e = run_vec<kI32, cemuInt32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr, grid_cap); epv = 4; break;
+    case cemuUint32: e = run_vec<kI32, cemuUint32>(src, dst, count, elem_base, d_keys, nkeys, stamp, s, cache.ptr, grid_cap); epv = 4; break;
     default: break;
   }
   if (e != cudaSuccess) {

@@ -91,14 +91,18 @@ inline size_t cache_entry_bytes(int kind) { return kind == kCacheWide32 ? 4 : 2;
 // same bits.  Cached calls need 16-byte aligned src/dst and elem_base % 4 == 0.
 cudaError_t launch_synth_reduce(int dtype, const void* src, void* dst, uint64_t count,
                                 uint64_t elem_base, const uint32_t* d_keys, uint32_t nkeys,
-                                int64_t* stamp, cudaStream_t stream, int* launches, CacheRef cache = {});
+                                int64_t* stamp, cudaStream_t stream, int* launches, CacheRef cache = {},
+                                uint32_t grid_cap = 0);
+// grid_cap > 0: at most that many CTAs (grid-stride) -- an emulated call
+// with a delay footprint keeps its own memory work on about as many SMs as
+// the real collective's kernel would use (cemuCommSetDelayFootprint).
 // launch_synth_reduce that also writes the cache entries of
 // [elem_base, elem_base + count) in the same pass (the first call over a
 // range): <= 256 emulated peers for the byte kinds (uint16 entries) or the
 // 32-bit integer kinds; a ragged tail's entries by a small fill.
 cudaError_t launch_synth_reduce_filling(int dtype, const void* src, void* dst, uint64_t count, uint64_t elem_base,
                                         const uint32_t* d_keys, uint32_t nkeys, int64_t* stamp, cudaStream_t stream,
-                                        int* launches, CacheRef cache);
+                                        int* launches, CacheRef cache, uint32_t grid_cap = 0);
 // Writes the cache entries of elements [elem_base, elem_base + count)
 // (byte kinds: whole payload words, i.e. rounded out to multiples of 4).
 // `words`: the 32-bit integer kinds' entries.

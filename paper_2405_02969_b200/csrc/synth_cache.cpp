@@ -140,12 +140,20 @@ cudaError_t synth_reduce(cemuComm* c, int dt, const void* src, void* dst, uint64
                          int64_t* stamp, cudaStream_t s, int* launches) {
   const uint32_t nk = static_cast<uint32_t>(c->virt.size());
   const bool al = (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 == 0;
+  // a delay footprint stands for the real collective's kernel: the emulated
+  // call's own memory pass -- a cached fold, or the synthesis of <= 16
+  // emulated ranks, both HBM-bound like the real reduction -- stays within
+  // as many CTAs instead of briefly taking every SM from the job's compute
+  // (DESIGN §6c).  Issue-bound synthesis (more ranks, a cache fill) keeps
+  // the whole machine: on a few CTAs it would outlast the modelled delay.
+  const uint32_t fp = (c->hold_ctas > 0 && (c->delay_active || c->delay_fn)) ? static_cast<uint32_t>(c->hold_ctas) : 0;
+  const uint32_t cap = nk <= 16 ? fp : 0;
   bool fill = false;
   const CacheRef cr = al ? cache_for(c, dt, e0, e0 + count, s, &fill) : CacheRef{};
-  if (!cr.ptr) return launch_synth_reduce(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches);
+  if (!cr.ptr) return launch_synth_reduce(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, {}, cap);
   if (fill && cr.kind == ((dt == cemuInt32 || dt == cemuUint32) ? kCacheWide32 : kCacheLanes16)) {
     // one pass synthesises, folds and writes the entries (+ the tail's)
-    return launch_synth_reduce_filling(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, cr);
+    return launch_synth_reduce_filling(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, cr, 0);
   }
   if (fill) {  // > 256 emulated ranks of a byte kind: fill, then the cached fold (centred or wide entries)
     if (stamp) {  // the call starts with the fill
@@ -156,7 +164,7 @@ cudaError_t synth_reduce(cemuComm* c, int dt, const void* src, void* dst, uint64
     if (const cudaError_t e = launch_synth_cache_fill(words, e0, count, c->d_virt_keys, nk, cr, s, launches)) return e;
     note_filled(c, cr, s);
   }
-  return launch_synth_reduce(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, cr);
+  return launch_synth_reduce(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, cr, fp);
 }
 
 cudaError_t cache_fused(cemuComm* c, int dt, FusedArgs& a, cudaStream_t s, int* launches) {

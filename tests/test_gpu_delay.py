@@ -391,3 +391,41 @@ def test_chain_join_continues_compute_from_the_release_end(cuda):
     assert int(chain.item()) == 1 << 62
     assert lib.cemuChainJoin(s, None, end) != 0  # null chain: invalid argument
     comm.close()
+
+
+@pytest.mark.parametrize("W,dt,count", [(8, 7, (2 << 20) + 3), (8, 9, (4 << 20) + 5), (64, 7, (1 << 20) + 7)])
+def test_footprint_keeps_the_synthesis_on_its_ctas_bit_exact(W, dt, count):
+    """With a delay footprint the emulated call's memory pass runs on at most
+    that many CTAs (grid-stride, as the real collective's kernel would);
+    the results stay bit-exact -- synthesised and, at world 64, folded from
+    the synthesis cache -- and the delay still ends on the model."""
+    from gpu_util import assert_bit_equal, host_input, to_np
+    comm = pb.Communicator(delay_config(W, 2, fixed=300.0), 0, 0)
+    comm.set_delay_footprint(32, 0)
+    for i in range(2):  # world 64: fill, then a cached fold
+        h = host_input(dt, count, seed=70 + i)
+        x = h.cuda()
+        y = torch.empty_like(x)
+        comm.all_reduce(x, y)
+        torch.cuda.synchronize()
+        want = P.allreduce(dt, P.PAYLOAD_HASH, W, [0], 0, 1, [to_np(h)], count)
+        assert_bit_equal(to_np(y), want, f"footprint W={W} dt={dt} call {i}")
+        rec = comm.call_record()
+        meas = (rec["t_end_ns"] - rec["t_start_ns"]) / 1e3
+        assert abs(meas - rec["model_latency_us"]) <= max(0.01 * rec["model_latency_us"], 2.0), rec
+    comm.close()
+
+
+@pytest.mark.parametrize("W,fixed", [(64, 300.0), (1024, 1000.0)])
+def test_many_steps_on_one_floor_release_on_time(W, fixed):
+    """A fixed delay gives all 2(W-1) steps the same floor: they leave by one
+    poll of the releasing warp, so the call ends on the model -- not K serial
+    releases later (126 steps at world 64 used to add 8.8 us)."""
+    comm = pb.Communicator(delay_config(W, 2, fixed=fixed), 0, 0)
+    for _ in range(3):
+        rec = run_coll(comm, 0, 1 << 16)
+        meas = (rec["t_end_ns"] - rec["t_start_ns"]) / 1e3
+        assert rec["steps"] == 2 * (W - 1)
+        assert abs(meas - fixed) <= 2.0, (meas, rec["overshoot_ns"])
+        assert rec["late_ns"] <= 2000, rec
+    comm.close()
