@@ -49,8 +49,10 @@ def test_emulated_matches_baseline():
     assert res["microbench_check"]["pass_table"], res["microbench"]
     for row in res["e2e"]:
         assert row["rel_err_table"] < 0.01, row
-    # the real-compute MLP: with the delay calibrated under compute load and
-    # NCCL's SM footprint emulated; 12 noisy iterations here, so
-    # the regression bound is looser than the < 1% the full runs show
+    # the real-compute MLP: the idle latency table with NCCL's SM footprint
+    # emulated and the emulator's memory pass held to it; 12
+    # noisy iterations here, so the regression bound is looser than the < 1%
+    # the full runs show -- and without the footprint the error is 6-8%
     mlp = res["mlp"]
-    assert min(mlp["rel_err_loaded_footprint"], mlp["rel_err_in_situ_footprint"]) < 0.02, mlp
+    assert mlp["rel_err_table_footprint"] < 0.02, mlp
+    assert mlp["rel_err_table"] > mlp["rel_err_table_footprint"], mlp
