@@ -32,6 +32,7 @@
 #include "kernels.hpp"
 #include "payload.cuh"
 
+
 namespace cemu_b200 {
 namespace {
 
@@ -1465,12 +1466,6 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
     gate_ref(j) = run;
   }
   __syncthreads();
-  // The release loop: thread 0 waits for the next gate; warp 0 finds how far
-  // the gates have passed at that instant (32 probes per round, O(log32 K));
-  // the whole block records that run of steps.  So many steps on one floor
-  // (a fixed or injected delay gives every step the same floor) leave
-  // together, not through a serial K-step loop that would lengthen the call
-  // (126 steps at world 64 cost 8.8 us that way).
   const int64_t lat = run_max_floor(d.k, sgate, release);  // the last gate
   if (threadIdx.x == 0) {
     slot[2] = lat;
@@ -1481,60 +1476,65 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
   // spin overshot.  The largest lateness is recorded (slot[5]), and how far
   // the whole call overran its modelled latency (slot[6]), so such a call
   // is visible, never silently longer.
-  __shared__ int64_t t_s;
-  __shared__ uint32_t e_s;
+  // Thread 0 releases, one step per poll while the floors are spread out
+  // (a few cycles per step: the last release follows the last floor by
+  // nanoseconds).  When it is catching up -- step j's floor had already
+  // passed -- and the gate 8 steps on has passed too, the whole run of
+  // passed steps (a fixed or injected delay gives every step the same
+  // floor) is found by binary search over the non-decreasing gates and
+  // released at once; its per-step times are written after the call's end
+  // is recorded.  A serial K-step loop would lengthen the call (126 steps on
+  // one floor at world 64 took 8.8 us).
+  if (threadIdx.x != 0) return;
+  constexpr uint32_t kRuns = 64, kSerialRun = 8;
+  __shared__ uint32_t run_b[kRuns], run_e[kRuns];
+  __shared__ int64_t run_t[kRuns];
+  auto gate = [&](uint32_t j) { return j < static_cast<uint32_t>(kInlineOffsets) ? sgate[j] : release[j]; };
+  uint32_t nruns = 0;
   const int64_t t0 = t0_s;
   int64_t late = 0;
-  uint32_t pos = 0;
-  while (pos < d.k) {
-    if (threadIdx.x == 0) {
-      const int64_t next = t0 + gate_ref(pos) * 1000;
-      int64_t t = globaltimer_ns();
-      while (t < next) {
-        if (next - t > 8000) __nanosleep(2000);
+  int64_t t = globaltimer_ns();
+  for (uint32_t j = 0; j < d.k;) {
+    const int64_t target = t0 + floor_at(j) * 1000;
+    if (t < target) {
+      do {
+        if (target - t > 8000) __nanosleep(2000);
         t = globaltimer_ns();
-      }
-      t_s = t;
-    }
-    __syncthreads();
-    const int64_t t = t_s;
-    if (warp == 0) {
-      // e = the first step in [pos, k) whose gate is still ahead of t
-      // (gates are non-decreasing); its gate at pos has passed
-      uint32_t lo = pos + 1, hi = d.k;  // the answer lies in [lo, hi]
+      } while (t < target);
+    } else if (j + kSerialRun < d.k && t0 + gate(j + kSerialRun) * 1000 <= t) {
+      uint32_t lo = j + kSerialRun + 1, hi = d.k;  // the first step whose gate is still ahead
       while (lo < hi) {
-        const uint32_t stride = (hi - lo + 31) / 32;
-        const uint32_t j = lo + lane * stride;  // probes lo, lo + stride, ...
-        const bool passed = j < hi && t0 + gate_ref(j) * 1000 <= t;
-        const uint32_t np = __popc(__ballot_sync(0xffffffffu, passed));  // the passed probes lead
-        if (np == 0) break;                                              // probe lo is ahead: e = lo
-        const uint32_t nhi = min(hi, lo + np * stride);  // the first probe still ahead (or hi)
-        lo = lo + (np - 1) * stride + 1;                 // just after the last passed probe
-        hi = nhi;
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (t0 + gate(mid) * 1000 <= t) lo = mid + 1; else hi = mid;
       }
-      if (lane == 0) e_s = lo;
+      if (nruns < kRuns) {
+        run_b[nruns] = j;
+        run_e[nruns] = lo;
+        run_t[nruns] = t;
+        ++nruns;
+      } else {
+        for (uint32_t i = j; i < lo; ++i) {
+          late = max(late, t - (t0 + floor_at(i) * 1000));
+          release[i] = t;
+        }
+      }
+      j = lo;
+      continue;
     }
-    __syncthreads();
-    const uint32_t e = e_s;
-    for (uint32_t j = pos + threadIdx.x; j < e; j += blockDim.x) {
-      late = max(late, t - (t0 + floor_at(j) * 1000));
-      release[j] = t;  // (beyond kInlineOffsets this overwrites the gate, already passed)
+    release[j] = t;
+    late = max(late, t - target);
+    ++j;
+  }
+  const int64_t end = globaltimer_ns();
+  slot[6] = max(int64_t{0}, end - (t0 + lat * 1000));  // the call itself ran long by this much
+  slot[1] = end;
+  for (uint32_t r = 0; r < nruns; ++r) {  // the runs' per-step times and lateness
+    for (uint32_t i = run_b[r]; i < run_e[r]; ++i) {
+      late = max(late, run_t[r] - (t0 + floor_at(i) * 1000));
+      release[i] = run_t[r];
     }
-    pos = e;
-    __syncthreads();  // e_s / t_s / the gates read above are done with
   }
-  // the block's largest lateness
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) late = max(late, __shfl_xor_sync(0xffffffffu, late, o));
-  if (lane == 0) wmax[warp] = late;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (uint32_t w = 1; w < blockDim.x / 32; ++w) late = max(late, wmax[w]);
-    slot[5] = late;
-    const int64_t end = globaltimer_ns();
-    slot[6] = max(int64_t{0}, end - (t0 + lat * 1000));  // the call itself ran long by this much
-    slot[1] = end;
-  }
+  slot[5] = late;
 }
 
 __global__ void __launch_bounds__(kThreads) delay_spin_kernel(DelayLaunch d, int64_t* slot) {
