@@ -94,3 +94,27 @@ def test_iteration_csv_round_trip_and_stats(tmp_path):
     assert sorted(back) == [0, 1, 2] and back[1]["buckets"] == [(0, 1010, 1500), (1, 1600, 2070)]
     st = W.iteration_stats(trace, warmup=1)
     assert st["count"] == 2 and abs(st["mean_us"] - np.mean(trace["iter_us"][1:])) < 1e-9
+
+
+@needs_ref
+def test_reference_loop_in_a_bounded_process():
+    """bench.py's what-if comparison arm runs the reference's own
+    run_training_loop in a separate, killable process (oracle/ref_loop.py):
+    per-iteration times come back as JSON; a bad model is a nonzero exit
+    with the reference's error, not an exception in the bench."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = ModelSpec.load("bert-like").render()
+    lines = [ln for ln in text.splitlines() if not ln.startswith(("iterations", "warmup"))]
+    short = "\n".join(lines + ["iterations = 4", "warmup = 1"]) + "\n"
+    r = subprocess.run([sys.executable, "-m", "oracle.ref_loop"], cwd=root, text=True, capture_output=True, timeout=120,
+                       input=json.dumps({"text": short, "world": 2, "bucket_bytes": 65536, "inject": 100.0}))
+    assert r.returncode == 0, r.stderr
+    it = json.loads(r.stdout.strip().splitlines()[-1])
+    assert len(it) == 4 and all(t > 0 for t in it)
+    bad = subprocess.run([sys.executable, "-m", "oracle.ref_loop"], cwd=root, text=True, capture_output=True,
+                         timeout=60, input=json.dumps({"text": "nonsense = 1\n", "world": 2, "bucket_bytes": 65536,
+                                                       "inject": 0}))
+    assert bad.returncode == 1 and bad.stderr.strip()
