@@ -178,7 +178,7 @@ cemuResult_t cemuCommDeregister(cemuComm_t comm, void* handle);
 /* Synthesis cache.  The emulated ranks' payloads depend only on
  * (seed, rank, element index), so their per-element sums are the same in
  * every call over the same element range.  A call over a range of >= 1 MiB
- * (or >= 64 KiB when elements x emulated ranks >= 2^27) with >= minPeers
+ * (or >= 64 KiB when elements x emulated ranks >= 2^21) with >= minPeers
  * emulated ranks writes those sums into a per-communicator
  * cache (2 bytes per element for the byte kinds up to
  * CEMU_SYNTH_CACHE_C16_MAX = 8192 emulated ranks, else 4) and later calls

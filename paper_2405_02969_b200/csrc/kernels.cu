@@ -1858,6 +1858,21 @@ cudaError_t launch_synth_reduce_filling(int dtype, const void* src, void* dst, u
       (words ? cache.kind != kCacheWide32 : (cache.kind != kCacheLanes16 || nkeys > 256))) {
     return cudaErrorInvalidValue;
   }
+  {
+    // buffers small enough for the peer-split kernels (which have no
+    // filling variant): the entries first, then the cached fold
+    const uint64_t ev = words || dtype == cemuFloat32 ? 4 : (dtype == cemuUint8 || dtype == cemuInt8 ? 16 : 8);
+    if (split_ways(words, nkeys, count / ev)) {
+      if (stamp) {  // the call starts with the fill
+        if (const cudaError_t e = launch_stamp(stamp, s, launches)) return e;
+        stamp = nullptr;
+      }
+      if (const cudaError_t e = launch_synth_cache_fill(words, elem_base, count, d_keys, nkeys, cache, s, launches)) {
+        return e;
+      }
+      return launch_synth_reduce(dtype, src, dst, count, elem_base, d_keys, nkeys, stamp, s, launches, cache, grid_cap);
+    }
+  }
   ++*launches;
   cudaError_t e = cudaErrorInvalidValue;
   uint32_t epv = 4;

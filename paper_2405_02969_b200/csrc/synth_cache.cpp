@@ -72,10 +72,11 @@ CacheRef cache_for(cemuComm* c, int dt, uint64_t b, uint64_t e, cudaStream_t s, 
     return {};
   }
   // small calls are launch-bound either way: not worth an entry -- unless
-  // the world makes even a small range's synthesis long (>= 2^27 peer-
-  // elements: e.g. a 1024-rank FSDP reduce-scatter chunk of ~0.4 MB)
+  // the world makes even a small range's synthesis longer than the launch
+  // (>= 2^21 peer-elements: at world 64 from 128 KiB of fp32, where the
+  // synthesis alone took 2.3-2.9 us per call against ~1.6 us cached)
   const uint64_t bytes = (e - b) * dtype_size(dt);
-  const bool heavy = (e - b) * static_cast<uint64_t>(c->virt.size()) >= (1ull << 27) && bytes >= (64u << 10);
+  const bool heavy = (e - b) * static_cast<uint64_t>(c->virt.size()) >= (1ull << 21) && bytes >= (64u << 10);
   if (bytes < (1u << 20) && !heavy) return {};
   const bool words = dt == cemuInt32 || dt == cemuUint32;
   auto& sc = words ? c->cache_words : c->cache_bytes;
