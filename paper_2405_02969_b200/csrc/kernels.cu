@@ -261,7 +261,7 @@ __device__ __forceinline__ void load_keys(uint2* skeys, const uint32_t* keys, ui
 //   kCache16 no synthesis: the peers' per-element byte sums t (<= 256
 //            peers, uint16 lanes) are read from the communicator's synthesis
 //            cache (synth_cache_fill wrote them; see "synthesis cache" below)
-//   kCache32 the same with uint32 entries: byte sums of > 256 peers, or the
+//   kCache32 the same with uint32 entries: byte sums of > 8192 peers, or the
 //            wrapping word sums of the 32-bit integer kinds
 //   kCacheC16 the same with centred uint16 entries (257..8192 peers; an
 //            entry 0 is an escape recomputed from the keys, kernels.hpp)
@@ -432,7 +432,8 @@ __device__ __forceinline__ void t16_to_lanes(uint32_t w01, uint32_t w23, uint32_
 // nonzero iff some 16-bit lane of x is 0 (a centred entry's escape)
 __device__ __forceinline__ uint32_t zero_lane16(uint32_t x) { return (x - 0x00010001u) & ~x & 0x80008000u; }
 
-// ... and from uint32 byte sums T_e (> 256 peers): the kGroups flush below
+// ... and from uint32 byte sums T_e (> 256 peers: centred escapes, uint32
+// entries beyond 8192 peers): the kGroups flush below
 // computes the same integers (sum over groups of t - 128 * group size).
 template <int K>
 __device__ __forceinline__ void t32_to_lanes(const uint4& t, uint32_t n, uint32_t* r) {

@@ -156,7 +156,7 @@ cudaError_t synth_reduce(cemuComm* c, int dt, const void* src, void* dst, uint64
     // one pass synthesises, folds and writes the entries (+ the tail's)
     return launch_synth_reduce_filling(dt, src, dst, count, e0, c->d_virt_keys, nk, stamp, s, launches, cr, 0);
   }
-  if (fill) {  // > 256 emulated ranks of a byte kind: fill, then the cached fold (centred or wide entries)
+  if (fill) {  // > 256 emulated ranks of a byte kind (centred or uint32 entries): fill, then the cached fold
     if (stamp) {  // the call starts with the fill
       if (const cudaError_t e = launch_stamp(stamp, s, launches)) return e;
       stamp = nullptr;
