@@ -128,3 +128,45 @@ def test_random_calls_through_the_synthesis_cache(cuda, block):
     assert sum(s["fills"] for s in stats) > 0
     for c in comms.values():
         c.close()
+
+
+@pytest.mark.parametrize("block", range(3))
+def test_random_mid_size_calls_through_the_synthesis_cache(cuda, block):
+    """64 KiB - 1 MiB allreduces / reduce-scatters at worlds whose ranges
+    reach 2^21 peer-elements (the cache's lower bound): small enough for the
+    peer-split kernels (entries filled by synth_cache_fill, then the cached
+    fold), partial overlaps, misaligned pointers, every entry form (uint16,
+    centred, uint32 words) -- every result equals the oracle."""
+    rng = random.Random(9100 + block)
+    comms = {}
+    for _ in range(16):
+        W = rng.choice([33, 64, 300, 1025])
+        rank = rng.randrange(W)
+        key = (W, rank)
+        if key not in comms:
+            comms[key] = pb.Communicator(config(W, (rank,), "hash", 1), rank, 0)
+        comm = comms[key]
+        dt = rng.choice([0, 1, 2, 6, 7, 9])
+        es = torch.empty(0, dtype=TORCH[dt]).element_size()
+        shift = rng.choice([0, 0, 0, 1])
+        what = f"W={W} rank={rank} dt={dt} shift={shift}"
+        if W >= 300 or rng.random() < 0.6:  # (reduce-scatter buffers of W chunks stay at the smaller worlds)
+            count = rng.randrange((64 << 10) // es, (1 << 20) // es)
+            h = host_input(dt, count, seed=rng.randrange(1 << 30))
+            want = P.allreduce(dt, P.PAYLOAD_HASH, W, [rank], rank, 1, [to_np(h)], count)
+            x = _on_device(h, shift)
+            y = _on_device(torch.zeros_like(h), 0)
+            comm.all_reduce(x, y)
+            torch.cuda.synchronize()
+            assert_bit_equal(to_np(y), want, f"mid-size allreduce n={count} " + what)
+        else:
+            rc = rng.randrange((64 << 10) // es, (512 << 10) // es) // 4 * 4
+            h = host_input(dt, rc * W, seed=rng.randrange(1 << 30))
+            want = P.reducescatter(dt, P.PAYLOAD_HASH, W, [rank], rank, 1, [to_np(h)], rc)
+            out = _on_device(torch.zeros(rc, dtype=TORCH[dt]), shift)
+            comm.reduce_scatter(_on_device(h, 0), out)
+            torch.cuda.synchronize()
+            assert_bit_equal(to_np(out), want, f"mid-size reduce-scatter rc={rc} " + what)
+    assert sum(c.synth_cache_stats()["fills"] for c in comms.values()) > 0
+    for c in comms.values():
+        c.close()
