@@ -430,8 +430,21 @@ cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs,
   f.ndst = static_cast<int>(k);
   f.gate = a.error;
   uintptr_t stage_at[kMaxReal] = {};
+  // CEMU_CE_DIRECT = d: the d peers after this GPU in ring order are read by
+  // the fold kernels straight from their send buffers over NVLink (SM loads,
+  // after the start barrier like the fused kernel's), the others staged by
+  // the copy engines -- a split of the incoming NVLink leg between the two
+  // engines (at k = 4 concurrent copy-engine pulls from every peer lose)
+  static const uint32_t direct_env = [] {
+    const char* e = std::getenv("CEMU_CE_DIRECT");
+    return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
+  }();
+  const uint32_t direct = std::min(direct_env, k - 1);
+  bool staged[kMaxReal] = {};
   for (uint32_t g = 0, slot = 0; g < k; ++g) {
     if (g == c->li) continue;
+    if ((g + k - c->li) % k <= direct) continue;  // read directly: f.src[g] stays the peer's send
+    staged[g] = true;
     CUDA_OK(cudaStreamWaitEvent(p.pull[g], started, 0));
     // peer g's staging, indexed like the buffers: vector v at stage[v - v_begin]
     stage_at[g] = reinterpret_cast<uintptr_t>(p.stage) + slot++ * slice - a.v_begin * 16;
@@ -441,8 +454,8 @@ cemuResult_t ce_allreduce(cemuComm* c, int dt, FusedArgs a, uint64_t stage_vecs,
   int ev = 2;
   for (uint64_t v0 = a.v_begin; v0 < a.v_end; v0 += cvec) {
     const uint64_t v1 = std::min(a.v_end, v0 + cvec);
-    for (uint32_t g = 0; g < k; ++g) {  // every peer's chunk on its own copy stream
-      if (g == c->li) continue;
+    for (uint32_t g = 0; g < k; ++g) {  // every staged peer's chunk on its own copy stream
+      if (!staged[g]) continue;
       cudaEvent_t pulled = p.ev[ev++];
       CUDA_OK(cudaMemcpyAsync(reinterpret_cast<void*>(stage_at[g] + v0 * 16), a.src[g] + v0, (v1 - v0) * 16,
                               cudaMemcpyDeviceToDevice, p.pull[g]));
