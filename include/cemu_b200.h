@@ -254,8 +254,10 @@ cemuResult_t cemuCommSetQueueChaining(cemuComm_t comm, int64_t gapUs);
  * slowing compute that runs beside it on other streams.  With ctas > 0 every
  * delayed call's wait also holds `ctas` CTAs (544 threads, smemBytes of
  * shared memory each) until its modelled end, so that contention is
- * emulated too.  0 (the default; CEMU_DELAY_HOLD_CTAS / _SMEM) holds one
- * CTA, the schedule's. */
+ * emulated too, and the call's own HBM-bound memory pass (a cached fold, or
+ * the synthesis of <= 16 emulated ranks) runs on at most `ctas` CTAs, as the
+ * real reduction would.  0 (the default; CEMU_DELAY_HOLD_CTAS / _SMEM)
+ * holds one CTA, the schedule's. */
 cemuResult_t cemuCommSetDelayFootprint(cemuComm_t comm, int ctas, size_t smemBytes);
 
 cemuResult_t cemuCommLastCallId(cemuComm_t comm, uint64_t* callId);
