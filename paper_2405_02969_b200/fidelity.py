@@ -339,7 +339,56 @@ def emulated_comm(k, fit=None, plugin=None, footprint=(0, 0)):
 NCCL_FOOTPRINT = (32, 82240 + 21568)
 
 
-def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=100, footprint=NCCL_FOOTPRINT):
+def mlp_fidelity(k, rank, barrier, sizes, plugin, loaded, mlp_iters, footprint):
+    """One repeat of the real-compute MLP check: the NCCL baseline before and
+    after the emulated runs (pooled, drift-bracketed; both halves feed the
+    in-situ calibration), the emulated loop under each calibration, and
+    compute alone.  Rank 0's row (other ranks: {})."""
+    service = []
+    barrier()
+    base = mlp_loop(NcclAllReduce(), mlp_iters, 3, service=service)
+    barrier()
+    row = {"model": "mlp_bf16_8x4096_25MiB"}
+    modes = ()
+    if rank == 0:
+        insitu, insitu_us = size_plugin(service)
+        row["loaded_calibration_us"] = [round(u, 2) for u in loaded]
+        row["in_situ_service_us"] = {str(b): round(u, 2) for b, u in insitu_us.items()}
+        row["footprint"] = {"ctas": footprint[0], "smem_bytes": footprint[1]}
+        modes = (("table", {"plugin": plugin}, (0, 0)),
+                 ("table_footprint", {"plugin": plugin}, footprint),
+                 ("loaded_footprint", {"plugin": table_plugin(sizes, loaded)}, footprint),
+                 ("in_situ_footprint", {"plugin": insitu}, footprint))
+        emus = {}
+        for tag, kw, fp in modes:
+            comm = emulated_comm(k, footprint=fp, **kw)
+            emus[tag] = mlp_loop(comm, mlp_iters, 3)
+            comm.close()
+        comp = mlp_loop(type("ComputeOnly", (), {"all_reduce": lambda self, t, recv=None, stream=None: t})(),
+                        mlp_iters, 3)
+        row["compute_only_mean_us"] = float(np.mean(comp))
+    barrier()
+    base2 = mlp_loop(NcclAllReduce(), mlp_iters, 3)
+    barrier()
+    if rank == 0:
+        pooled = list(base) + list(base2)
+        bm = float(np.mean(pooled))
+        row["baseline_mean_us"] = bm
+        row["baseline_halves_mean_us"] = [float(np.mean(base)), float(np.mean(base2))]
+        row["baseline_stddev_us"] = float(np.std(pooled, ddof=1))
+        # the baseline mean's own uncertainty: two standard errors, relative
+        # (iterations with real GEMMs beside NCCL vary by a few percent)
+        row["baseline_noise_2sem_rel"] = float(2 * np.std(pooled, ddof=1) / np.sqrt(len(pooled)) / bm)
+        row["iterations"] = {"baseline": len(pooled), "emulated": mlp_iters}
+        for tag, *_ in modes:
+            row[f"emulated_{tag}_mean_us"] = float(np.mean(emus[tag]))
+            row[f"rel_err_{tag}"] = float(abs(np.mean(emus[tag]) - bm) / bm)
+    barrier()
+    return row
+
+
+def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=100, footprint=NCCL_FOOTPRINT,
+        mlp_repeats=1):
     sizes = sizes or SIZES
     rank, k = dist.get_rank(), dist.get_world_size()
     host = dist.new_group(backend="gloo")
@@ -402,49 +451,24 @@ def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=100, footprint
         res["e2e"].append(row)
     # --- e2e: a real bf16 MLP (tensor-core GEMMs beside the collectives) ----
     loaded = loaded_sweep(sizes, 20)
-    service = []
-    barrier()
-    # the baseline runs twice -- before and after the emulated runs -- so a
-    # drift of the box (clocks, power) over the measurement cannot pose as
-    # an emulation error; both halves feed the in-situ calibration
-    base = mlp_loop(NcclAllReduce(), mlp_iters, 3, service=service)
-    barrier()
-    row = {"model": "mlp_bf16_8x4096_25MiB"}
-    modes = ()
-    if rank == 0:
-        insitu, insitu_us = size_plugin(service)
-        row["loaded_calibration_us"] = [round(u, 2) for u in loaded]
-        row["in_situ_service_us"] = {str(b): round(u, 2) for b, u in insitu_us.items()}
-        row["footprint"] = {"ctas": footprint[0], "smem_bytes": footprint[1]}
-        modes = (("table", {"plugin": plugin}, (0, 0)),
-                 ("table_footprint", {"plugin": plugin}, footprint),
-                 ("loaded_footprint", {"plugin": table_plugin(sizes, loaded)}, footprint),
-                 ("in_situ_footprint", {"plugin": insitu}, footprint))
-        emus = {}
-        for tag, kw, fp in modes:
-            comm = emulated_comm(k, footprint=fp, **kw)
-            emus[tag] = mlp_loop(comm, mlp_iters, 3)
-            comm.close()
-        comp = mlp_loop(type("ComputeOnly", (), {"all_reduce": lambda self, t, recv=None, stream=None: t})(),
-                        mlp_iters, 3)
-        row["compute_only_mean_us"] = float(np.mean(comp))
-    barrier()
-    base2 = mlp_loop(NcclAllReduce(), mlp_iters, 3)
-    barrier()
-    if rank == 0:
-        pooled = list(base) + list(base2)
-        bm = float(np.mean(pooled))
-        row["baseline_mean_us"] = bm
-        row["baseline_halves_mean_us"] = [float(np.mean(base)), float(np.mean(base2))]
-        row["baseline_stddev_us"] = float(np.std(pooled, ddof=1))
-        # the baseline mean's own uncertainty: two standard errors, relative
-        # (iterations with real GEMMs beside NCCL vary by a few percent)
-        row["baseline_noise_2sem_rel"] = float(2 * np.std(pooled, ddof=1) / np.sqrt(len(pooled)) / bm)
-        row["iterations"] = {"baseline": len(pooled), "emulated": mlp_iters}
-        for tag, *_ in modes:
-            row[f"emulated_{tag}_mean_us"] = float(np.mean(emus[tag]))
-            row[f"rel_err_{tag}"] = float(abs(np.mean(emus[tag]) - bm) / bm)
-    barrier()
+    reps_rows = [mlp_fidelity(k, rank, barrier, sizes, plugin, loaded, mlp_iters, footprint)
+                 for _ in range(max(1, mlp_repeats))]
+    row = reps_rows[0]
+    modes = ("table", "table_footprint", "loaded_footprint", "in_situ_footprint")
+    if rank == 0 and len(reps_rows) > 1:
+        # repeats: the error of the pooled means, and every repeat's own
+        bm = float(np.mean([r["baseline_mean_us"] for r in reps_rows]))
+        row = {"model": row["model"], "repeats": len(reps_rows), "baseline_mean_us": bm,
+               "footprint": row["footprint"],
+               "baseline_noise_2sem_rel": float(np.mean([r["baseline_noise_2sem_rel"] for r in reps_rows])
+                                                / np.sqrt(len(reps_rows))),
+               "compute_only_mean_us": float(np.mean([r["compute_only_mean_us"] for r in reps_rows]))}
+        for tag in modes:
+            em = float(np.mean([r[f"emulated_{tag}_mean_us"] for r in reps_rows]))
+            row[f"emulated_{tag}_mean_us"] = em
+            row[f"rel_err_{tag}"] = float(abs(em - bm) / bm)
+            row[f"rel_err_{tag}_per_repeat"] = [round(r[f"rel_err_{tag}"], 5) for r in reps_rows]
+        row["per_repeat"] = reps_rows
     res["mlp"] = row
     if rank == 0:
         spin_errs = {t: max(r[f"rel_err_{t}"] for r in res["e2e"]) for t in ("ab", "table")}
@@ -452,7 +476,7 @@ def run(sizes=None, reps=100, segments=3, e2e_iters=20, mlp_iters=100, footprint
                             "spin_models_max_rel_err_ab": spin_errs["ab"],
                             "spin_models_max_rel_err_table": spin_errs["table"],
                             "spin_models_pass_table": spin_errs["table"] < 0.01,
-                            "mlp_rel_err": {t: row[f"rel_err_{t}"] for t, *_ in modes}}
+                            "mlp_rel_err": {t: row[f"rel_err_{t}"] for t in modes}}
     return res
 
 
@@ -462,6 +486,7 @@ def main():
     ap.add_argument("--segments", type=int, default=3)
     ap.add_argument("--e2e-iters", type=int, default=20)
     ap.add_argument("--mlp-iters", type=int, default=100)
+    ap.add_argument("--mlp-repeats", type=int, default=3, help="repeats of the real-compute MLP check")
     ap.add_argument("--max-mib", type=int, default=256)
     ap.add_argument("--footprint-ctas", type=int, default=NCCL_FOOTPRINT[0], help="NCCL's channel count on this box")
     ap.add_argument("--footprint-smem", type=int, default=NCCL_FOOTPRINT[1], help="shared memory per NCCL CTA")
@@ -471,7 +496,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     sizes = [s for s in SIZES if s <= (args.max_mib << 20)]
     res = run(sizes, args.reps, args.segments, args.e2e_iters, args.mlp_iters,
-              (args.footprint_ctas, args.footprint_smem))
+              (args.footprint_ctas, args.footprint_smem), args.mlp_repeats)
     if dist.get_rank() == 0:
         print("FIDELITY " + json.dumps(res), flush=True)
     dist.barrier()
