@@ -773,7 +773,7 @@ def run_ours(args, rank, world_size, local_rank):
             from paper_2405_02969_b200 import fidelity
             try:
                 fid = fidelity.run([s for s in fidelity.SIZES if s <= (64 << 20)], reps=100, segments=1,
-                                   e2e_iters=10, mlp_iters=60)
+                                   e2e_iters=10, mlp_iters=60, mlp_repeats=3)
             except Exception as e:  # noqa: BLE001 -- reported in the line, never fatal to the bench
                 fid = {"error": repr(e)[:500]}
             if rank == 0:
