@@ -306,6 +306,18 @@ def ncu_traffic(buffer_bytes):
     return None
 
 
+def ncu_fused(k, buffer_bytes):
+    """The fused kernel's committed ncu counters at k real GPUs (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_fused.json")) as f:
+            d = json.load(f)
+        if int(d.get("buffer_bytes", -1)) == buffer_bytes:
+            return d["k"].get(str(k))
+    except (OSError, KeyError, ValueError):
+        pass
+    return None
+
+
 def ncu_field(name):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -695,8 +707,11 @@ def run_ours(args, rank, world_size, local_rank):
     else:
         achieved = 2 * nbytes / (ms_per_step * 1e-3) / 1e9
         fused = os.environ.get("CEMU_FUSED", "1") != "0"
+        ce_step = n == 2 and fused and os.environ.get("CEMU_CE", "2") != "0"
+        fc = ncu_fused(n, nbytes) if fused and not ce_step else None  # the step IS the fused kernel
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": None,
+                    "frac": round(achieved / peak, 4),
+                    "traffic": (fc["dram_bytes_read"] + fc["dram_bytes_write"]) if fc else None,
                     "kernel": (("peer_barrier_kernel x2 + fused_allreduce_vec<fp32> (fold-only) per chunk; "
                                 "peer pulls on the copy engines, peer stores from the SMs") if n == 2 and fused and
                                os.environ.get("CEMU_CE", "2") != "0" else
@@ -812,6 +827,13 @@ def run_ours(args, rank, world_size, local_rank):
                               "achieved_GBps": round(nv / (ms_per_step * 1e-3) / 1e9, 1),
                               "peer_peak_GBps": 770.0, "peak_source": "B200_PROFILING.md measured peer copy",
                               "frac": round(nv / (ms_per_step * 1e-3) / 1e9 / 770.0, 4)}
+            fcn = ncu_fused(n, nbytes)
+            if fcn:  # the fused kernel's committed NVLink counters (= 2(N-1)/N x buffer each way)
+                line["nvlink"]["ncu_fused_kernel_per_launch"] = {
+                    "nvlrx_bytes_data_user": fcn["nvlrx_bytes_data_user"],
+                    "nvltx_bytes_data_user": fcn["nvltx_bytes_data_user"], "duration_ms": fcn["duration_ms"],
+                    "source": "profiles/r02_ncu_fused (CEMU_CE=0: the fused kernel"
+                              + ("; this step runs the copy-engine pipeline)" if n == 2 else ")")}
         emit(line)
     comm.close()
     if n > 1:
