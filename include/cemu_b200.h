@@ -223,6 +223,12 @@ typedef struct {
                             was late even if the call ended on time */
   int64_t overshoot_ns;  /* max(0, t_end - (t_origin + max_j floor_j)): how
                             much longer than modelled the call itself took */
+  int64_t stall_ns;      /* the longest interval between two consecutive
+                            clock reads of the releasing thread: ~2-4 us (its
+                            sleep) normally; a pause of the whole device
+                            (nothing of the kernel running, ~1 ms about once
+                            a second on the measured boxes) shows here and
+                            bounds how late it made a release */
 } cemuCallRecord;
 
 /* Delay-model plugin: replaces DelayModelFn / make_delay_model

@@ -67,7 +67,7 @@ class CallRecord(C.Structure):
         ("steps", C.c_uint32), ("world", C.c_uint32), ("model_bytes", C.c_uint64),
         ("model_latency_us", C.c_int64), ("t_start_ns", C.c_int64), ("t_end_ns", C.c_int64),
         ("device_latency_us", C.c_int64), ("t_origin_ns", C.c_int64), ("late_ns", C.c_int64),
-        ("overshoot_ns", C.c_int64),
+        ("overshoot_ns", C.c_int64), ("stall_ns", C.c_int64),
     ]
 
 

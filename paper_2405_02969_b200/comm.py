@@ -372,6 +372,7 @@ class Communicator:
             "model_latency_us": rec.model_latency_us, "t_start_ns": rec.t_start_ns,
             "t_end_ns": rec.t_end_ns, "device_latency_us": rec.device_latency_us,
             "t_origin_ns": rec.t_origin_ns, "late_ns": rec.late_ns, "overshoot_ns": rec.overshoot_ns,
+            "stall_ns": rec.stall_ns,
             "floors_us": floors[:k].copy(), "release_ns": release[:k].copy(),
             "offsets_us": offsets[:k].copy(),
         }

@@ -1140,6 +1140,7 @@ cemuResult_t cemuCommCallRecord(cemuComm_t c, uint64_t id, cemuCallRecord* rec, 
   rec->t_origin_ns = h[4];
   rec->late_ns = h[5];
   rec->overshoot_ns = h[6];
+  rec->stall_ns = h[3];
   const size_t n = std::min<size_t>(cap, m.k);
   if (floors) std::memcpy(floors, h.data() + kSlotHeader, n * 8);
   if (release) std::memcpy(release, h.data() + kSlotHeader + c->kmax, n * 8);

@@ -1468,10 +1468,7 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
   }
   __syncthreads();
   const int64_t lat = run_max_floor(d.k, sgate, release);  // the last gate
-  if (threadIdx.x == 0) {
-    slot[2] = lat;
-    slot[3] = d.k;
-  }
+  if (threadIdx.x == 0) slot[2] = lat;
   // A step released after its floor is late: the emulator's own work (the
   // synthesis kernels before this one) outlasted that step's floor, or the
   // spin overshot.  The largest lateness is recorded (slot[5]), and how far
@@ -1495,12 +1492,18 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
   const int64_t t0 = t0_s;
   int64_t late = 0;
   int64_t t = globaltimer_ns();
+  // the longest interval between two consecutive clock reads: a few us
+  // (the sleep) normally; a pause of the whole device -- nothing of this
+  // kernel running -- shows here and explains a late release (slot[3])
+  int64_t prev = t, stall = 0;
   for (uint32_t j = 0; j < d.k;) {
     const int64_t target = t0 + floor_at(j) * 1000;
     if (t < target) {
       do {
         if (target - t > 8000) __nanosleep(2000);
         t = globaltimer_ns();
+        stall = max(stall, t - prev);
+        prev = t;
       } while (t < target);
     } else if (j + kSerialRun < d.k && t0 + gate(j + kSerialRun) * 1000 <= t) {
       uint32_t lo = j + kSerialRun + 1, hi = d.k;  // the first step whose gate is still ahead
@@ -1529,6 +1532,7 @@ __device__ __forceinline__ void delay_spin_body(const DelayLaunch& d, int64_t* s
   const int64_t end = globaltimer_ns();
   slot[6] = max(int64_t{0}, end - (t0 + lat * 1000));  // the call itself ran long by this much
   slot[1] = end;
+  slot[3] = max(stall, end - prev);
   for (uint32_t r = 0; r < nruns; ++r) {  // the runs' per-step times and lateness
     for (uint32_t i = run_b[r]; i < run_e[r]; ++i) {
       late = max(late, run_t[r] - (t0 + floor_at(i) * 1000));
