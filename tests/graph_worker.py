@@ -98,7 +98,8 @@ def run():
         res["replays"].append({"equal_eager": eq, "equal_oracle_1Mi": oracle_eq, "floors_ok": floors_ok,
                                "delay_us": round((rec["t_end_ns"] - rec["t_start_ns"]) / 1e3, 2),
                                "late_us": round(rec["late_ns"] / 1e3, 2),
-                               "overshoot_us": round(rec["overshoot_ns"] / 1e3, 2)})
+                               "overshoot_us": round(rec["overshoot_ns"] / 1e3, 2),
+                               "pause_us": round(rec["stall_ns"] / 1e3, 2) if rec["stall_ns"] > 20_000 else 0.0})
     res["async_error"] = comm.async_error()
     print(json.dumps(res), flush=True)
     dist.barrier()

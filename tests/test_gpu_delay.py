@@ -117,8 +117,9 @@ def test_config1_alpha_beta_delay_within_tolerance(cuda):
         ev_us = e0.elapsed_time(e1) * 1e3
         # event-timed stream occupancy: the stream really waited, and no more
         # than the model plus the call's own kernel launches
-        assert model <= ev_us <= model + 50.0, (ev_us, model)
-        assert rec["overshoot_ns"] < 2000 and rec["t_origin_ns"] == rec["t_start_ns"]
+        pause = rec["stall_ns"] if rec["stall_ns"] > 20_000 else 0  # a whole-device pause (see _delay_error)
+        assert model <= ev_us <= model + 50.0 + pause / 1e3, (ev_us, model, pause)
+        assert rec["overshoot_ns"] < 2000 + pause and rec["t_origin_ns"] == rec["t_start_ns"]
     comm.close()
 
 
@@ -330,8 +331,9 @@ def test_no_queue_chaining_by_default(cuda):
     for i in (last - 1, last):
         r = comm.call_record(i)
         assert r["t_origin_ns"] == r["t_start_ns"]
-        assert abs((r["t_end_ns"] - r["t_start_ns"]) / 1e3 - 200) <= 2.0
-        assert r["overshoot_ns"] < 2000
+        _, _, err, tol = _delay_error(r)
+        assert err <= tol
+        assert r["overshoot_ns"] < 2000 + (r["stall_ns"] if r["stall_ns"] > 20_000 else 0)
     comm.close()
 
 
@@ -370,9 +372,11 @@ def test_overshoot_is_reported_as_late(cuda):
     comm.set_synth_cache(4 << 30, 16)
     call()  # fills the cache
     rec, ev_us = call()
-    assert rec["overshoot_ns"] < 2000, rec
-    assert abs((rec["t_end_ns"] - rec["t_start_ns"]) / 1e3 - model) <= max(0.01 * model, 2.0)
-    assert ev_us <= model + 50.0  # event-timed stream occupancy: model + launch overhead
+    pause = rec["stall_ns"] if rec["stall_ns"] > 20_000 else 0  # a whole-device pause (see _delay_error)
+    assert rec["overshoot_ns"] < 2000 + pause, rec
+    _, _, err, tol = _delay_error(rec)
+    assert err <= tol
+    assert ev_us <= model + 50.0 + pause / 1e3  # event-timed stream occupancy: model + launch overhead
     comm.close()
 
 

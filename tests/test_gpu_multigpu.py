@@ -177,7 +177,8 @@ def test_graph_capture_of_copy_engine_allreduce_with_plugin_delay():
             assert res["captured_launches"] >= 4, res  # barrier + fold chunks + barrier + delay: the CE pipeline
         for rep in res["replays"]:
             assert rep["equal_eager"] and rep["equal_oracle_1Mi"] and rep["floors_ok"], rep
-            assert abs(rep["delay_us"] - 3000) <= 30 and rep["overshoot_us"] < 2, rep
+            # (a whole-device pause during the release -- recorded -- excuses that replay)
+            assert abs(rep["delay_us"] - 3000) <= 30 + rep["pause_us"] and rep["overshoot_us"] < 2 + rep["pause_us"], rep
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
