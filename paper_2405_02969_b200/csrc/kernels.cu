@@ -461,7 +461,7 @@ template <int K, int U, int kMode, bool kEnt = false>
 __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skeys, uint32_t nkeys,
                                           uint32_t one, uint32_t* r, const void* cache = nullptr,
                                           uint64_t j0 = 0, uint32_t* ent = nullptr,
-                                          const uint32_t* gkeys = nullptr) {
+                                          const uint32_t* gkeys = nullptr, uint64_t jlim = ~0ull) {
   using T = VT<K>;
   constexpr int NW = U * T::WPV;
   if constexpr (kMode == kCacheC16) {
@@ -474,7 +474,10 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         const uint64_t j = j0 + static_cast<uint64_t>(u) * kThreads * W + w;
-        c[u * W + w] = ld_stream64(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(cache) + 4 * j));
+        // words past the range (the last tile's idle vectors) are never read:
+        // the segment may end right before an unmapped page
+        c[u * W + w] = j < jlim ? ld_stream64(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(cache) + 4 * j))
+                                : make_uint2(0x80008000u, 0x80008000u);
       }
     }
 #pragma unroll
@@ -498,6 +501,7 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t jv = j0 + static_cast<uint64_t>(u) * kThreads * W;
+      if (jv >= jlim) continue;  // the last tile's idle vectors: nothing to read (nor store)
       if constexpr (T::kWords) {  // four words = four elements: one 16-byte entry
         const uint4 c = ld_stream(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(cache) + jv));
         r[u * 4 + 0] = c.x;
@@ -713,7 +717,7 @@ __global__ void __launch_bounds__(kThreads) synth_reduce_vec(
     // 3. fold + stream out
     uint32_t r[T::kWords ? NW : NW * 4];
     uint32_t ent[kFill ? (T::kWords ? NW : 2 * NW) : 1];
-    peer_sums<K, U, kMode, kFill>(ctr, skeys, nkeys, one, r, cache, j0, ent, keys);
+    peer_sums<K, U, kMode, kFill>(ctr, skeys, nkeys, one, r, cache, j0, ent, keys, word_base + nvec * W);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
@@ -1092,7 +1096,7 @@ __global__ void __launch_bounds__(kThreads) fused_allreduce_vec(const __grid_con
     uint32_t ctr[NW];
     if constexpr (!cached(kMode)) tile_ctrs<W, U>(j0, ctr);
     uint32_t r[T::kWords ? NW : NW * 4];
-    peer_sums<K, U, kMode>(ctr, skeys, a.nkeys, 1u, r, a.cache, j0, nullptr, a.keys);
+    peer_sums<K, U, kMode>(ctr, skeys, a.nkeys, 1u, r, a.cache, j0, nullptr, a.keys, a.word_base + a.v_end * W);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t v = base + static_cast<uint64_t>(u) * kThreads + threadIdx.x;
