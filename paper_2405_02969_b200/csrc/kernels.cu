@@ -473,11 +473,11 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
     for (int u = 0; u < U; ++u) {
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        const uint64_t j = j0 + static_cast<uint64_t>(u) * kThreads * W + w;
-        // words past the range (the last tile's idle vectors) are never read:
-        // the segment may end right before an unmapped page
-        c[u * W + w] = j < jlim ? ld_stream64(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(cache) + 4 * j))
-                                : make_uint2(0x80008000u, 0x80008000u);
+        // the last tile's idle vectors read the range's last word instead of
+        // words past it (the segment may end right before an unmapped page);
+        // their lanes are never stored
+        const uint64_t j = min(j0 + static_cast<uint64_t>(u) * kThreads * W, jlim - W) + w;
+        c[u * W + w] = ld_stream64(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(cache) + 4 * j));
       }
     }
 #pragma unroll
@@ -500,8 +500,10 @@ __device__ __forceinline__ void peer_sums(const uint32_t* ctr, const uint2* skey
     constexpr int W = T::WPV;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint64_t jv = j0 + static_cast<uint64_t>(u) * kThreads * W;
-      if (jv >= jlim) continue;  // the last tile's idle vectors: nothing to read (nor store)
+      // the last tile's idle vectors read the range's last vector's entries,
+      // not entries past the range (the segment may end right before an
+      // unmapped page); their lanes are never stored
+      const uint64_t jv = min(j0 + static_cast<uint64_t>(u) * kThreads * W, jlim - W);
       if constexpr (T::kWords) {  // four words = four elements: one 16-byte entry
         const uint4 c = ld_stream(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(cache) + jv));
         r[u * 4 + 0] = c.x;
